@@ -1,0 +1,500 @@
+/*
+ * TEST INFRASTRUCTURE ONLY -- CPU restatement of the reference stem executor.
+ *
+ * This is the parity oracle for the B200 executor: only tests/, the smoke()
+ * check of __graft_entry__.py and bench.py's cpu_baseline leg may load it, and
+ * only as the checker. The product path (libstn_exec.so) never calls it.
+ *
+ * It executes a flattened plan (include/stn_exec.h, stn_plan_desc) exactly as
+ * the reference `stemtn` runtime does, in the same loop order and with the
+ * same IEEE operations, so its results are bitwise identical to the reference
+ * (pinned against outputs of the reference itself: tests/golden/, produced by
+ * oracle/_ref/ref_tool from /root/reference):
+ *   load_leaf     runtime.hpp:367-384  (mixed-radix digits 371-378,
+ *                                        restrict_axis tensor.hpp:102-117,
+ *                                        from_tensor runtime.hpp:93-100)
+ *   permute       runtime.hpp:113-140  (odometer stride walk)
+ *   gemm          runtime.hpp:386-418  (D-batched C[d] += A[d] * B[d], loop m,k,n)
+ *   run           runtime.hpp:420-453  (live map, cache fetch, peak/mults bookkeeping)
+ *   branch cache  runtime.hpp:456-500  (branch steps once, keep consumed outputs)
+ *   run_scheme    runtime.hpp:555-605  (ascending-assignment double sum)
+ * Complex products are written out as (ar*br - ai*bi, ar*bi + ai*br), which is
+ * what GCC emits for std::complex multiplication of finite values; the file is
+ * compiled with -ffp-contract=off so no FMA changes the rounding.
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "stn_exec.h"
+
+static __thread char g_err[512];
+void stn_set_error_c(const char *msg) {
+  strncpy(g_err, msg, sizeof g_err - 1);
+  g_err[sizeof g_err - 1] = 0;
+}
+const char *oracle_last_error(void) { return g_err; }
+
+/* ---- typed tensors ------------------------------------------------------------ */
+typedef struct {
+  int rank;
+  int dims[64];
+  size_t n;
+  void *data; /* interleaved (re, im) of float or double */
+} tt_t;
+
+static size_t elsize(int prec) { return prec == STN_SINGLE ? 8 : 16; }
+
+static int tt_alloc(tt_t *t, int rank, const int *dims, int prec) {
+  t->rank = rank;
+  t->n = 1;
+  for (int i = 0; i < rank; ++i) {
+    t->dims[i] = dims[i];
+    t->n *= (size_t)dims[i];
+  }
+  t->data = calloc(t->n ? t->n : 1, elsize(prec));
+  return t->data != NULL;
+}
+static void tt_free(tt_t *t) {
+  free(t->data);
+  t->data = NULL;
+}
+static int tt_copy(tt_t *dst, const tt_t *src, int prec) {
+  if (!tt_alloc(dst, src->rank, src->dims, prec)) return 0;
+  memcpy(dst->data, src->data, src->n * elsize(prec));
+  return 1;
+}
+
+/* permute: result axis i is input axis perm[i] (runtime.hpp:113-140) */
+static int tt_permute(tt_t *out, const tt_t *t, const int32_t *perm, int prec) {
+  int r = t->rank;
+  int identity = 1;
+  for (int i = 0; i < r; ++i) identity &= (perm[i] == i);
+  if (r <= 1 || identity) return tt_copy(out, t, prec);
+  int od[64];
+  for (int i = 0; i < r; ++i) od[i] = t->dims[perm[i]];
+  if (!tt_alloc(out, r, od, prec)) return 0;
+  size_t in_strides[64], step[64];
+  int idx[64];
+  in_strides[r - 1] = 1;
+  for (int i = r - 2; i >= 0; --i) in_strides[i] = in_strides[i + 1] * (size_t)t->dims[i + 1];
+  for (int i = 0; i < r; ++i) {
+    step[i] = in_strides[perm[i]];
+    idx[i] = 0;
+  }
+  size_t es = elsize(prec), src = 0;
+  char *o = (char *)out->data;
+  const char *s = (const char *)t->data;
+  for (size_t flat = 0; flat < out->n; ++flat) {
+    memcpy(o + flat * es, s + src * es, es);
+    for (int ax = r - 1; ax >= 0; --ax) {
+      idx[ax]++;
+      src += step[ax];
+      if (idx[ax] < od[ax]) break;
+      src -= (size_t)od[ax] * step[ax];
+      idx[ax] = 0;
+    }
+  }
+  return 1;
+}
+
+/* ---- plan-side helpers -------------------------------------------------------- */
+typedef struct {
+  const stn_plan_desc *d;
+  int prec;
+  int *step_of_node; /* node -> step index or -1 */
+  int *leaf_of_node; /* node -> leaf index or -1 */
+} plan_t;
+
+static int plan_init(plan_t *p, const stn_plan_desc *d, int prec) {
+  p->d = d;
+  p->prec = prec;
+  p->step_of_node = (int *)malloc(sizeof(int) * (size_t)(d->n_nodes > 0 ? d->n_nodes : 1));
+  p->leaf_of_node = (int *)malloc(sizeof(int) * (size_t)(d->n_nodes > 0 ? d->n_nodes : 1));
+  if (!p->step_of_node || !p->leaf_of_node) return 0;
+  for (int i = 0; i < d->n_nodes; ++i) p->step_of_node[i] = p->leaf_of_node[i] = -1;
+  for (int i = 0; i < d->n_steps; ++i) {
+    if (d->steps[i].node < 0 || d->steps[i].node >= d->n_nodes) return 0;
+    p->step_of_node[d->steps[i].node] = i;
+  }
+  for (int i = 0; i < d->n_leaves; ++i) {
+    if (d->leaves[i].node < 0 || d->leaves[i].node >= d->n_nodes) return 0;
+    p->leaf_of_node[d->leaves[i].node] = i;
+  }
+  return 1;
+}
+static void plan_free(plan_t *p) {
+  free(p->step_of_node);
+  free(p->leaf_of_node);
+}
+
+/* mixed-radix digits, first sliced edge most significant (runtime.hpp:371-378) */
+int oracle_decode_assignment(const stn_plan_desc *d, uint64_t assignment, int32_t *digits) {
+  uint64_t rest = assignment;
+  for (int i = d->n_sliced; i-- > 0;) {
+    uint64_t dim = (uint64_t)d->sliced_dims[i];
+    digits[i] = (int32_t)(rest % dim);
+    rest /= dim;
+  }
+  return STN_OK;
+}
+
+/* load_leaf (runtime.hpp:367-384): restrict in double, cast to R, permute */
+static int load_leaf(const plan_t *p, int node, const int32_t *digits, tt_t *out) {
+  const stn_leaf_desc *l = &p->d->leaves[p->leaf_of_node[node]];
+  int rank = l->rank, dims[64];
+  size_t n = 1;
+  for (int i = 0; i < rank; ++i) {
+    dims[i] = l->dims[i];
+    n *= (size_t)dims[i];
+  }
+  double *cur = (double *)malloc(16 * (n ? n : 1));
+  if (!cur) return 0;
+  memcpy(cur, l->values, 16 * n);
+  for (int s = 0; s < l->n_sliced; ++s) { /* restrict_axis (tensor.hpp:102-117) */
+    int axis = l->sliced_axis[s], index = digits[l->sliced_index[s]];
+    size_t outer = 1, inner = 1, ax = (size_t)dims[axis];
+    for (int i = 0; i < axis; ++i) outer *= (size_t)dims[i];
+    for (int i = axis + 1; i < rank; ++i) inner *= (size_t)dims[i];
+    double *nx = (double *)malloc(16 * (outer * inner ? outer * inner : 1));
+    if (!nx) {
+      free(cur);
+      return 0;
+    }
+    for (size_t o = 0; o < outer; ++o)
+      for (size_t in = 0; in < inner; ++in)
+        memcpy(nx + 2 * (o * inner + in), cur + 2 * ((o * ax + (size_t)index) * inner + in), 16);
+    free(cur);
+    cur = nx;
+    for (int i = axis; i < rank - 1; ++i) dims[i] = dims[i + 1];
+    rank--;
+  }
+  tt_t typed;
+  if (!tt_alloc(&typed, rank, dims, p->prec)) {
+    free(cur);
+    return 0;
+  }
+  if (p->prec == STN_SINGLE) {
+    float *f = (float *)typed.data;
+    for (size_t i = 0; i < 2 * typed.n; ++i) f[i] = (float)cur[i];
+  } else {
+    memcpy(typed.data, cur, 16 * typed.n);
+  }
+  free(cur);
+  int ok = tt_permute(out, &typed, l->perm, p->prec);
+  tt_free(&typed);
+  return ok;
+}
+
+#define GEMM_LOOP(R)                                                               \
+  do {                                                                             \
+    const R *pa = (const R *)al.data, *pb = (const R *)bl.data;                    \
+    R *pc = (R *)c.data;                                                           \
+    for (size_t dd = 0; dd < D; ++dd) {                                            \
+      const R *ba = pa + 2 * dd * M * K;                                           \
+      const R *bb = pb + 2 * dd * K * N;                                           \
+      R *bc = pc + 2 * dd * M * N;                                                 \
+      for (size_t m = 0; m < M; ++m)                                               \
+        for (size_t k = 0; k < K; ++k) {                                           \
+          R ar = ba[2 * (m * K + k)], ai = ba[2 * (m * K + k) + 1];                \
+          const R *brow = bb + 2 * k * N;                                          \
+          R *crow = bc + 2 * m * N;                                                \
+          for (size_t nn = 0; nn < N; ++nn) {                                      \
+            R br = brow[2 * nn], bi = brow[2 * nn + 1];                            \
+            R re = ar * br - ai * bi;                                              \
+            R im = ar * bi + ai * br;                                              \
+            crow[2 * nn] += re;                                                    \
+            crow[2 * nn + 1] += im;                                                \
+          }                                                                        \
+        }                                                                          \
+    }                                                                              \
+  } while (0)
+
+/* gemm (runtime.hpp:386-418) */
+static int gemm(const plan_t *p, const stn_step_desc *s, const tt_t *a, const tt_t *b, tt_t *out) {
+  tt_t al, bl, c;
+  if (!tt_permute(&al, a, s->lperm, p->prec)) return 0;
+  if (!tt_permute(&bl, b, s->rperm, p->prec)) {
+    tt_free(&al);
+    return 0;
+  }
+  size_t D = (size_t)s->D, M = (size_t)s->M, N = (size_t)s->N, K = (size_t)s->K;
+  int produced[64];
+  for (int i = 0; i < s->orank; ++i) produced[s->operm[i]] = s->out_dims[i];
+  if (!tt_alloc(&c, s->orank, produced, p->prec) || c.n != D * M * N) {
+    tt_free(&al);
+    tt_free(&bl);
+    return 0;
+  }
+  if (p->prec == STN_SINGLE)
+    GEMM_LOOP(float);
+  else
+    GEMM_LOOP(double);
+  tt_free(&al);
+  tt_free(&bl);
+  int ok = tt_permute(out, &c, s->operm, p->prec);
+  tt_free(&c);
+  return ok;
+}
+
+/* ---- branch cache --------------------------------------------------------------- */
+typedef struct oracle_cache {
+  uint64_t identity, mults, elements;
+  int prec;
+  int n_nodes;
+  tt_t *node; /* kept outputs; data == NULL when absent */
+} oracle_cache;
+
+void oracle_cache_free(oracle_cache *c) {
+  if (!c) return;
+  for (int i = 0; i < c->n_nodes; ++i) tt_free(&c->node[i]);
+  free(c->node);
+  free(c);
+}
+
+/* build_cache_typed (runtime.hpp:456-488) */
+oracle_cache *oracle_cache_build(const stn_plan_desc *d, int prec) {
+  plan_t p;
+  if (!plan_init(&p, d, prec)) {
+    stn_set_error_c("oracle: malformed plan");
+    plan_free(&p);
+    return NULL;
+  }
+  oracle_cache *c = (oracle_cache *)calloc(1, sizeof *c);
+  tt_t *all = (tt_t *)calloc((size_t)d->n_nodes, sizeof(tt_t));
+  c->node = (tt_t *)calloc((size_t)d->n_nodes, sizeof(tt_t));
+  c->n_nodes = d->n_nodes;
+  c->prec = prec;
+  c->identity = d->identity;
+  int32_t zero[4096] = {0};
+  int ok = c && all && c->node && d->n_sliced <= 4096;
+  for (int i = 0; ok && i < d->n_steps; ++i) {
+    const stn_step_desc *s = &d->steps[i];
+    if (!s->is_branch) continue;
+    tt_t ops[2];
+    int ids[2] = {s->lhs, s->rhs};
+    for (int k = 0; ok && k < 2; ++k) {
+      if (all[ids[k]].data)
+        ok = tt_copy(&ops[k], &all[ids[k]], prec);
+      else
+        ok = p.leaf_of_node[ids[k]] >= 0 && load_leaf(&p, ids[k], zero, &ops[k]);
+    }
+    if (ok) ok = gemm(&p, s, &ops[0], &ops[1], &all[s->node]);
+    tt_free(&ops[0]);
+    tt_free(&ops[1]);
+    c->mults += s->mults;
+  }
+  /* keep only outputs consumed by non-branch steps, or the root */
+  char *needed = (char *)calloc((size_t)d->n_nodes, 1);
+  ok = ok && needed;
+  for (int i = 0; ok && i < d->n_steps; ++i)
+    if (!d->steps[i].is_branch) needed[d->steps[i].lhs] = needed[d->steps[i].rhs] = 1;
+  if (ok) needed[d->root] = 1;
+  for (int n = 0; ok && n < d->n_nodes; ++n) {
+    if (all[n].data && needed[n]) {
+      c->node[n] = all[n];
+      c->elements += all[n].n;
+      all[n].data = NULL;
+    }
+    tt_free(&all[n]);
+  }
+  free(needed);
+  free(all);
+  plan_free(&p);
+  if (!ok) {
+    stn_set_error_c("oracle: cache build failed");
+    oracle_cache_free(c);
+    return NULL;
+  }
+  return c;
+}
+
+int oracle_cache_info(const oracle_cache *c, uint64_t *identity, uint64_t *mults,
+                      uint64_t *elements) {
+  if (identity) *identity = c->identity;
+  if (mults) *mults = c->mults;
+  if (elements) *elements = c->elements;
+  return STN_OK;
+}
+
+/* ---- one subtask (Engine::run, runtime.hpp:420-453) ---------------------------- */
+int oracle_run_subtask_digits(const stn_plan_desc *d, int prec, const int32_t *digits,
+                              const oracle_cache *cache, double *out, int64_t out_cap,
+                              stn_subtask_info *info) {
+  if (cache && cache->identity != d->identity) {
+    stn_set_error_c("SubtaskFailure: branch cache belongs to a different plan");
+    return STN_ERR_SUBTASK_FAILURE;
+  }
+  if (cache && cache->prec != prec) {
+    stn_set_error_c("SubtaskFailure: branch cache precision mismatch");
+    return STN_ERR_SUBTASK_FAILURE;
+  }
+  plan_t p;
+  if (!plan_init(&p, d, prec)) {
+    plan_free(&p);
+    stn_set_error_c("oracle: malformed plan");
+    return STN_ERR_MALFORMED_NETWORK;
+  }
+  tt_t *live = (tt_t *)calloc((size_t)d->n_nodes, sizeof(tt_t));
+  int ok = live != NULL, status = STN_OK;
+  int step_count = 0;
+  uint64_t mults = 0, peak = 0;
+  /* fetch: live (move), cache (copy), leaf */
+#define FETCH(nid, dst)                                                               \
+  do {                                                                                 \
+    if (live[nid].data) {                                                             \
+      dst = live[nid];                                                                \
+      live[nid].data = NULL;                                                          \
+    } else if (cache && cache->node[nid].data) {                                      \
+      ok = tt_copy(&dst, &cache->node[nid], prec);                                    \
+    } else if (p.leaf_of_node[nid] >= 0) {                                            \
+      ok = load_leaf(&p, nid, digits, &dst);                                          \
+    } else {                                                                           \
+      ok = 0;                                                                          \
+      status = STN_ERR_SUBTASK_FAILURE;                                                \
+      stn_set_error_c("SubtaskFailure: operand unavailable");                          \
+    }                                                                                  \
+  } while (0)
+  for (int i = 0; ok && i < d->n_steps; ++i) {
+    const stn_step_desc *s = &d->steps[i];
+    if (cache && s->is_branch) continue;
+    tt_t a = {0}, b = {0};
+    FETCH(s->lhs, a);
+    if (ok) FETCH(s->rhs, b);
+    if (ok) ok = gemm(&p, s, &a, &b, &live[s->node]);
+    tt_free(&a);
+    tt_free(&b);
+    if (!ok) break;
+    step_count++;
+    mults += s->mults;
+    if (live[s->node].n > peak) peak = live[s->node].n;
+  }
+  tt_t result = {0};
+  if (ok) FETCH(d->root, result);
+  if (ok && (int64_t)result.n > out_cap) {
+    ok = 0;
+    status = STN_ERR_INVALID_ARGUMENT;
+    stn_set_error_c("oracle: output buffer too small");
+  }
+  if (ok) {
+    if (prec == STN_SINGLE) {
+      const float *f = (const float *)result.data;
+      for (size_t j = 0; j < 2 * result.n; ++j) out[j] = (double)f[j];
+    } else {
+      memcpy(out, result.data, 16 * result.n);
+    }
+    if (info) {
+      info->step_count = step_count;
+      info->mults = mults;
+      info->peak_elements = peak;
+    }
+  }
+  tt_free(&result);
+  for (int n = 0; live && n < d->n_nodes; ++n) tt_free(&live[n]);
+  free(live);
+  plan_free(&p);
+#undef FETCH
+  if (!ok && status == STN_OK) {
+    status = STN_ERR_OUT_OF_MEMORY;
+    stn_set_error_c("oracle: allocation or shape failure");
+  }
+  return status;
+}
+
+int oracle_run_subtask(const stn_plan_desc *d, int prec, uint64_t assignment,
+                       const oracle_cache *cache, double *out, int64_t out_cap,
+                       stn_subtask_info *info) {
+  if (assignment >= d->subtasks) {
+    stn_set_error_c("SubtaskFailure: assignment out of range");
+    return STN_ERR_SUBTASK_FAILURE;
+  }
+  int32_t *digits = (int32_t *)calloc((size_t)(d->n_sliced ? d->n_sliced : 1), 4);
+  if (!digits) return STN_ERR_OUT_OF_MEMORY;
+  oracle_decode_assignment(d, assignment, digits);
+  int st = oracle_run_subtask_digits(d, prec, digits, cache, out, out_cap, info);
+  if (info) info->assignment = assignment;
+  free(digits);
+  return st;
+}
+
+/* ---- run_scheme: threads over slices, ascending double sum (runtime.hpp:555-605) ---- */
+typedef struct {
+  const stn_plan_desc *d;
+  int prec;
+  const oracle_cache *cache;
+  uint64_t lo, hi;
+  int64_t out_elems;
+  double *values; /* [(hi-lo)][2*out_elems] */
+  volatile uint64_t next;
+  pthread_mutex_t mu;
+  int status;
+} scheme_job;
+
+static void *scheme_worker(void *arg) {
+  scheme_job *j = (scheme_job *)arg;
+  for (;;) {
+    pthread_mutex_lock(&j->mu);
+    uint64_t a = j->next++;
+    int failed = j->status != STN_OK;
+    pthread_mutex_unlock(&j->mu);
+    if (a >= j->hi - j->lo || failed) return NULL;
+    int st = oracle_run_subtask(j->d, j->prec, j->lo + a, j->cache,
+                                j->values + 2 * (size_t)j->out_elems * a, j->out_elems, NULL);
+    if (st != STN_OK) {
+      pthread_mutex_lock(&j->mu);
+      j->status = st;
+      pthread_mutex_unlock(&j->mu);
+      return NULL;
+    }
+  }
+}
+
+/* Runs slices [lo, hi) on `threads` host threads with a shared cache. values
+ * (optional) receives every per-slice result; sum (optional) the ascending
+ * double sum. */
+int oracle_run_slices(const stn_plan_desc *d, int prec, const oracle_cache *cache, uint64_t lo,
+                      uint64_t hi, int threads, int64_t out_elems, double *values, double *sum) {
+  if (hi < lo || threads < 1) return STN_ERR_INVALID_ARGUMENT;
+  uint64_t n = hi - lo;
+  double *vals = values ? values : (double *)calloc(2 * (size_t)out_elems * (n ? n : 1), 8);
+  if (!vals) return STN_ERR_OUT_OF_MEMORY;
+  scheme_job j;
+  j.d = d, j.prec = prec, j.cache = cache, j.lo = lo, j.hi = hi, j.out_elems = out_elems;
+  j.values = vals, j.next = 0, j.status = STN_OK;
+  pthread_mutex_init(&j.mu, NULL);
+  pthread_t *th = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
+  int started = 0;
+  for (int t = 1; th && t < threads; ++t)
+    if (pthread_create(&th[started], NULL, scheme_worker, &j) == 0) started++;
+  scheme_worker(&j);
+  for (int t = 0; t < started; ++t) pthread_join(th[t], NULL);
+  free(th);
+  pthread_mutex_destroy(&j.mu);
+  if (j.status == STN_OK && sum) {
+    for (int64_t i = 0; i < 2 * out_elems; ++i) sum[i] = 0.0;
+    for (uint64_t a = 0; a < n; ++a)
+      for (int64_t i = 0; i < 2 * out_elems; ++i) sum[i] += vals[2 * (size_t)out_elems * a + i];
+  }
+  if (!values) free(vals);
+  return j.status;
+}
+
+/* Root tensor size of a plan (product of the root's canonical dims). */
+int64_t oracle_out_elements(const stn_plan_desc *d) {
+  for (int i = 0; i < d->n_steps; ++i)
+    if (d->steps[i].node == d->root) {
+      int64_t n = 1;
+      for (int k = 0; k < d->steps[i].orank; ++k) n *= d->steps[i].out_dims[k];
+      return n;
+    }
+  for (int i = 0; i < d->n_leaves; ++i)
+    if (d->leaves[i].node == d->root) {
+      int64_t n = 1;
+      for (int k = 0; k < d->leaves[i].rank; ++k) n *= d->leaves[i].dims[k];
+      for (int k = 0; k < d->leaves[i].n_sliced; ++k) n /= d->leaves[i].dims[d->leaves[i].sliced_axis[k]];
+      return n;
+    }
+  return -1;
+}
