@@ -184,6 +184,30 @@ typedef struct stn_plan_info {
   int32_t steps_generic;         /* per-slice steps on the generic SIMT kernel */
 } stn_plan_info;
 
+/* Per-kernel-class timing of the launches made while profiling is on (CUDA
+ * events around every launch, on the launch stream). `bytes` and `flops` are
+ * ALGORITHMIC: operand reads + result writes of the contraction (slice-
+ * invariant operands counted once per batch) and 8 real flops per complex
+ * multiply-add (runtime.hpp:330 `mults`). */
+typedef enum stn_kernel_kind {
+  STN_KERNEL_GENERIC = 0,   /* strided SIMT contraction (any dims, D batches) */
+  STN_KERNEL_ABSORB = 1,    /* bond-2 bandwidth absorb (big stem x small branch) */
+  STN_KERNEL_GEMM_SIMT = 2, /* tiled SIMT complex GEMM */
+  STN_KERNEL_GEMM_TC = 3,   /* tcgen05 split-TF32 complex GEMM */
+  STN_KERNEL_PERMUTE = 4,   /* operand/result axis permutation */
+  STN_KERNEL_LEAF = 5,      /* per-slice leaf gather */
+  STN_KERNEL_ROOT = 6,      /* ordered fp64 root accumulation */
+  STN_KERNEL_KINDS = 7
+} stn_kernel_kind;
+
+typedef struct stn_kernel_profile {
+  int32_t kind;     /* stn_kernel_kind */
+  int32_t launches;
+  double ms;        /* summed device time of the launches */
+  double bytes;     /* summed algorithmic bytes */
+  double flops;     /* summed algorithmic flops */
+} stn_kernel_profile;
+
 /* ---- library ---------------------------------------------------------------- */
 const char *stn_version(void);
 int stn_abi_version(void);
@@ -213,6 +237,13 @@ int stn_plan_set_leaf_values(stn_plan *plan, int32_t vertex, const double *value
                              int64_t n_complex);
 /* Upper bound on slices executed together in one batched pass (0 = automatic). */
 int stn_plan_set_max_batch(stn_plan *plan, int32_t max_batch);
+
+/* Turns per-launch event timing on/off (off by default) and reads the totals
+ * accumulated since the last reset; out must hold STN_KERNEL_KINDS entries.
+ * Reading synchronizes on the recorded events. */
+int stn_plan_set_profiling(stn_plan *plan, int enable);
+int stn_plan_get_profile(stn_plan *plan, stn_kernel_profile *out);
+int stn_plan_reset_profile(stn_plan *plan);
 
 /* ---- branch cache ------------------------------------------------------------ */
 int stn_cache_build(stn_plan *plan, void *stream, stn_cache **out);

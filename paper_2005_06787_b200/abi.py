@@ -101,6 +101,14 @@ class PlanInfo(C.Structure):
     ]
 
 
+KERNEL_KINDS = ["generic", "absorb", "gemm_simt", "gemm_tc", "permute", "leaf", "root"]
+
+
+class KernelProfile(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("launches", C.c_int32), ("ms", C.c_double),
+                ("bytes", C.c_double), ("flops", C.c_double)]
+
+
 # Every symbol include/stn_exec.h declares, with its ctypes signature.
 _P = C.c_void_p
 _PP = C.POINTER(C.c_void_p)
@@ -117,6 +125,9 @@ SIGNATURES = {
     "stn_plan_get_info": (C.c_int, [_P, C.POINTER(PlanInfo)]),
     "stn_plan_set_leaf_values": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_double), C.c_int64]),
     "stn_plan_set_max_batch": (C.c_int, [_P, C.c_int32]),
+    "stn_plan_set_profiling": (C.c_int, [_P, C.c_int]),
+    "stn_plan_get_profile": (C.c_int, [_P, C.POINTER(KernelProfile)]),
+    "stn_plan_reset_profile": (C.c_int, [_P]),
     "stn_cache_build": (C.c_int, [_P, _P, _PP]),
     "stn_cache_destroy": (C.c_int, [_P]),
     "stn_cache_info": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),

@@ -1,0 +1,523 @@
+// SIMT kernels of the B200 stem executor (sm_100a).
+//
+// Arithmetic modes:
+//   exact  - every complex product is (ar*br - ai*bi, ar*bi + ai*br) with
+//            separately rounded IEEE operations (__fmul_rn/__fadd_rn never
+//            contract into FMA) and every output sums its K terms in ascending
+//            k order starting from zero. That is the reference loop
+//            (runtime.hpp:396-407) operation for operation, so results are
+//            bitwise identical to the reference CPU executor.
+//   fast   - the same order with fused multiply-adds.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+
+namespace stn {
+
+namespace {
+
+template <class R>
+struct Cx;
+template <>
+struct Cx<float> {
+  using T = float2;
+};
+template <>
+struct Cx<double> {
+  using T = double2;
+};
+template <class R>
+using cx_t = typename Cx<R>::T;
+
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+// acc += a * b
+template <bool EXACT, class T>
+__device__ __forceinline__ void cmac(T &acc, const T a, const T b) {
+  if constexpr (EXACT) {
+    auto re = sub_rn(mul_rn(a.x, b.x), mul_rn(a.y, b.y));
+    auto im = add_rn(mul_rn(a.x, b.y), mul_rn(a.y, b.x));
+    acc.x = add_rn(acc.x, re);
+    acc.y = add_rn(acc.y, im);
+  } else {
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(-a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y);
+    acc.y = fma(a.y, b.x, acc.y);
+  }
+}
+
+inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 16) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b > max_blocks) b = max_blocks;
+  if (b < 1) b = 1;
+  return int(b);
+}
+
+// ---------------------------------------------------------------------------
+// Generic strided contraction. One thread per output element (grid-stride);
+// the K sum runs over an odometer in ascending k. POW2: every (merged) dim is a
+// power of two and indices decompose with shifts (all circuit networks).
+// ---------------------------------------------------------------------------
+template <class R, bool EXACT, bool POW2>
+__global__ void __launch_bounds__(256)
+    k_generic(const __grid_constant__ StridedGeom g, const BatchPtrs p) {
+  using T = cx_t<R>;
+  const int b = blockIdx.y;
+  const T *A = static_cast<const T *>(p.a) + int64_t(b) * p.a_bs;
+  const T *B = static_cast<const T *>(p.b) + int64_t(b) * p.b_bs;
+  T *O = static_cast<T *>(p.out) + int64_t(b) * p.out_bs;
+  const int last = g.n_k - 1;
+  const int64_t kd_last = last >= 0 ? g.k_dim[last] : 1;
+  const int64_t ka_last = last >= 0 ? g.k_sa[last] : 0;
+  const int64_t kb_last = last >= 0 ? g.k_sb[last] : 0;
+  const int64_t k_outer = g.k_size / kd_last;
+  for (int64_t o = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; o < g.out_size;
+       o += int64_t(gridDim.x) * blockDim.x) {
+    int64_t rem = o, ao = 0, bo = 0;
+    for (int i = g.n_out - 1; i >= 0; --i) {
+      int64_t idx;
+      if constexpr (POW2) {
+        const int sh = __ffsll(g.out_dim[i]) - 1;
+        idx = rem & (g.out_dim[i] - 1);
+        rem >>= sh;
+      } else {
+        idx = rem % g.out_dim[i];
+        rem /= g.out_dim[i];
+      }
+      ao += idx * g.out_sa[i];
+      bo += idx * g.out_sb[i];
+    }
+    T acc;
+    acc.x = 0;
+    acc.y = 0;
+    for (int64_t ko = 0; ko < k_outer; ++ko) {
+      int64_t r2 = ko, ka = ao, kb = bo;
+      for (int i = last - 1; i >= 0; --i) {
+        int64_t idx;
+        if constexpr (POW2) {
+          const int sh = __ffsll(g.k_dim[i]) - 1;
+          idx = r2 & (g.k_dim[i] - 1);
+          r2 >>= sh;
+        } else {
+          idx = r2 % g.k_dim[i];
+          r2 /= g.k_dim[i];
+        }
+        ka += idx * g.k_sa[i];
+        kb += idx * g.k_sb[i];
+      }
+      for (int64_t kk = 0; kk < kd_last; ++kk) {
+        cmac<EXACT>(acc, A[ka], B[kb]);
+        ka += ka_last;
+        kb += kb_last;
+      }
+    }
+    O[o] = acc;
+  }
+}
+
+// out[o] = in[a_off(o)] : axis permutation (the reference's permute,
+// runtime.hpp:113-140, as a gather over the output index).
+template <class R, bool POW2>
+__global__ void __launch_bounds__(256)
+    k_permute(const __grid_constant__ StridedGeom g, const void *in_, void *out_, int64_t in_bs,
+              int64_t out_bs) {
+  using T = cx_t<R>;
+  const int b = blockIdx.y;
+  const T *in = static_cast<const T *>(in_) + int64_t(b) * in_bs;
+  T *out = static_cast<T *>(out_) + int64_t(b) * out_bs;
+  for (int64_t o = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; o < g.out_size;
+       o += int64_t(gridDim.x) * blockDim.x) {
+    int64_t rem = o, ao = 0;
+    for (int i = g.n_out - 1; i >= 0; --i) {
+      int64_t idx;
+      if constexpr (POW2) {
+        const int sh = __ffsll(g.out_dim[i]) - 1;
+        idx = rem & (g.out_dim[i] - 1);
+        rem >>= sh;
+      } else {
+        idx = rem % g.out_dim[i];
+        rem /= g.out_dim[i];
+      }
+      ao += idx * g.out_sa[i];
+    }
+    out[o] = in[ao];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Bond-2 absorb: stream the big operand X once through shared memory.
+//   load : X tile (tile M bits x all K bits) -> xs, 16-byte coalesced runs
+//   math : O[t, n] = sum_k xs[t, k] * W[k, n], k ascending, W from smem
+//   store: O tile (tile M bits x all N bits) -> global, 16-byte coalesced runs
+// One CTA per assignment of the outer M bits (and per slice in the batch).
+// ---------------------------------------------------------------------------
+constexpr int kAbsorbThreads = 256;
+
+template <bool EXACT, int NC>
+__global__ void __launch_bounds__(kAbsorbThreads)
+    k_absorb(const __grid_constant__ AbsorbGeom g, const BatchPtrs p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int b = blockIdx.y;
+  const float2 *X = static_cast<const float2 *>(p.a) + int64_t(b) * p.a_bs;
+  const float2 *W = static_cast<const float2 *>(p.b) + int64_t(b) * p.b_bs;
+  float2 *O = static_cast<float2 *>(p.out) + int64_t(b) * p.out_bs;
+
+  const int xt = g.xt_bits, ot = g.ot_bits;
+  const int K = 1 << g.kb, N = 1 << g.nb;
+  const int x_hi_n = 1 << (xt - g.x_run), o_hi_n = 1 << (ot - g.o_run);
+  float2 *xs = reinterpret_cast<float2 *>(smem_raw);
+  float2 *os = xs + (1 << xt);
+  float2 *ws = os + (1 << ot);                              // [k][n]
+  int64_t *xhi = reinterpret_cast<int64_t *>(ws + K * N);   // X offset of high tile bits
+  int64_t *ohi = xhi + x_hi_n;                              // O offset of high tile bits
+  int *xk = reinterpret_cast<int *>(ohi + o_hi_n);          // tile-local X offset of k
+  int *on = xk + K;                                         // tile-local O offset of n
+
+  // base offsets of this CTA's outer M bits
+  const uint64_t outer = blockIdx.x;
+  int64_t base_x = 0, base_o = 0;
+  for (int j = 0; j < g.ob; ++j)
+    if ((outer >> j) & 1) {
+      base_x += int64_t(1) << g.outer_x[j];
+      base_o += int64_t(1) << g.outer_o[j];
+    }
+
+  const int tid = threadIdx.x;
+  for (int i = tid; i < x_hi_n; i += kAbsorbThreads) {
+    int64_t off = 0;
+    for (int l = g.x_run; l < xt; ++l)
+      if ((i >> (l - g.x_run)) & 1) off += int64_t(1) << g.x_tile_pos[l];
+    xhi[i] = off;
+  }
+  for (int i = tid; i < o_hi_n; i += kAbsorbThreads) {
+    int64_t off = 0;
+    for (int l = g.o_run; l < ot; ++l)
+      if ((i >> (l - g.o_run)) & 1) off += int64_t(1) << g.o_tile_pos[l];
+    ohi[i] = off;
+  }
+  for (int k = tid; k < K; k += kAbsorbThreads) {
+    int off = 0;
+    for (int j = 0; j < g.kb; ++j)
+      if ((k >> j) & 1) off |= 1 << g.k_xl[j];
+    xk[k] = off;
+  }
+  for (int n = tid; n < N; n += kAbsorbThreads) {
+    int off = 0;
+    for (int j = 0; j < g.nb; ++j)
+      if ((n >> j) & 1) off |= 1 << g.n_ol[j];
+    on[n] = off;
+  }
+  for (int i = tid; i < K * N; i += kAbsorbThreads) {
+    const int k = i / N, n = i % N;
+    int64_t off = 0;
+    for (int j = 0; j < g.kb; ++j)
+      if ((k >> j) & 1) off += g.w_k_stride[j];
+    for (int j = 0; j < g.nb; ++j)
+      if ((n >> j) & 1) off += g.w_n_stride[j];
+    ws[i] = W[off];
+  }
+  __syncthreads();
+
+  // load the X tile: pairs of consecutive elements (x_run >= 1)
+  {
+    const int run_mask = (1 << g.x_run) - 1;
+    const int pairs = 1 << (xt - 1);
+    for (int q = tid; q < pairs; q += kAbsorbThreads) {
+      const int i = q << 1;
+      const int64_t src = base_x + xhi[i >> g.x_run] + (i & run_mask);
+      const float4 v = __ldg(reinterpret_cast<const float4 *>(X + src));
+      reinterpret_cast<float4 *>(xs)[q] = v;
+    }
+  }
+  __syncthreads();
+
+  // math: each thread owns tile rows t; NC outputs per pass over K
+  const int T = 1 << g.tb;
+  for (int t = tid; t < T; t += kAbsorbThreads) {
+    int xo = 0, oo = 0;
+    for (int j = 0; j < g.tb; ++j)
+      if ((t >> j) & 1) {
+        xo |= 1 << g.t_xl[j];
+        oo |= 1 << g.t_ol[j];
+      }
+    for (int n0 = 0; n0 < N; n0 += NC) {
+      float2 acc[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) acc[c] = make_float2(0.f, 0.f);
+      for (int k = 0; k < K; ++k) {
+        const float2 x = xs[xo | xk[k]];
+        const float2 *wr = ws + k * N + n0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          if (n0 + c < N) cmac<EXACT>(acc[c], x, wr[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        if (n0 + c < N) os[oo | on[n0 + c]] = acc[c];
+    }
+  }
+  __syncthreads();
+
+  // store the O tile
+  {
+    const int run_mask = (1 << g.o_run) - 1;
+    const int pairs = 1 << (ot - 1);
+    for (int q = tid; q < pairs; q += kAbsorbThreads) {
+      const int i = q << 1;
+      const int64_t dst = base_o + ohi[i >> g.o_run] + (i & run_mask);
+      reinterpret_cast<float4 *>(O + dst)[0] = reinterpret_cast<const float4 *>(os)[q];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tiled SIMT complex GEMM, C[d] = A[d] (MxK, row-major) * B[d] (KxN, row-major).
+// 64x64 output tile per CTA, 16-wide K steps, 4x4 outputs per thread; every
+// output accumulates k in ascending order.
+// ---------------------------------------------------------------------------
+template <class R, bool EXACT>
+__global__ void __launch_bounds__(256)
+    k_gemm_simt(const GemmShape s, const BatchPtrs p) {
+  using T = cx_t<R>;
+  constexpr int BM = 64, BN = 64, BK = 16;
+  __shared__ T As[BK][BM + 1];
+  __shared__ T Bs[BK][BN + 1];
+  const int64_t batch = blockIdx.z;  // = slice * D + d
+  const int64_t slice = batch / s.D, d = batch % s.D;
+  const T *A = static_cast<const T *>(p.a) + slice * p.a_bs + d * s.M * s.K;
+  const T *B = static_cast<const T *>(p.b) + slice * p.b_bs + d * s.K * s.N;
+  T *C = static_cast<T *>(p.out) + slice * p.out_bs + d * s.M * s.N;
+  const int64_t m0 = int64_t(blockIdx.y) * BM, n0 = int64_t(blockIdx.x) * BN;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  T acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j].x = acc[i][j].y = 0;
+  for (int64_t k0 = 0; k0 < s.K; k0 += BK) {
+    for (int e = threadIdx.x; e < BM * BK; e += 256) {
+      const int mm = e / BK, kk = e % BK;
+      const int64_t gm = m0 + mm, gk = k0 + kk;
+      T v;
+      v.x = v.y = 0;
+      if (gm < s.M && gk < s.K) v = A[gm * s.K + gk];
+      As[kk][mm] = v;
+    }
+    for (int e = threadIdx.x; e < BK * BN; e += 256) {
+      const int kk = e / BN, nn = e % BN;
+      const int64_t gk = k0 + kk, gn = n0 + nn;
+      T v;
+      v.x = v.y = 0;
+      if (gk < s.K && gn < s.N) v = B[gk * s.N + gn];
+      Bs[kk][nn] = v;
+    }
+    __syncthreads();
+    const int kmax = int(s.K - k0 < BK ? s.K - k0 : BK);
+    for (int kk = 0; kk < kmax; ++kk) {
+      T a[4], bb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bb[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cmac<EXACT>(acc[i][j], a[i], bb[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t gm = m0 + ty * 4 + i, gn = n0 + tx + 16 * j;
+      if (gm < s.M && gn < s.N) C[gm * s.N + gn] = acc[i][j];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Per-slice leaf preparation (runtime.hpp:367-384): digit restriction, cast,
+// canonical layout, for every sliced leaf and every slice of the batch.
+// ---------------------------------------------------------------------------
+template <class R>
+__global__ void k_leaf_gather(const LeafGatherTable t, void *arena_, const int32_t *digits,
+                              int nbatch) {
+  using T = cx_t<R>;
+  T *arena = static_cast<T *>(arena_);
+  const int64_t total = t.total_out * nbatch;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int b = int(i / t.total_out);
+    const int64_t e = i % t.total_out;
+    const int leaf = t.elem_leaf[e];
+    int64_t src = t.src_base[e];
+    for (int a = t.ax_begin[leaf]; a < t.ax_begin[leaf + 1]; ++a)
+      src += t.ax_stride[a] * digits[int64_t(b) * t.n_sliced + t.ax_slice[a]];
+    T v;
+    v.x = R(t.values[2 * src]);
+    v.y = R(t.values[2 * src + 1]);
+    arena[t.dst_off[leaf] * nbatch + int64_t(b) * t.dst_bs[leaf] + t.elem_local[e]] = v;
+  }
+}
+
+// Root of each slice -> double; optional per-slice copy; ascending-order
+// accumulation over the batch (runtime.hpp:601-605).
+template <class R>
+__global__ void k_root_accumulate(const void *root_, int64_t root_bs, int64_t n, int nbatch,
+                                  double *acc, double *per_slice) {
+  using T = cx_t<R>;
+  const T *root = static_cast<const T *>(root_);
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    double sr = acc ? acc[2 * i] : 0.0, si = acc ? acc[2 * i + 1] : 0.0;
+    for (int b = 0; b < nbatch; ++b) {
+      const T v = root[int64_t(b) * root_bs + i];
+      const double vr = double(v.x), vi = double(v.y);
+      if (per_slice) {
+        per_slice[2 * (int64_t(b) * n + i)] = vr;
+        per_slice[2 * (int64_t(b) * n + i) + 1] = vi;
+      }
+      sr = __dadd_rn(sr, vr);
+      si = __dadd_rn(si, vi);
+    }
+    if (acc) {
+      acc[2 * i] = sr;
+      acc[2 * i + 1] = si;
+    }
+  }
+}
+
+__global__ void k_sum_ordered(const double *per_slice, uint64_t n_slices, int64_t n, double *out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < 2 * n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (uint64_t a = 0; a < n_slices; ++a) s = __dadd_rn(s, per_slice[a * 2 * n + i]);
+    out[i] = s;
+  }
+}
+
+bool all_pow2(const StridedGeom &g) {
+  for (int i = 0; i < g.n_out; ++i)
+    if (g.out_dim[i] & (g.out_dim[i] - 1)) return false;
+  for (int i = 0; i < g.n_k; ++i)
+    if (g.k_dim[i] & (g.k_dim[i] - 1)) return false;
+  return true;
+}
+
+}  // namespace
+
+template <class R>
+cudaError_t launch_generic(const StridedGeom &g, const BatchPtrs &p, bool exact,
+                           cudaStream_t stream) {
+  if (g.out_size == 0 || p.nbatch == 0) return cudaSuccess;
+  dim3 grid(grid_for(g.out_size, 256), p.nbatch);
+  const bool pow2 = all_pow2(g);
+  if (exact) {
+    if (pow2)
+      k_generic<R, true, true><<<grid, 256, 0, stream>>>(g, p);
+    else
+      k_generic<R, true, false><<<grid, 256, 0, stream>>>(g, p);
+  } else {
+    if (pow2)
+      k_generic<R, false, true><<<grid, 256, 0, stream>>>(g, p);
+    else
+      k_generic<R, false, false><<<grid, 256, 0, stream>>>(g, p);
+  }
+  return cudaGetLastError();
+}
+
+template <class R>
+cudaError_t launch_permute(const StridedGeom &g, const void *in, void *out, int64_t in_bs,
+                           int64_t out_bs, int nbatch, cudaStream_t stream) {
+  if (g.out_size == 0 || nbatch == 0) return cudaSuccess;
+  dim3 grid(grid_for(g.out_size, 256), nbatch);
+  if (all_pow2(g))
+    k_permute<R, true><<<grid, 256, 0, stream>>>(g, in, out, in_bs, out_bs);
+  else
+    k_permute<R, false><<<grid, 256, 0, stream>>>(g, in, out, in_bs, out_bs);
+  return cudaGetLastError();
+}
+
+size_t absorb_smem_bytes(const AbsorbGeom &g) {
+  const size_t K = size_t(1) << g.kb, N = size_t(1) << g.nb;
+  return 8 * ((size_t(1) << g.xt_bits) + (size_t(1) << g.ot_bits) + K * N) +
+         8 * ((size_t(1) << (g.xt_bits - g.x_run)) + (size_t(1) << (g.ot_bits - g.o_run))) +
+         4 * (K + N);
+}
+
+cudaError_t launch_absorb(const AbsorbGeom &g, const BatchPtrs &p, bool exact,
+                          cudaStream_t stream) {
+  const size_t smem = absorb_smem_bytes(g);
+  dim3 grid(unsigned(uint64_t(1) << g.ob), p.nbatch);
+  constexpr int NC = 8;
+  auto kern = exact ? k_absorb<true, NC> : k_absorb<false, NC>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kAbsorbThreads, smem, stream>>>(g, p);
+  return cudaGetLastError();
+}
+
+template <class R>
+cudaError_t launch_gemm_simt(const GemmShape &s, const BatchPtrs &p, bool exact,
+                             cudaStream_t stream) {
+  if (s.M == 0 || s.N == 0 || p.nbatch == 0) return cudaSuccess;
+  dim3 grid(unsigned((s.N + 63) / 64), unsigned((s.M + 63) / 64), unsigned(s.D * p.nbatch));
+  if (exact)
+    k_gemm_simt<R, true><<<grid, 256, 0, stream>>>(s, p);
+  else
+    k_gemm_simt<R, false><<<grid, 256, 0, stream>>>(s, p);
+  return cudaGetLastError();
+}
+
+template <class R>
+cudaError_t launch_leaf_gather(const LeafGatherTable &t, void *arena, const int32_t *digits,
+                               int nbatch, cudaStream_t stream) {
+  if (t.total_out == 0 || nbatch == 0) return cudaSuccess;
+  k_leaf_gather<R><<<grid_for(t.total_out * nbatch, 256), 256, 0, stream>>>(t, arena, digits,
+                                                                            nbatch);
+  return cudaGetLastError();
+}
+
+template <class R>
+cudaError_t launch_root_accumulate(const void *root, int64_t root_bs, int64_t n, int nbatch,
+                                   double *acc, double *per_slice, cudaStream_t stream) {
+  k_root_accumulate<R><<<grid_for(n, 256), 256, 0, stream>>>(root, root_bs, n, nbatch, acc,
+                                                            per_slice);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sum_ordered(const double *per_slice, uint64_t n_slices, int64_t n, double *out,
+                               cudaStream_t stream) {
+  k_sum_ordered<<<grid_for(2 * n, 256), 256, 0, stream>>>(per_slice, n_slices, n, out);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_generic<float>(const StridedGeom &, const BatchPtrs &, bool,
+                                           cudaStream_t);
+template cudaError_t launch_generic<double>(const StridedGeom &, const BatchPtrs &, bool,
+                                            cudaStream_t);
+template cudaError_t launch_permute<float>(const StridedGeom &, const void *, void *, int64_t,
+                                           int64_t, int, cudaStream_t);
+template cudaError_t launch_permute<double>(const StridedGeom &, const void *, void *, int64_t,
+                                            int64_t, int, cudaStream_t);
+template cudaError_t launch_gemm_simt<float>(const GemmShape &, const BatchPtrs &, bool,
+                                             cudaStream_t);
+template cudaError_t launch_gemm_simt<double>(const GemmShape &, const BatchPtrs &, bool,
+                                              cudaStream_t);
+template cudaError_t launch_leaf_gather<float>(const LeafGatherTable &, void *, const int32_t *,
+                                               int, cudaStream_t);
+template cudaError_t launch_leaf_gather<double>(const LeafGatherTable &, void *, const int32_t *,
+                                                int, cudaStream_t);
+template cudaError_t launch_root_accumulate<float>(const void *, int64_t, int64_t, int, double *,
+                                                   double *, cudaStream_t);
+template cudaError_t launch_root_accumulate<double>(const void *, int64_t, int64_t, int,
+                                                    double *, double *, cudaStream_t);
+
+}  // namespace stn

@@ -1,0 +1,124 @@
+// Internal interface between the host executor (stn_exec.cpp) and the sm_100a
+// kernels (kernels.cu, gemm_tc.cu). Not part of the C ABI.
+//
+// Every tensor is complex, interleaved (re, im), in the reference's canonical
+// layout: axes sorted by ascending edge id, row-major (runtime.hpp:341-346).
+// A "batch" is a set of slices executed together; operand batch strides are in
+// complex elements and are 0 for slice-invariant operands.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace stn {
+
+constexpr int kMaxAxes = 40;
+
+// Generic strided contraction (any bond dimensions, D batches included):
+//   out[o] = sum_k A[a_off(o) + ka_off(k)] * B[b_off(o) + kb_off(k)]
+// with o running over the canonical output index and k over the K axes in the
+// reference's [D|M|K] order (ascending edge id, first axis most significant).
+// Axes are listed outermost first; adjacent axes are pre-merged where both
+// operand strides allow it.
+struct StridedGeom {
+  int n_out;
+  int n_k;
+  int64_t out_size;
+  int64_t k_size;
+  int64_t out_dim[kMaxAxes];
+  int64_t out_sa[kMaxAxes];
+  int64_t out_sb[kMaxAxes];
+  int64_t k_dim[kMaxAxes];
+  int64_t k_sa[kMaxAxes];
+  int64_t k_sb[kMaxAxes];
+};
+
+// Batched operand pointers.
+struct BatchPtrs {
+  const void *a;
+  const void *b;
+  void *out;
+  int64_t a_bs, b_bs, out_bs;  // complex-element batch strides
+  int nbatch;
+};
+
+// Bond-2 "absorb": one big operand X (the stem side) contracted with a small
+// operand W over K bits, producing N new bits:
+//   O[m, n] = sum_k X[m, k] * W[k, n]
+// X/O/W bits are positions in the flat canonical index (bit 0 = fastest axis).
+// A CTA owns one assignment of the "outer" M bits and the full tile over the
+// "tile" M bits T, all K bits and all N bits. Tile-local indices list the tile
+// bits in ascending position of the respective tensor, so the lowest bits of X
+// and O (always inside the tile) give coalesced runs.
+constexpr int kAbsorbMaxTileBits = 14;  // X/O tile <= 2^14 complex (128 KiB)
+constexpr int kAbsorbMaxKN = 6;         // K, N <= 64
+struct AbsorbGeom {
+  int x_bits, o_bits;       // log2 |X|, log2 |O|
+  int kb, nb, tb, ob;       // #K, #N, #tile M, #outer M bits
+  int xt_bits, ot_bits;     // tile bits in X (kb+tb) and in O (nb+tb)
+  int x_run, o_run;         // lowest X / O bits that are contiguous inside the tile
+  int w_is_lhs;             // 1: W is the lhs operand (product order w*x)
+  int64_t w_k_stride[kAbsorbMaxKN];  // W element stride of each K bit (k bit j, LSB first)
+  int64_t w_n_stride[kAbsorbMaxKN];  // W element stride of each N bit (n bit j, LSB first)
+  uint8_t x_tile_pos[kAbsorbMaxTileBits + kAbsorbMaxKN];  // X position of tile-local X bit i
+  uint8_t o_tile_pos[kAbsorbMaxTileBits + kAbsorbMaxKN];  // O position of tile-local O bit i
+  uint8_t t_xl[kAbsorbMaxTileBits];  // tile-local X bit of T bit j (T bits in ascending X pos)
+  uint8_t t_ol[kAbsorbMaxTileBits];  // tile-local O bit of T bit j
+  uint8_t k_xl[kAbsorbMaxKN];        // tile-local X bit of K bit j (ascending X pos)
+  uint8_t n_ol[kAbsorbMaxKN];        // tile-local O bit of N bit j (ascending O pos)
+  uint8_t outer_x[34];               // X position of outer M bit j
+  uint8_t outer_o[34];               // O position of outer M bit j
+};
+
+// Dense batched complex GEMM on materialised operands:
+//   C[d] (M x N) = A[d] (M x K, row-major) * B[d] (K x N, row-major)
+struct GemmShape {
+  int64_t D, M, N, K;
+};
+
+// Slice-dependent leaf gather: for every sliced leaf and every slice in the
+// batch, restrict the double-precision vertex tensor on its sliced axes
+// (digits), convert to the executor's real type and lay it out canonically.
+struct LeafGatherTable {
+  const double *values;        // device: all sliced leaves' values, concatenated
+  const int64_t *src_base;     // [total_out] source complex index with sliced axes at 0
+  const int32_t *elem_leaf;    // [total_out] leaf id of output element
+  const int64_t *dst_off;      // [n_leaves] per-slice arena offset (scaled by the batch size)
+  const int64_t *dst_bs;       // [n_leaves] batch stride of the leaf's output
+  const int32_t *elem_local;   // [total_out] element index inside its leaf
+  const int32_t *ax_begin;     // [n_leaves + 1] range into ax_stride/ax_slice
+  const int64_t *ax_stride;    // source stride of each sliced axis
+  const int32_t *ax_slice;     // sliced-edge index of each sliced axis
+  int64_t total_out;
+  int n_sliced;
+};
+
+// ---- launchers (kernels.cu); all asynchronous on `stream` ----
+template <class R>
+cudaError_t launch_generic(const StridedGeom &g, const BatchPtrs &p, bool exact,
+                           cudaStream_t stream);
+cudaError_t launch_absorb(const AbsorbGeom &g, const BatchPtrs &p, bool exact, cudaStream_t stream);
+template <class R>
+cudaError_t launch_permute(const StridedGeom &g, const void *in, void *out, int64_t in_bs,
+                           int64_t out_bs, int nbatch, cudaStream_t stream);
+template <class R>
+cudaError_t launch_gemm_simt(const GemmShape &s, const BatchPtrs &p, bool exact,
+                             cudaStream_t stream);
+template <class R>
+cudaError_t launch_leaf_gather(const LeafGatherTable &t, void *arena, const int32_t *digits,
+                               int nbatch, cudaStream_t stream);
+template <class R>
+cudaError_t launch_root_accumulate(const void *root, int64_t root_bs, int64_t n, int nbatch,
+                                   double *acc, double *per_slice, cudaStream_t stream);
+cudaError_t launch_sum_ordered(const double *per_slice, uint64_t n_slices, int64_t n,
+                               double *out, cudaStream_t stream);
+
+// tcgen05 split-TF32 complex GEMM (gemm_tc.cu). Requires M % 128 == 0,
+// N % 32 == 0, K % 16 == 0 (complex elements); returns cudaErrorNotSupported
+// otherwise so the caller can pick another kernel.
+cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspace,
+                           size_t workspace_bytes, cudaStream_t stream);
+size_t gemm_tc_workspace_bytes(const GemmShape &s);
+bool gemm_tc_supported(const GemmShape &s);
+
+}  // namespace stn

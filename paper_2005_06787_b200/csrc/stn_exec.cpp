@@ -1,0 +1,1544 @@
+// Host side of the B200 stem executor: the C ABI of include/stn_exec.h.
+//
+// What happens where:
+//   stn_plan_create   validates the flattened ExecutablePlan, derives the
+//                     contraction geometry of every step (the reference's
+//                     transpose-GEMM-transpose of runtime.hpp:386-418 becomes a
+//                     stride/bit description), picks a kernel per step, builds
+//                     three programs (branch-cache build, per-slice with cache,
+//                     per-slice without cache) with liveness-planned arenas, and
+//                     uploads the leaf tensors.
+//   stn_cache_build   runs the branch program once; consumed outputs stay in HBM
+//                     (runtime.hpp:456-500).
+//   stn_run_*         run the per-slice program for batches of slices: one
+//                     leaf-gather launch, one launch per step, one ordered
+//                     fp64 accumulation (runtime.hpp:420-453, 601-605).
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "stn_exec.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_error(int status, const std::string &msg) {
+  g_last_error = msg;
+  return status;
+}
+
+struct Failure {
+  int status;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int status, const std::string &msg) { throw Failure{status, msg}; }
+void require(bool cond, int status, const std::string &msg) {
+  if (!cond) fail(status, msg);
+}
+void cuda_check(cudaError_t e, const char *what) {
+  if (e != cudaSuccess)
+    fail(e == cudaErrorMemoryAllocation ? STN_ERR_OUT_OF_MEMORY : STN_ERR_CUDA,
+         std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F &&f) {
+  try {
+    f();
+    return STN_OK;
+  } catch (const Failure &e) {
+    return set_error(e.status, e.msg);
+  } catch (const std::bad_alloc &) {
+    return set_error(STN_ERR_OUT_OF_MEMORY, "host allocation failed");
+  } catch (const std::exception &e) {
+    return set_error(STN_ERR_INVALID_ARGUMENT, e.what());
+  }
+}
+
+// ---------------------------------------------------------------------------
+// device buffers
+// ---------------------------------------------------------------------------
+struct DevBuf {
+  void *ptr = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf &) = delete;
+  DevBuf &operator=(const DevBuf &) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  void reserve(size_t n) {
+    if (n <= bytes) return;
+    release();
+    cuda_check(cudaMalloc(&ptr, n), "cudaMalloc");
+    bytes = n;
+  }
+  template <class T>
+  void upload(const std::vector<T> &v) {
+    reserve(std::max<size_t>(v.size() * sizeof(T), 16));
+    if (!v.empty())
+      cuda_check(cudaMemcpy(ptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice),
+                 "upload");
+  }
+  template <class T>
+  T *as() const {
+    return static_cast<T *>(ptr);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// plan model
+// ---------------------------------------------------------------------------
+enum class Kern { Generic, Absorb, GemmSimt, GemmTc };
+
+struct Node {
+  bool is_leaf = false;
+  int step = -1;  // producing step index
+  int leaf = -1;  // leaf index
+  std::vector<int> dims;  // canonical dims
+  int64_t size = 1;
+  bool sliced_leaf = false;
+  int consumer = -1;  // step index consuming this node (-1: root or unused)
+};
+
+struct StepPlan {
+  stn_step_desc d{};
+  std::vector<int> lperm, rperm, operm, out_dims;
+  Kern kern = Kern::Generic;
+  stn::StridedGeom geo{};  // generic
+  // absorb
+  stn::AbsorbGeom ag{};
+  bool x_is_lhs = true;
+  // gemm path
+  bool a_id = true, b_id = true, c_id = true;
+  stn::StridedGeom pa{}, pb{}, pc{};
+  stn::GemmShape gs{};
+  int64_t lsize = 0, rsize = 0, osize = 0;
+};
+
+enum class Src { ConstLeaf, SliceLeaf, Cache, Arena, Persist };
+
+struct Ref {
+  Src kind = Src::Arena;
+  int node = -1;
+  int64_t off = 0;  // per-slice arena offset (elements) / cache or constant offset
+  int64_t size = 0;
+};
+
+struct Op {
+  int step = -1;
+  Ref a, b, out;
+  int64_t scr_a = -1, scr_b = -1, scr_c = -1;  // arena scratch offsets (gemm path)
+};
+
+struct Program {
+  std::vector<Op> ops;
+  int64_t arena_elems = 0;  // per slice
+  std::vector<int> slice_leaves;           // leaf node ids gathered per slice
+  std::map<int, int64_t> slice_leaf_off;   // node -> arena offset
+  Ref root;
+  bool has_root = false;
+  uint64_t mults = 0;
+  uint64_t peak = 0;
+  // device leaf-gather table
+  DevBuf t_src_base, t_elem_leaf, t_dst_off, t_dst_bs, t_elem_local, t_ax_begin, t_ax_stride,
+      t_ax_slice;
+  stn::LeafGatherTable table{};
+};
+
+}  // namespace
+
+struct stn_cache {
+  uint64_t identity = 0;
+  uint64_t leaf_epoch = 0;
+  uint64_t mults = 0;
+  uint64_t elements = 0;
+  const stn_plan *plan = nullptr;
+  DevBuf storage;
+};
+
+struct stn_plan {
+  int device = 0;
+  int mode = STN_MODE_FAST;
+  int precision = STN_SINGLE;
+  size_t esize = 8;  // bytes per complex element
+  uint64_t identity = 0, subtasks = 0;
+  int merged_groups = 0, exec_cw = 0;
+  int root = -1;
+  std::vector<int32_t> sliced_dims;
+  std::vector<Node> nodes;
+  std::vector<StepPlan> steps;
+  std::vector<stn_leaf_desc> leaf_desc;  // arrays below own the data
+  std::vector<std::vector<int32_t>> leaf_dims, leaf_sax, leaf_sidx, leaf_perm;
+  std::vector<std::vector<double>> leaf_values;
+  std::map<int, int> leaf_of_vertex;
+  // leaves feeding branch steps (cache staleness tracking)
+  std::vector<char> leaf_feeds_branch;
+  uint64_t leaf_epoch = 0;
+  // constants: canonical unsliced leaves (executor precision)
+  std::map<int, int64_t> const_off;  // node -> element offset
+  DevBuf consts;
+  int64_t consts_elems = 0;
+  // sliced leaves: double values, concatenated
+  std::map<int, int64_t> sliced_val_off;  // leaf node -> complex offset into sliced_vals
+  DevBuf sliced_vals;
+  // programs
+  Program build, with_cache, no_cache;
+  std::map<int, int64_t> cache_off;  // node -> element offset in cache storage
+  int64_t cache_elems = 0;
+  // runtime state
+  DevBuf arena, digits, scratch_out, tc_workspace;
+  int64_t out_elements = 1;
+  std::vector<int> out_dims;
+  int max_batch = 0;
+  int kernel_launches = 0;
+  // per-launch profiling (CUDA events on the launch stream)
+  bool profiling = false;
+  struct Pending {
+    int kind;
+    double bytes, flops;
+    cudaEvent_t e0, e1;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+  stn_kernel_profile totals[STN_KERNEL_KINDS] = {};
+  ~stn_plan() {
+    for (auto &p : pending) {
+      cudaEventDestroy(p.e0);
+      cudaEventDestroy(p.e1);
+    }
+    for (auto e : event_pool) cudaEventDestroy(e);
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// geometry helpers
+// ---------------------------------------------------------------------------
+std::vector<int64_t> row_major_strides(const std::vector<int> &dims) {
+  std::vector<int64_t> s(dims.size(), 1);
+  for (int i = int(dims.size()) - 2; i >= 0; --i) s[i] = s[i + 1] * dims[i + 1];
+  return s;
+}
+
+struct Axis {
+  int64_t dim, sa, sb;
+};
+
+// merges adjacent axes whose strides are contiguous in both operands
+std::vector<Axis> merge_axes(const std::vector<Axis> &in) {
+  std::vector<Axis> out;
+  for (const Axis &a : in) {
+    if (a.dim == 1) continue;
+    if (!out.empty()) {
+      Axis &p = out.back();
+      if (p.sa == a.sa * a.dim && p.sb == a.sb * a.dim) {
+        p.dim *= a.dim;
+        p.sa = a.sa;
+        p.sb = a.sb;
+        continue;
+      }
+    }
+    out.push_back(a);
+  }
+  return out;
+}
+
+void fill_geom(stn::StridedGeom &g, const std::vector<Axis> &out_axes,
+               const std::vector<Axis> &k_axes) {
+  std::vector<Axis> o = merge_axes(out_axes), k = merge_axes(k_axes);
+  require(int(o.size()) <= stn::kMaxAxes && int(k.size()) <= stn::kMaxAxes,
+          STN_ERR_INVALID_ARGUMENT, "contraction rank exceeds executor limit");
+  memset(&g, 0, sizeof g);
+  g.n_out = int(o.size());
+  g.n_k = int(k.size());
+  g.out_size = 1;
+  g.k_size = 1;
+  for (int i = 0; i < g.n_out; ++i) {
+    g.out_dim[i] = o[i].dim;
+    g.out_sa[i] = o[i].sa;
+    g.out_sb[i] = o[i].sb;
+    g.out_size *= o[i].dim;
+  }
+  for (int i = 0; i < g.n_k; ++i) {
+    g.k_dim[i] = k[i].dim;
+    g.k_sa[i] = k[i].sa;
+    g.k_sb[i] = k[i].sb;
+    g.k_size *= k[i].dim;
+  }
+}
+
+// permutation as a gather: out axis i = in axis perm[i]
+void fill_permute(stn::StridedGeom &g, const std::vector<int> &in_dims,
+                  const std::vector<int> &perm) {
+  std::vector<int64_t> s = row_major_strides(in_dims);
+  std::vector<Axis> ax;
+  for (size_t i = 0; i < perm.size(); ++i) ax.push_back({in_dims[perm[i]], s[perm[i]], 0});
+  fill_geom(g, ax, {});
+}
+
+bool is_identity(const std::vector<int> &p) {
+  for (size_t i = 0; i < p.size(); ++i)
+    if (p[i] != int(i)) return false;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// absorb geometry (bond-2, D == 1): see kernels.h AbsorbGeom
+// ---------------------------------------------------------------------------
+bool build_absorb(StepPlan &sp, const std::vector<int> &ldims, const std::vector<int> &rdims) {
+  const stn_step_desc &d = sp.d;
+  if (d.nd != 0) return false;
+  for (int x : ldims)
+    if (x != 2) return false;
+  for (int x : rdims)
+    if (x != 2) return false;
+  const int lr = int(ldims.size()), rr = int(rdims.size()), orank = int(sp.out_dims.size());
+  const bool x_lhs = sp.lsize >= sp.rsize;
+  const int xr = x_lhs ? lr : rr, wr = x_lhs ? rr : lr;
+  const int kb = d.nk;
+  const int nb = wr - kb;  // W-side free bits
+  const int mb = xr - kb;
+  if (kb > stn::kAbsorbMaxKN || nb > stn::kAbsorbMaxKN || xr < 12) return false;
+  // K bits: (x position, w position)
+  std::vector<std::pair<int, int>> kbits;
+  for (int q = 0; q < d.nk; ++q) {
+    int la = sp.lperm[d.nd + d.nm + q], rb = sp.rperm[d.nd + q];
+    int xa = x_lhs ? la : rb, wa = x_lhs ? rb : la;
+    kbits.push_back({xr - 1 - xa, wr - 1 - wa});
+  }
+  std::sort(kbits.begin(), kbits.end());
+  // output bits: M pairs (x pos, o pos) from X, N pairs (w pos, o pos) from W
+  std::vector<std::pair<int, int>> mbits, nbits;  // (xpos, opos), (opos, wpos)
+  for (int i = 0; i < orank; ++i) {
+    int p = sp.operm[i];
+    int opos = orank - 1 - i;
+    bool from_lhs = p < d.nd + d.nm;
+    if (from_lhs) {
+      int la = sp.lperm[p];
+      if (x_lhs)
+        mbits.push_back({lr - 1 - la, opos});
+      else
+        nbits.push_back({opos, lr - 1 - la});
+    } else {
+      int q = p - d.nd - d.nm;
+      int rb = sp.rperm[d.nd + d.nk + q];
+      if (x_lhs)
+        nbits.push_back({opos, rr - 1 - rb});
+      else
+        mbits.push_back({rr - 1 - rb, opos});
+    }
+  }
+  std::sort(nbits.begin(), nbits.end());
+  if (int(mbits.size()) != mb || int(nbits.size()) != nb) return false;
+  // W positions of K and N bits must be ascending with their X/O order
+  for (size_t j = 1; j < kbits.size(); ++j)
+    if (kbits[j].second < kbits[j - 1].second) return false;
+  for (size_t j = 1; j < nbits.size(); ++j)
+    if (nbits[j].second < nbits[j - 1].second) return false;
+
+  // choose tile M bits T: low X bits, low O bits, then ascending X position
+  const int x_bits = xr, o_bits = orank;
+  const int Lx = std::min(5, x_bits), Lo = std::min(5, o_bits);
+  std::vector<char> in_t(mbits.size(), 0);
+  int tb = 0;
+  for (size_t j = 0; j < mbits.size(); ++j)
+    if (mbits[j].first < Lx || mbits[j].second < Lo) {
+      in_t[j] = 1;
+      tb++;
+    }
+  const int target = 11;
+  {
+    std::vector<size_t> order(mbits.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(),
+              [&](size_t a, size_t b) { return mbits[a].first < mbits[b].first; });
+    for (size_t j : order) {
+      if (in_t[j]) continue;
+      if (kb + tb >= target || nb + tb >= target) break;
+      in_t[j] = 1;
+      tb++;
+    }
+  }
+  if (kb + tb > 13 || nb + tb > 13) return false;  // <= 64 KiB per tile
+  if (kb + tb < 2 || nb + tb < 2) return false;
+  const int ob = mb - tb;
+  if (ob > 31) return false;
+
+  stn::AbsorbGeom g;
+  memset(&g, 0, sizeof g);
+  g.x_bits = x_bits;
+  g.o_bits = o_bits;
+  g.kb = kb;
+  g.nb = nb;
+  g.tb = tb;
+  g.ob = ob;
+  g.xt_bits = kb + tb;
+  g.ot_bits = nb + tb;
+  g.w_is_lhs = x_lhs ? 0 : 1;
+  for (int j = 0; j < kb; ++j) g.w_k_stride[j] = int64_t(1) << kbits[j].second;
+  for (int j = 0; j < nb; ++j) g.w_n_stride[j] = int64_t(1) << nbits[j].second;
+  // tile-local X bits: K bits and T bits by ascending X position
+  std::vector<std::pair<int, int>> xt;  // (xpos, tag) tag: -1-k for K bit k, j for M bit j
+  for (int j = 0; j < kb; ++j) xt.push_back({kbits[j].first, -1 - j});
+  for (size_t j = 0; j < mbits.size(); ++j)
+    if (in_t[j]) xt.push_back({mbits[j].first, int(j)});
+  std::sort(xt.begin(), xt.end());
+  std::vector<std::pair<int, int>> otl;  // (opos, tag) tag: -1-n for N bit n, j for M bit j
+  for (int j = 0; j < nb; ++j) otl.push_back({nbits[j].first, -1 - j});
+  for (size_t j = 0; j < mbits.size(); ++j)
+    if (in_t[j]) otl.push_back({mbits[j].second, int(j)});
+  std::sort(otl.begin(), otl.end());
+  std::map<int, int> xl_of_m, ol_of_m;
+  for (int i = 0; i < int(xt.size()); ++i) {
+    g.x_tile_pos[i] = uint8_t(xt[i].first);
+    if (xt[i].second < 0)
+      g.k_xl[-1 - xt[i].second] = uint8_t(i);
+    else
+      xl_of_m[xt[i].second] = i;
+  }
+  for (int i = 0; i < int(otl.size()); ++i) {
+    g.o_tile_pos[i] = uint8_t(otl[i].first);
+    if (otl[i].second < 0)
+      g.n_ol[-1 - otl[i].second] = uint8_t(i);
+    else
+      ol_of_m[otl[i].second] = i;
+  }
+  // T bits in ascending X position
+  int tj = 0, oj = 0;
+  {
+    std::vector<size_t> order(mbits.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(),
+              [&](size_t a, size_t b) { return mbits[a].first < mbits[b].first; });
+    for (size_t j : order) {
+      if (in_t[j]) {
+        g.t_xl[tj] = uint8_t(xl_of_m[int(j)]);
+        g.t_ol[tj] = uint8_t(ol_of_m[int(j)]);
+        tj++;
+      } else {
+        g.outer_x[oj] = uint8_t(mbits[j].first);
+        g.outer_o[oj] = uint8_t(mbits[j].second);
+        oj++;
+      }
+    }
+  }
+  g.x_run = 0;
+  while (g.x_run < g.xt_bits && g.x_tile_pos[g.x_run] == g.x_run) g.x_run++;
+  g.o_run = 0;
+  while (g.o_run < g.ot_bits && g.o_tile_pos[g.o_run] == g.o_run) g.o_run++;
+  if (g.x_run < 1 || g.o_run < 1) return false;
+  sp.ag = g;
+  sp.x_is_lhs = x_lhs;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// plan construction
+// ---------------------------------------------------------------------------
+void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
+                   const std::vector<int> &rdims) {
+  const stn_step_desc &d = sp.d;
+  const bool single = P.precision == STN_SINGLE;
+  const bool exact = P.mode == STN_MODE_EXACT;
+  // generic geometry (always built: also the fallback)
+  {
+    std::vector<int64_t> ls = row_major_strides(ldims), rs = row_major_strides(rdims);
+    std::vector<Axis> out_axes, k_axes;
+    for (int i = 0; i < d.orank; ++i) {
+      int p = sp.operm[i];
+      if (p < d.nd) {
+        out_axes.push_back({sp.out_dims[i], ls[sp.lperm[p]], rs[sp.rperm[p]]});
+      } else if (p < d.nd + d.nm) {
+        out_axes.push_back({sp.out_dims[i], ls[sp.lperm[p]], 0});
+      } else {
+        int q = p - d.nd - d.nm;
+        out_axes.push_back({sp.out_dims[i], 0, rs[sp.rperm[d.nd + d.nk + q]]});
+      }
+    }
+    for (int q = 0; q < d.nk; ++q) {
+      int la = sp.lperm[d.nd + d.nm + q], rb = sp.rperm[d.nd + q];
+      k_axes.push_back({ldims[la], ls[la], rs[rb]});
+    }
+    fill_geom(sp.geo, out_axes, k_axes);
+  }
+  sp.kern = Kern::Generic;
+  const int64_t small = std::min(sp.lsize, sp.rsize);
+  const int64_t big = std::max(sp.lsize, sp.rsize);
+  // bandwidth-bound absorb: one big operand, a small K x N side
+  if (single && big >= (int64_t(1) << 12) && small <= 4096 && build_absorb(sp, ldims, rdims)) {
+    sp.kern = Kern::Absorb;
+    return;
+  }
+  // dense GEMM path: materialise [D|M|K], [D|K|N], run GEMM, permute [D|M|N]
+  if (d.M >= 8 && d.N >= 8 && d.K >= 8 && d.mults >= (uint64_t(1) << 18)) {
+    std::vector<int> prod_dims(d.orank);
+    for (int i = 0; i < d.orank; ++i) prod_dims[sp.operm[i]] = sp.out_dims[i];
+    sp.a_id = is_identity(sp.lperm);
+    sp.b_id = is_identity(sp.rperm);
+    sp.c_id = is_identity(sp.operm);
+    fill_permute(sp.pa, ldims, sp.lperm);
+    fill_permute(sp.pb, rdims, sp.rperm);
+    fill_permute(sp.pc, prod_dims, sp.operm);
+    sp.gs = {d.D, d.M, d.N, d.K};
+    sp.kern = (single && !exact && stn::gemm_tc_supported(sp.gs)) ? Kern::GemmTc : Kern::GemmSimt;
+  }
+}
+
+void build_program(stn_plan &P, Program &prog, int which /*0 build, 1 cache, 2 no cache*/) {
+  prog.ops.clear();
+  prog.slice_leaves.clear();
+  prog.slice_leaf_off.clear();
+  prog.mults = 0;
+  prog.peak = 0;
+  struct Item {
+    int64_t size, start, end;
+    int64_t *off;
+  };
+  std::vector<Item> items;
+  std::vector<std::unique_ptr<int64_t>> offs;
+  auto new_item = [&](int64_t size, int64_t start, int64_t end) {
+    offs.emplace_back(new int64_t(0));
+    items.push_back({size, start, end, offs.back().get()});
+    return offs.back().get();
+  };
+  // which steps run
+  std::vector<int> run;
+  for (int i = 0; i < int(P.steps.size()); ++i) {
+    bool br = P.steps[i].d.is_branch != 0;
+    if (which == 0 && br) run.push_back(i);
+    if (which == 1 && !br) run.push_back(i);
+    if (which == 2) run.push_back(i);
+  }
+  std::map<int, int> op_of_step;
+  for (int k = 0; k < int(run.size()); ++k) op_of_step[run[k]] = k;
+  const int64_t n_ops = int64_t(run.size());
+  // consumer op of each node within this program
+  std::map<int, int64_t> consumer_op;
+  for (int k = 0; k < int(run.size()); ++k) {
+    const StepPlan &sp = P.steps[run[k]];
+    consumer_op[sp.d.lhs] = k;
+    consumer_op[sp.d.rhs] = k;
+  }
+  auto end_of = [&](int node) -> int64_t {
+    auto it = consumer_op.find(node);
+    return it == consumer_op.end() ? n_ops : it->second;  // root lives to the end
+  };
+  // where a program input comes from
+  std::map<int, int64_t *> out_off_ptr;   // node produced in this program -> arena offset
+  std::map<int, int64_t *> leaf_off_ptr;  // sliced leaf -> arena offset
+  auto make_input = [&](int node) -> Ref {
+    Ref r;
+    r.node = node;
+    r.size = P.nodes[node].size;
+    const Node &nd = P.nodes[node];
+    if (!nd.is_leaf) {
+      int st = nd.step;
+      if (op_of_step.count(st)) {
+        if (which == 0 && P.cache_off.count(node)) {
+          r.kind = Src::Persist;
+          r.off = P.cache_off.at(node);
+        } else {
+          r.kind = Src::Arena;  // offset resolved after allocation
+        }
+      } else {
+        require(which == 1 && P.cache_off.count(node), STN_ERR_SUBTASK_FAILURE,
+                "operand for node " + std::to_string(node) + " unavailable");
+        r.kind = Src::Cache;
+        r.off = P.cache_off.at(node);
+      }
+    } else if (nd.sliced_leaf) {
+      require(which != 0, STN_ERR_SUBTASK_FAILURE, "sliced leaf feeds a branch step");
+      r.kind = Src::SliceLeaf;
+      if (!leaf_off_ptr.count(node)) {
+        leaf_off_ptr[node] = new_item(nd.size, -1, end_of(node));
+        prog.slice_leaves.push_back(node);
+      }
+    } else {
+      r.kind = Src::ConstLeaf;
+      r.off = P.const_off.at(node);
+    }
+    return r;
+  };
+  for (int k = 0; k < int(run.size()); ++k) {
+    const StepPlan &sp = P.steps[run[k]];
+    Op op;
+    op.step = run[k];
+    op.a = make_input(sp.d.lhs);
+    op.b = make_input(sp.d.rhs);
+    op.out.node = sp.d.node;
+    op.out.size = sp.osize;
+    if (which == 0 && P.cache_off.count(sp.d.node)) {
+      op.out.kind = Src::Persist;
+      op.out.off = P.cache_off.at(sp.d.node);
+    } else {
+      op.out.kind = Src::Arena;
+      out_off_ptr[sp.d.node] = new_item(sp.osize, k, end_of(sp.d.node));
+    }
+    prog.ops.push_back(op);
+    prog.mults += sp.d.mults;
+    prog.peak = std::max<uint64_t>(prog.peak, uint64_t(sp.osize));
+  }
+  // gemm-path scratch (lifetime: the op itself)
+  std::vector<std::array<int64_t *, 3>> scr(prog.ops.size(), {nullptr, nullptr, nullptr});
+  for (size_t k = 0; k < prog.ops.size(); ++k) {
+    const StepPlan &sp = P.steps[prog.ops[k].step];
+    if (sp.kern != Kern::GemmSimt && sp.kern != Kern::GemmTc) continue;
+    if (!sp.a_id) scr[k][0] = new_item(sp.lsize, int64_t(k), int64_t(k));
+    if (!sp.b_id) scr[k][1] = new_item(sp.rsize, int64_t(k), int64_t(k));
+    if (!sp.c_id) scr[k][2] = new_item(sp.osize, int64_t(k), int64_t(k));
+  }
+  // liveness allocation: biggest first, lowest non-conflicting offset
+  std::vector<size_t> order(items.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](size_t a, size_t b) { return items[a].size > items[b].size; });
+  const int64_t align = 64;  // elements (512 B in single precision)
+  auto aligned = [&](int64_t x) { return (x + align - 1) / align * align; };
+  std::vector<size_t> placed;
+  int64_t arena = 0;
+  for (size_t i : order) {
+    Item &it = items[i];
+    std::vector<std::pair<int64_t, int64_t>> busy;
+    for (size_t j : placed) {
+      const Item &o = items[j];
+      if (o.start <= it.end && it.start <= o.end) busy.push_back({*o.off, *o.off + aligned(o.size)});
+    }
+    std::sort(busy.begin(), busy.end());
+    int64_t cand = 0;
+    for (auto &[lo, hi] : busy) {
+      if (cand + aligned(it.size) <= lo) break;
+      cand = std::max(cand, hi);
+    }
+    *it.off = cand;
+    arena = std::max(arena, cand + aligned(it.size));
+    placed.push_back(i);
+  }
+  prog.arena_elems = arena;
+  for (size_t k = 0; k < prog.ops.size(); ++k) {
+    Op &op = prog.ops[k];
+    for (Ref *r : {&op.a, &op.b})
+      if (r->kind == Src::Arena)
+        r->off = *out_off_ptr.at(r->node);
+      else if (r->kind == Src::SliceLeaf)
+        r->off = *leaf_off_ptr.at(r->node);
+    if (op.out.kind == Src::Arena) op.out.off = *out_off_ptr.at(op.out.node);
+    op.scr_a = scr[k][0] ? *scr[k][0] : -1;
+    op.scr_b = scr[k][1] ? *scr[k][1] : -1;
+    op.scr_c = scr[k][2] ? *scr[k][2] : -1;
+  }
+  for (int node : prog.slice_leaves) prog.slice_leaf_off[node] = *leaf_off_ptr.at(node);
+  // root
+  prog.has_root = which != 0;
+  if (prog.has_root) {
+    int root = P.root;
+    if (out_off_ptr.count(root)) {
+      prog.root = Ref{Src::Arena, root, *out_off_ptr.at(root), P.nodes[root].size};
+    } else if (P.nodes[root].is_leaf) {
+      prog.root = Ref{};
+      prog.root.node = root;
+      prog.root.size = P.nodes[root].size;
+      if (P.nodes[root].sliced_leaf) {
+        prog.root.kind = Src::SliceLeaf;
+        if (!leaf_off_ptr.count(root)) {
+          // a lone sliced leaf: give it its own arena slot at the end
+          prog.slice_leaves.push_back(root);
+          prog.slice_leaf_off[root] = prog.arena_elems;
+          prog.arena_elems += aligned(P.nodes[root].size);
+        }
+        prog.root.off = prog.slice_leaf_off.at(root);
+      } else {
+        prog.root.kind = Src::ConstLeaf;
+        prog.root.off = P.const_off.at(root);
+      }
+    } else {
+      require(which == 1 && P.cache_off.count(root), STN_ERR_SUBTASK_FAILURE,
+              "root unavailable");
+      prog.root = Ref{Src::Cache, root, P.cache_off.at(root), P.nodes[root].size};
+    }
+  }
+  // leaf-gather table
+  std::vector<int64_t> src_base, dst_off, dst_bs, ax_stride;
+  std::vector<int32_t> elem_leaf, elem_local, ax_begin, ax_slice;
+  ax_begin.push_back(0);
+  for (size_t li = 0; li < prog.slice_leaves.size(); ++li) {
+    int node = prog.slice_leaves[li];
+    const stn_leaf_desc &L = P.leaf_desc[P.nodes[node].leaf];
+    std::vector<int> dims(L.dims, L.dims + L.rank);
+    std::vector<int64_t> st = row_major_strides(dims);
+    std::vector<char> sliced(L.rank, 0);
+    for (int s = 0; s < L.n_sliced; ++s) {
+      sliced[L.sliced_axis[s]] = 1;
+      ax_stride.push_back(st[L.sliced_axis[s]]);
+      ax_slice.push_back(L.sliced_index[s]);
+    }
+    ax_begin.push_back(int32_t(ax_stride.size()));
+    std::vector<int> kept_axes;
+    for (int a = 0; a < L.rank; ++a)
+      if (!sliced[a]) kept_axes.push_back(a);
+    // canonical axis i = kept axis perm[i]
+    std::vector<int> cdims(L.perm_rank);
+    std::vector<int64_t> cstr(L.perm_rank);
+    for (int i = 0; i < L.perm_rank; ++i) {
+      cdims[i] = dims[kept_axes[L.perm[i]]];
+      cstr[i] = st[kept_axes[L.perm[i]]];
+    }
+    int64_t n = 1;
+    for (int x : cdims) n *= x;
+    const int64_t voff = P.sliced_val_off.at(node);
+    for (int64_t e = 0; e < n; ++e) {
+      int64_t rem = e, src = 0;
+      for (int i = L.perm_rank - 1; i >= 0; --i) {
+        src += (rem % cdims[i]) * cstr[i];
+        rem /= cdims[i];
+      }
+      src_base.push_back(voff + src);
+      elem_leaf.push_back(int32_t(li));
+      elem_local.push_back(int32_t(e));
+    }
+    dst_off.push_back(prog.slice_leaf_off.at(node));
+    dst_bs.push_back(P.nodes[node].size);
+  }
+  prog.t_src_base.upload(src_base);
+  prog.t_elem_leaf.upload(elem_leaf);
+  prog.t_elem_local.upload(elem_local);
+  prog.t_dst_off.upload(dst_off);
+  prog.t_dst_bs.upload(dst_bs);
+  prog.t_ax_begin.upload(ax_begin);
+  prog.t_ax_stride.upload(ax_stride);
+  prog.t_ax_slice.upload(ax_slice);
+  stn::LeafGatherTable &t = prog.table;
+  t.values = P.sliced_vals.as<double>();
+  t.src_base = prog.t_src_base.as<int64_t>();
+  t.elem_leaf = prog.t_elem_leaf.as<int32_t>();
+  t.dst_off = prog.t_dst_off.as<int64_t>();
+  t.dst_bs = prog.t_dst_bs.as<int64_t>();
+  t.elem_local = prog.t_elem_local.as<int32_t>();
+  t.ax_begin = prog.t_ax_begin.as<int32_t>();
+  t.ax_stride = prog.t_ax_stride.as<int64_t>();
+  t.ax_slice = prog.t_ax_slice.as<int32_t>();
+  t.total_out = int64_t(src_base.size());
+  t.n_sliced = int(P.sliced_dims.size());
+}
+
+// canonical, executor-precision copy of an unsliced leaf (load_leaf without
+// restriction: from_tensor + permute, runtime.hpp:382-383)
+void canonical_leaf(const stn_plan &P, int leaf, std::vector<double> &out) {
+  const stn_leaf_desc &L = P.leaf_desc[leaf];
+  std::vector<int> dims(L.dims, L.dims + L.rank);
+  std::vector<int64_t> st = row_major_strides(dims);
+  std::vector<int> cdims(L.perm_rank);
+  std::vector<int64_t> cstr(L.perm_rank);
+  for (int i = 0; i < L.perm_rank; ++i) {
+    cdims[i] = dims[L.perm[i]];
+    cstr[i] = st[L.perm[i]];
+  }
+  int64_t n = 1;
+  for (int x : cdims) n *= x;
+  out.resize(2 * n);
+  for (int64_t e = 0; e < n; ++e) {
+    int64_t rem = e, src = 0;
+    for (int i = L.perm_rank - 1; i >= 0; --i) {
+      src += (rem % cdims[i]) * cstr[i];
+      rem /= cdims[i];
+    }
+    out[2 * e] = L.values[2 * src];
+    out[2 * e + 1] = L.values[2 * src + 1];
+  }
+}
+
+void upload_consts(stn_plan &P) {
+  std::vector<unsigned char> host(size_t(P.consts_elems) * P.esize);
+  for (auto &[node, off] : P.const_off) {
+    std::vector<double> v;
+    canonical_leaf(P, P.nodes[node].leaf, v);
+    for (size_t i = 0; i < v.size(); ++i) {
+      if (P.precision == STN_SINGLE) {
+        float f = float(v[i]);
+        memcpy(host.data() + (size_t(off) * 2 + i) * 4, &f, 4);
+      } else {
+        memcpy(host.data() + (size_t(off) * 2 + i) * 8, &v[i], 8);
+      }
+    }
+  }
+  P.consts.upload(host);
+}
+
+void upload_sliced_values(stn_plan &P) {
+  std::vector<double> vals;
+  for (auto &[node, off] : P.sliced_val_off) {
+    const stn_leaf_desc &L = P.leaf_desc[P.nodes[node].leaf];
+    int64_t n = 1;
+    for (int a = 0; a < L.rank; ++a) n *= L.dims[a];
+    vals.resize(std::max<size_t>(vals.size(), size_t(2 * (off + n))));
+    memcpy(vals.data() + 2 * off, L.values, size_t(16 * n));
+  }
+  P.sliced_vals.upload(vals);
+}
+
+void create_plan(const stn_plan_desc *desc, int device, int mode, stn_plan *P) {
+  require(desc != nullptr, STN_ERR_INVALID_ARGUMENT, "NULL plan descriptor");
+  require(desc->precision == STN_SINGLE || desc->precision == STN_DOUBLE,
+          STN_ERR_INVALID_ARGUMENT, "bad precision");
+  require(mode == STN_MODE_FAST || mode == STN_MODE_EXACT, STN_ERR_INVALID_ARGUMENT, "bad mode");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  require(e == cudaSuccess && ndev > 0, STN_ERR_NO_DEVICE, "no CUDA device available");
+  require(device >= 0 && device < ndev, STN_ERR_NO_DEVICE, "device index out of range");
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  cudaDeviceProp prop;
+  cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  require(prop.major == 10, STN_ERR_NO_DEVICE,
+          std::string("executor is built for sm_100a; device is ") + prop.name);
+  P->device = device;
+  P->mode = mode;
+  P->precision = desc->precision;
+  P->esize = desc->precision == STN_SINGLE ? 8 : 16;
+  P->identity = desc->identity;
+  P->subtasks = desc->subtasks;
+  P->merged_groups = desc->merged_groups;
+  P->exec_cw = desc->exec_cw;
+  P->root = desc->root;
+  require(desc->n_nodes > 0 && desc->root >= 0 && desc->root < desc->n_nodes,
+          STN_ERR_MALFORMED_NETWORK, "bad node count / root");
+  P->sliced_dims.assign(desc->sliced_dims, desc->sliced_dims + desc->n_sliced);
+  for (int32_t d : P->sliced_dims) require(d > 0, STN_ERR_MALFORMED_NETWORK, "bad sliced dim");
+  P->nodes.assign(desc->n_nodes, Node{});
+  // leaves (copied: the descriptor may be freed after create)
+  const int nl = desc->n_leaves;
+  P->leaf_desc.resize(nl);
+  P->leaf_dims.resize(nl);
+  P->leaf_sax.resize(nl);
+  P->leaf_sidx.resize(nl);
+  P->leaf_perm.resize(nl);
+  P->leaf_values.resize(nl);
+  for (int i = 0; i < nl; ++i) {
+    const stn_leaf_desc &L = desc->leaves[i];
+    require(L.node >= 0 && L.node < desc->n_nodes && L.rank >= 0 && L.rank <= 64 &&
+                L.n_sliced >= 0 && L.n_sliced <= L.rank && L.perm_rank == L.rank - L.n_sliced,
+            STN_ERR_MALFORMED_NETWORK, "malformed leaf " + std::to_string(i));
+    P->leaf_dims[i].assign(L.dims, L.dims + L.rank);
+    P->leaf_sax[i].assign(L.sliced_axis, L.sliced_axis + L.n_sliced);
+    P->leaf_sidx[i].assign(L.sliced_index, L.sliced_index + L.n_sliced);
+    P->leaf_perm[i].assign(L.perm, L.perm + L.perm_rank);
+    int64_t n = 1;
+    for (int a = 0; a < L.rank; ++a) {
+      require(L.dims[a] > 0, STN_ERR_MALFORMED_NETWORK, "bond dimension must be positive");
+      n *= L.dims[a];
+    }
+    P->leaf_values[i].assign(L.values, L.values + 2 * n);
+    for (int s = 0; s < L.n_sliced; ++s)
+      require(L.sliced_axis[s] >= 0 && L.sliced_axis[s] < L.rank && L.sliced_index[s] >= 0 &&
+                  L.sliced_index[s] < desc->n_sliced &&
+                  L.dims[L.sliced_axis[s]] == desc->sliced_dims[L.sliced_index[s]],
+              STN_ERR_MALFORMED_NETWORK, "malformed sliced axis");
+    for (int s = 1; s < L.n_sliced; ++s)
+      require(L.sliced_axis[s] < L.sliced_axis[s - 1], STN_ERR_MALFORMED_NETWORK,
+              "sliced axes must be in descending order");
+    stn_leaf_desc c = L;
+    c.dims = P->leaf_dims[i].data();
+    c.sliced_axis = P->leaf_sax[i].data();
+    c.sliced_index = P->leaf_sidx[i].data();
+    c.perm = P->leaf_perm[i].data();
+    c.values = P->leaf_values[i].data();
+    P->leaf_desc[i] = c;
+    Node &nd = P->nodes[L.node];
+    require(!nd.is_leaf, STN_ERR_MALFORMED_NETWORK, "duplicate leaf node");
+    nd.is_leaf = true;
+    nd.leaf = i;
+    nd.sliced_leaf = L.n_sliced > 0;
+    std::vector<int> kept;
+    std::vector<char> sl(L.rank, 0);
+    for (int s = 0; s < L.n_sliced; ++s) sl[L.sliced_axis[s]] = 1;
+    for (int a = 0; a < L.rank; ++a)
+      if (!sl[a]) kept.push_back(L.dims[a]);
+    std::vector<char> seen(L.perm_rank, 0);
+    for (int a = 0; a < L.perm_rank; ++a) {
+      require(L.perm[a] >= 0 && L.perm[a] < L.perm_rank && !seen[L.perm[a]],
+              STN_ERR_MALFORMED_NETWORK, "leaf perm is not a permutation");
+      seen[L.perm[a]] = 1;
+      nd.dims.push_back(kept[L.perm[a]]);
+    }
+    nd.size = 1;
+    for (int x : nd.dims) nd.size *= x;
+    P->leaf_of_vertex[L.vertex] = i;
+  }
+  // steps
+  P->steps.resize(desc->n_steps);
+  for (int i = 0; i < desc->n_steps; ++i) {
+    const stn_step_desc &d = desc->steps[i];
+    StepPlan &sp = P->steps[i];
+    sp.d = d;
+    require(d.node >= 0 && d.node < desc->n_nodes && d.lhs >= 0 && d.lhs < desc->n_nodes &&
+                d.rhs >= 0 && d.rhs < desc->n_nodes,
+            STN_ERR_MALFORMED_NETWORK, "step node id out of range");
+    require(d.lrank == d.nd + d.nm + d.nk && d.rrank == d.nd + d.nk + d.nn &&
+                d.orank == d.nd + d.nm + d.nn && d.orank <= 64,
+            STN_ERR_MALFORMED_NETWORK, "step axis groups inconsistent");
+    sp.lperm.assign(d.lperm, d.lperm + d.lrank);
+    sp.rperm.assign(d.rperm, d.rperm + d.rrank);
+    sp.operm.assign(d.operm, d.operm + d.orank);
+    sp.out_dims.assign(d.out_dims, d.out_dims + d.orank);
+    sp.d.lperm = sp.d.rperm = sp.d.operm = sp.d.out_dims = nullptr;
+    Node &nd = P->nodes[d.node];
+    require(!nd.is_leaf && nd.step < 0, STN_ERR_MALFORMED_NETWORK, "node produced twice");
+    nd.step = i;
+    nd.dims = sp.out_dims;
+    nd.size = 1;
+    for (int x : nd.dims) nd.size *= x;
+  }
+  // consumers, operand shapes and per-step geometry (post-order: children first)
+  P->leaf_feeds_branch.assign(nl, 0);
+  for (int i = 0; i < desc->n_steps; ++i) {
+    StepPlan &sp = P->steps[i];
+    const stn_step_desc &d = sp.d;
+    for (int c : {d.lhs, d.rhs}) {
+      Node &cn = P->nodes[c];
+      require(cn.is_leaf || (cn.step >= 0 && cn.step < i), STN_ERR_MALFORMED_NETWORK,
+              "steps are not in post-order");
+      require(cn.consumer < 0, STN_ERR_MALFORMED_NETWORK, "node consumed twice");
+      cn.consumer = i;
+      if (cn.is_leaf && d.is_branch) P->leaf_feeds_branch[cn.leaf] = 1;
+    }
+    const std::vector<int> &ld = P->nodes[d.lhs].dims, &rd = P->nodes[d.rhs].dims;
+    require(int(ld.size()) == d.lrank && int(rd.size()) == d.rrank, STN_ERR_MALFORMED_NETWORK,
+            "operand rank mismatch at node " + std::to_string(d.node));
+    sp.lsize = P->nodes[d.lhs].size;
+    sp.rsize = P->nodes[d.rhs].size;
+    sp.osize = P->nodes[d.node].size;
+    // group dims must agree with the recorded D, M, N, K
+    int64_t D = 1, M = 1, N = 1, K = 1;
+    for (int q = 0; q < d.nd; ++q) D *= ld[sp.lperm[q]];
+    for (int q = 0; q < d.nm; ++q) M *= ld[sp.lperm[d.nd + q]];
+    for (int q = 0; q < d.nk; ++q) K *= ld[sp.lperm[d.nd + d.nm + q]];
+    for (int q = 0; q < d.nn; ++q) N *= rd[sp.rperm[d.nd + d.nk + q]];
+    require(D == d.D && M == d.M && N == d.N && K == d.K && sp.osize == D * M * N,
+            STN_ERR_MALFORMED_NETWORK, "step shape inconsistent at node " + std::to_string(d.node));
+    choose_kernel(*P, sp, ld, rd);
+  }
+  // root
+  {
+    const Node &r = P->nodes[P->root];
+    require(r.is_leaf || r.step >= 0, STN_ERR_MALFORMED_NETWORK, "root is neither leaf nor step");
+    P->out_dims = r.dims;
+    P->out_elements = r.size;
+  }
+  // constant (unsliced) leaves and sliced-leaf values
+  int64_t coff = 0, soff = 0;
+  for (int i = 0; i < nl; ++i) {
+    int node = desc->leaves[i].node;
+    const Node &nd = P->nodes[node];
+    if (nd.sliced_leaf) {
+      P->sliced_val_off[node] = soff;
+      int64_t n = 1;
+      for (int a = 0; a < desc->leaves[i].rank; ++a) n *= desc->leaves[i].dims[a];
+      soff += n;
+    } else {
+      P->const_off[node] = coff;
+      coff += (nd.size + 7) / 8 * 8;
+    }
+  }
+  P->consts_elems = std::max<int64_t>(coff, 1);
+  upload_consts(*P);
+  upload_sliced_values(*P);
+  // branch outputs that survive the cache build (runtime.hpp:473-487)
+  {
+    std::vector<char> needed(desc->n_nodes, 0);
+    for (auto &sp : P->steps)
+      if (!sp.d.is_branch) needed[sp.d.lhs] = needed[sp.d.rhs] = 1;
+    needed[P->root] = 1;
+    int64_t off = 0;
+    for (auto &sp : P->steps)
+      if (sp.d.is_branch && needed[sp.d.node]) {
+        P->cache_off[sp.d.node] = off;
+        off += (sp.osize + 63) / 64 * 64;
+      }
+    P->cache_elems = off;
+  }
+  build_program(*P, P->build, 0);
+  build_program(*P, P->with_cache, 1);
+  build_program(*P, P->no_cache, 2);
+}
+
+// ---------------------------------------------------------------------------
+// execution
+// ---------------------------------------------------------------------------
+// ---- per-launch profiling ----
+cudaEvent_t take_event(stn_plan &P) {
+  if (!P.event_pool.empty()) {
+    cudaEvent_t e = P.event_pool.back();
+    P.event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+  return e;
+}
+
+struct ProfScope {
+  stn_plan &P;
+  cudaStream_t st;
+  cudaEvent_t e0 = nullptr;
+  ProfScope(stn_plan &p, cudaStream_t s) : P(p), st(s) {
+    if (P.profiling) {
+      e0 = take_event(P);
+      cuda_check(cudaEventRecord(e0, st), "cudaEventRecord");
+    }
+  }
+  void done(int kind, double bytes, double flops) {
+    P.kernel_launches++;
+    if (!P.profiling) return;
+    cudaEvent_t e1 = take_event(P);
+    cuda_check(cudaEventRecord(e1, st), "cudaEventRecord");
+    P.pending.push_back({kind, bytes, flops, e0, e1});
+    e0 = take_event(P);
+    cuda_check(cudaEventRecord(e0, st), "cudaEventRecord");
+  }
+  ~ProfScope() {
+    if (e0) P.event_pool.push_back(e0);
+  }
+};
+
+void collect_profile(stn_plan &P) {
+  for (auto &p : P.pending) {
+    cuda_check(cudaEventSynchronize(p.e1), "cudaEventSynchronize");
+    float ms = 0;
+    cuda_check(cudaEventElapsedTime(&ms, p.e0, p.e1), "cudaEventElapsedTime");
+    stn_kernel_profile &t = P.totals[p.kind];
+    t.kind = p.kind;
+    t.launches++;
+    t.ms += ms;
+    t.bytes += p.bytes;
+    t.flops += p.flops;
+    P.event_pool.push_back(p.e0);
+    P.event_pool.push_back(p.e1);
+  }
+  P.pending.clear();
+}
+
+void *elem_ptr(const stn_plan &P, void *base, int64_t elems) {
+  return static_cast<unsigned char *>(base) + size_t(elems) * P.esize;
+}
+
+struct Resolved {
+  const void *ptr;
+  int64_t bs;
+};
+
+Resolved resolve(stn_plan &P, const Ref &r, const stn_cache *cache, int nb) {
+  switch (r.kind) {
+    case Src::ConstLeaf:
+      return {elem_ptr(P, P.consts.ptr, r.off), 0};
+    case Src::Cache:
+    case Src::Persist:
+      return {elem_ptr(P, cache->storage.ptr, r.off), 0};
+    case Src::Arena:
+    case Src::SliceLeaf:
+      return {elem_ptr(P, P.arena.ptr, r.off * nb), r.size};
+  }
+  return {nullptr, 0};
+}
+
+template <class R>
+void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaStream_t st) {
+  const StepPlan &sp = P.steps[op.step];
+  Resolved a = resolve(P, op.a, cache, nb), b = resolve(P, op.b, cache, nb);
+  Resolved o = resolve(P, op.out, cache, nb);
+  void *out = const_cast<void *>(o.ptr);
+  const bool exact = P.mode == STN_MODE_EXACT;
+  const double es = double(P.esize);
+  // algorithmic traffic: slice-invariant operands once per batch
+  auto reads = [&](const Resolved &r, int64_t size) { return es * size * (r.bs ? nb : 1); };
+  const double io_bytes = reads(a, sp.lsize) + reads(b, sp.rsize) + es * sp.osize * nb;
+  const double flops = 8.0 * double(sp.d.mults) * nb;
+  ProfScope prof(P, st);
+  switch (sp.kern) {
+    case Kern::Generic: {
+      stn::BatchPtrs p{a.ptr, b.ptr, out, a.bs, b.bs, o.bs, nb};
+      cuda_check(stn::launch_generic<R>(sp.geo, p, exact, st), "generic kernel");
+      prof.done(STN_KERNEL_GENERIC, io_bytes, flops);
+      break;
+    }
+    case Kern::Absorb: {
+      const Resolved &x = sp.x_is_lhs ? a : b;
+      const Resolved &w = sp.x_is_lhs ? b : a;
+      stn::BatchPtrs p{x.ptr, w.ptr, out, x.bs, w.bs, o.bs, nb};
+      cuda_check(stn::launch_absorb(sp.ag, p, exact, st), "absorb kernel");
+      prof.done(STN_KERNEL_ABSORB, io_bytes, flops);
+      break;
+    }
+    case Kern::GemmSimt:
+    case Kern::GemmTc: {
+      const void *ga = a.ptr, *gb = b.ptr;
+      int64_t ga_bs = a.bs, gb_bs = b.bs;
+      if (!sp.a_id) {
+        void *dst = elem_ptr(P, P.arena.ptr, op.scr_a * nb);
+        cuda_check(stn::launch_permute<R>(sp.pa, a.ptr, dst, a.bs, sp.lsize, nb, st), "permute");
+        prof.done(STN_KERNEL_PERMUTE, 2 * es * sp.lsize * nb, 0);
+        ga = dst;
+        ga_bs = sp.lsize;
+      }
+      if (!sp.b_id) {
+        void *dst = elem_ptr(P, P.arena.ptr, op.scr_b * nb);
+        cuda_check(stn::launch_permute<R>(sp.pb, b.ptr, dst, b.bs, sp.rsize, nb, st), "permute");
+        prof.done(STN_KERNEL_PERMUTE, 2 * es * sp.rsize * nb, 0);
+        gb = dst;
+        gb_bs = sp.rsize;
+      }
+      void *gc = sp.c_id ? out : elem_ptr(P, P.arena.ptr, op.scr_c * nb);
+      int64_t gc_bs = sp.c_id ? o.bs : sp.osize;
+      stn::BatchPtrs p{ga, gb, gc, ga_bs, gb_bs, gc_bs, nb};
+      const double gbytes = es * (sp.lsize * (ga_bs ? nb : 1) + sp.rsize * (gb_bs ? nb : 1) +
+                                  double(sp.osize) * nb);
+      bool done = false;
+      if (sp.kern == Kern::GemmTc) {
+        size_t ws = stn::gemm_tc_workspace_bytes(sp.gs);
+        P.tc_workspace.reserve(std::max<size_t>(ws, 16));
+        cudaError_t e = stn::launch_gemm_tc(sp.gs, p, P.tc_workspace.ptr, ws, st);
+        if (e == cudaSuccess) {
+          done = true;
+          prof.done(STN_KERNEL_GEMM_TC, gbytes, flops);
+        } else {
+          require(e == cudaErrorNotSupported, STN_ERR_CUDA,
+                  std::string("tcgen05 gemm: ") + cudaGetErrorString(e));
+          cudaGetLastError();
+        }
+      }
+      if (!done) {
+        cuda_check(stn::launch_gemm_simt<R>(sp.gs, p, exact, st), "gemm kernel");
+        prof.done(STN_KERNEL_GEMM_SIMT, gbytes, flops);
+      }
+      if (!sp.c_id) {
+        cuda_check(stn::launch_permute<R>(sp.pc, gc, out, sp.osize, o.bs, nb, st), "permute");
+        prof.done(STN_KERNEL_PERMUTE, 2 * es * sp.osize * nb, 0);
+      }
+      break;
+    }
+  }
+}
+
+int auto_batch(const stn_plan &P, const Program &prog) {
+  if (P.max_batch > 0) return P.max_batch;
+  const int64_t per = std::max<int64_t>(prog.arena_elems, 1) * int64_t(P.esize);
+  int64_t nb = (int64_t(256) << 20) / per;  // aim for >= 256 MiB of work per pass
+  return int(std::max<int64_t>(1, std::min<int64_t>(nb, 256)));
+}
+
+// Runs `n` slices (digits row-major n x n_sliced on the host) of `prog`.
+void run_batch(stn_plan &P, Program &prog, const stn_cache *cache, const int32_t *digits_host,
+               int n, cudaStream_t st, double *acc, double *per_slice) {
+  const size_t arena_bytes = size_t(std::max<int64_t>(prog.arena_elems, 1)) * n * P.esize;
+  P.arena.reserve(arena_bytes);
+  const int ns = int(P.sliced_dims.size());
+  if (ns > 0 && !prog.slice_leaves.empty()) {
+    P.digits.reserve(size_t(n) * ns * 4);
+    cuda_check(cudaMemcpyAsync(P.digits.ptr, digits_host, size_t(n) * ns * 4,
+                               cudaMemcpyHostToDevice, st),
+               "digits upload");
+  }
+  if (!prog.slice_leaves.empty()) {
+    ProfScope prof(P, st);
+    if (P.precision == STN_SINGLE)
+      cuda_check(stn::launch_leaf_gather<float>(prog.table, P.arena.ptr, P.digits.as<int32_t>(),
+                                                n, st),
+                 "leaf gather");
+    else
+      cuda_check(stn::launch_leaf_gather<double>(prog.table, P.arena.ptr, P.digits.as<int32_t>(),
+                                                 n, st),
+                 "leaf gather");
+    prof.done(STN_KERNEL_LEAF, double(prog.table.total_out) * n * (16 + P.esize), 0);
+  }
+  for (const Op &op : prog.ops) {
+    if (P.precision == STN_SINGLE)
+      launch_op<float>(P, op, cache, n, st);
+    else
+      launch_op<double>(P, op, cache, n, st);
+  }
+  if (prog.has_root && (acc || per_slice)) {
+    ProfScope prof(P, st);
+    Resolved r = resolve(P, prog.root, cache, n);
+    if (P.precision == STN_SINGLE)
+      cuda_check(stn::launch_root_accumulate<float>(r.ptr, r.bs, P.out_elements, n, acc,
+                                                    per_slice, st),
+                 "root accumulate");
+    else
+      cuda_check(stn::launch_root_accumulate<double>(r.ptr, r.bs, P.out_elements, n, acc,
+                                                     per_slice, st),
+                 "root accumulate");
+    prof.done(STN_KERNEL_ROOT, double(P.out_elements) * n * (P.esize + 16), 0);
+  }
+}
+
+void decode(const stn_plan &P, uint64_t a, int32_t *digits) {
+  uint64_t rest = a;
+  for (size_t i = P.sliced_dims.size(); i-- > 0;) {
+    uint64_t d = uint64_t(P.sliced_dims[i]);
+    digits[i] = int32_t(rest % d);
+    rest /= d;
+  }
+}
+
+void check_cache(const stn_plan &P, const stn_cache *cache) {
+  if (!cache) return;
+  require(cache->identity == P.identity && cache->plan == &P, STN_ERR_SUBTASK_FAILURE,
+          "branch cache belongs to a different plan");
+  require(cache->leaf_epoch == P.leaf_epoch, STN_ERR_SUBTASK_FAILURE,
+          "branch cache is stale: leaf values feeding branch steps changed");
+}
+
+// Runs slices given by a digit generator over [0, n) in batches.
+template <class DigitsOf>
+void run_slices_impl(stn_plan &P, const stn_cache *cache, uint64_t n, DigitsOf &&digits_of,
+                     cudaStream_t st, double *acc, double *per_slice,
+                     std::vector<double> *batch_ms = nullptr) {
+  Program &prog = cache ? P.with_cache : P.no_cache;
+  const int ns = int(P.sliced_dims.size());
+  const int nb = auto_batch(P, prog);
+  std::vector<int32_t> dig;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (batch_ms) {
+    cuda_check(cudaEventCreate(&e0), "event");
+    cuda_check(cudaEventCreate(&e1), "event");
+  }
+  for (uint64_t a0 = 0; a0 < n; a0 += uint64_t(nb)) {
+    const int cnt = int(std::min<uint64_t>(uint64_t(nb), n - a0));
+    dig.assign(size_t(cnt) * std::max(ns, 1), 0);
+    for (int i = 0; i < cnt; ++i) digits_of(a0 + i, dig.data() + size_t(i) * ns);
+    if (batch_ms) cuda_check(cudaEventRecord(e0, st), "event");
+    run_batch(P, prog, cache, dig.data(), cnt, st, acc,
+              per_slice ? per_slice + 2 * size_t(P.out_elements) * a0 : nullptr);
+    if (batch_ms) {
+      cuda_check(cudaEventRecord(e1, st), "event");
+      cuda_check(cudaEventSynchronize(e1), "event sync");
+      float ms = 0;
+      cuda_check(cudaEventElapsedTime(&ms, e0, e1), "event time");
+      for (int i = 0; i < cnt; ++i) batch_ms->push_back(double(ms) / cnt);
+    }
+  }
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+}
+
+void build_cache(stn_plan &P, cudaStream_t st, stn_cache *c) {
+  c->identity = P.identity;
+  c->leaf_epoch = P.leaf_epoch;
+  c->plan = &P;
+  c->storage.reserve(size_t(std::max<int64_t>(P.cache_elems, 1)) * P.esize);
+  for (auto &sp : P.steps)
+    if (sp.d.is_branch) c->mults += sp.d.mults;
+  for (auto &[node, off] : P.cache_off) c->elements += uint64_t(P.nodes[node].size);
+  run_batch(P, P.build, c, nullptr, 1, st, nullptr, nullptr);
+}
+
+void run_one(stn_plan &P, const int32_t *digits, const stn_cache *cache, cudaStream_t st,
+             double *out_host, stn_subtask_info *info) {
+  check_cache(P, cache);
+  Program &prog = cache ? P.with_cache : P.no_cache;
+  P.scratch_out.reserve(16 * size_t(P.out_elements));
+  std::vector<int32_t> dig(digits, digits + P.sliced_dims.size());
+  if (dig.empty()) dig.push_back(0);
+  run_batch(P, prog, cache, dig.data(), 1, st, nullptr, P.scratch_out.as<double>());
+  cuda_check(cudaMemcpyAsync(out_host, P.scratch_out.ptr, 16 * size_t(P.out_elements),
+                             cudaMemcpyDeviceToHost, st),
+             "result download");
+  cuda_check(cudaStreamSynchronize(st), "stream sync");
+  if (info) {
+    info->step_count = int32_t(prog.ops.size());
+    info->mults = prog.mults;
+    info->peak_elements = prog.peak;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+void stn_set_error_c(const char *msg) { g_last_error = msg ? msg : ""; }
+
+const char *stn_version(void) { return "stn_exec 0.1 (sm_100a)"; }
+int stn_abi_version(void) { return STN_ABI_VERSION; }
+const char *stn_last_error(void) { return g_last_error.c_str(); }
+
+const char *stn_status_name(int status) {
+  static const char *kinds[] = {"MalformedNetwork", "CapExceeded",       "OpenEdgeSliced",
+                                "IndexOutOfRange",  "MissingParams",     "SyntaxError",
+                                "InvariantViolation", "QubitCoverage",   "LayoutTooSmall",
+                                "Infeasible",       "EdgeNotFound",      "SchemaError",
+                                "Stuck",            "HashMismatch",      "WidthExceedsBudget",
+                                "SubtaskFailure",   "MissingResult",     "ChecksumMismatch",
+                                "EmptySamples"};
+  if (status == 0) return "Ok";
+  if (status >= 1 && status <= 19) return kinds[status - 1];
+  switch (status) {
+    case STN_ERR_CUDA: return "CudaError";
+    case STN_ERR_INVALID_ARGUMENT: return "InvalidArgument";
+    case STN_ERR_OUT_OF_MEMORY: return "OutOfMemory";
+    case STN_ERR_NO_DEVICE: return "NoDevice";
+    case STN_ERR_IO: return "IOError";
+  }
+  return "Unknown";
+}
+
+int stn_plan_create(const stn_plan_desc *desc, int device, int mode, stn_plan **out) {
+  if (!out) return set_error(STN_ERR_INVALID_ARGUMENT, "NULL output pointer");
+  *out = nullptr;
+  auto P = std::make_unique<stn_plan>();
+  int st = guarded([&] { create_plan(desc, device, mode, P.get()); });
+  if (st == STN_OK) *out = P.release();
+  return st;
+}
+
+int stn_plan_destroy(stn_plan *plan) {
+  if (plan) {
+    cudaSetDevice(plan->device);
+    delete plan;
+  }
+  return STN_OK;
+}
+
+int stn_plan_get_info(const stn_plan *P, stn_plan_info *info) {
+  if (!P || !info) return set_error(STN_ERR_INVALID_ARGUMENT, "NULL argument");
+  memset(info, 0, sizeof *info);
+  info->identity = P->identity;
+  info->subtasks = P->subtasks;
+  info->n_sliced = int32_t(P->sliced_dims.size());
+  info->out_rank = int32_t(P->out_dims.size());
+  info->out_elements = P->out_elements;
+  for (size_t i = 0; i < P->out_dims.size() && i < 64; ++i) info->out_dims[i] = P->out_dims[i];
+  info->per_slice_steps = int32_t(P->with_cache.ops.size());
+  info->per_slice_mults = P->with_cache.mults;
+  for (auto &sp : P->steps)
+    if (sp.d.is_branch) info->branch_mults += sp.d.mults;
+  info->peak_elements = P->with_cache.peak;
+  info->arena_bytes_per_slice = uint64_t(P->with_cache.arena_elems) * P->esize;
+  info->cache_bytes = uint64_t(P->cache_elems) * P->esize;
+  for (auto &op : P->with_cache.ops) {
+    Kern k = P->steps[op.step].kern;
+    if (k == Kern::GemmTc) info->steps_tensor_core++;
+    else if (k == Kern::Absorb) info->steps_absorb++;
+    else info->steps_generic++;
+  }
+  return STN_OK;
+}
+
+int stn_plan_set_leaf_values(stn_plan *P, int32_t vertex, const double *values, int64_t n) {
+  if (!P || !values) return set_error(STN_ERR_INVALID_ARGUMENT, "NULL argument");
+  return guarded([&] {
+    auto it = P->leaf_of_vertex.find(vertex);
+    require(it != P->leaf_of_vertex.end(), STN_ERR_INDEX_OUT_OF_RANGE,
+            "vertex " + std::to_string(vertex) + " is not a leaf of this plan");
+    const int li = it->second;
+    require(int64_t(P->leaf_values[li].size()) == 2 * n, STN_ERR_MALFORMED_NETWORK,
+            "tensor data length does not match the vertex tensor");
+    cuda_check(cudaSetDevice(P->device), "cudaSetDevice");
+    std::copy(values, values + 2 * n, P->leaf_values[li].begin());
+    const int node = P->leaf_desc[li].node;
+    if (P->nodes[node].sliced_leaf)
+      upload_sliced_values(*P);
+    else
+      upload_consts(*P);
+    if (P->leaf_feeds_branch[li]) P->leaf_epoch++;
+  });
+}
+
+int stn_plan_set_max_batch(stn_plan *P, int32_t max_batch) {
+  if (!P || max_batch < 0) return set_error(STN_ERR_INVALID_ARGUMENT, "bad argument");
+  P->max_batch = max_batch;
+  return STN_OK;
+}
+
+int stn_plan_set_profiling(stn_plan *P, int enable) {
+  if (!P) return set_error(STN_ERR_INVALID_ARGUMENT, "NULL plan");
+  P->profiling = enable != 0;
+  return STN_OK;
+}
+
+int stn_plan_get_profile(stn_plan *P, stn_kernel_profile *out) {
+  if (!P || !out) return set_error(STN_ERR_INVALID_ARGUMENT, "NULL argument");
+  return guarded([&] {
+    cuda_check(cudaSetDevice(P->device), "cudaSetDevice");
+    collect_profile(*P);
+    for (int k = 0; k < STN_KERNEL_KINDS; ++k) {
+      out[k] = P->totals[k];
+      out[k].kind = k;
+    }
+  });
+}
+
+int stn_plan_reset_profile(stn_plan *P) {
+  if (!P) return set_error(STN_ERR_INVALID_ARGUMENT, "NULL plan");
+  return guarded([&] {
+    collect_profile(*P);
+    for (auto &t : P->totals) t = stn_kernel_profile{};
+  });
+}
+
+int stn_cache_build(stn_plan *P, void *stream, stn_cache **out) {
+  if (!P || !out) return set_error(STN_ERR_INVALID_ARGUMENT, "NULL argument");
+  *out = nullptr;
+  auto c = std::make_unique<stn_cache>();
+  int st = guarded([&] {
+    cuda_check(cudaSetDevice(P->device), "cudaSetDevice");
+    build_cache(*P, static_cast<cudaStream_t>(stream), c.get());
+    cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "cache build");
+  });
+  if (st == STN_OK) *out = c.release();
+  return st;
+}
+
+int stn_cache_destroy(stn_cache *c) {
+  delete c;
+  return STN_OK;
+}
+
+int stn_cache_info(const stn_cache *c, uint64_t *identity, uint64_t *mults, uint64_t *elements) {
+  if (!c) return set_error(STN_ERR_INVALID_ARGUMENT, "NULL cache");
+  if (identity) *identity = c->identity;
+  if (mults) *mults = c->mults;
+  if (elements) *elements = c->elements;
+  return STN_OK;
+}
+
+int stn_run_subtask(stn_plan *P, uint64_t assignment, const stn_cache *cache, void *stream,
+                    double *out_host, stn_subtask_info *info) {
+  if (!P || !out_host) return set_error(STN_ERR_INVALID_ARGUMENT, "NULL argument");
+  return guarded([&] {
+    require(assignment < P->subtasks, STN_ERR_SUBTASK_FAILURE, "assignment out of range");
+    cuda_check(cudaSetDevice(P->device), "cudaSetDevice");
+    std::vector<int32_t> dig(std::max<size_t>(P->sliced_dims.size(), 1), 0);
+    decode(*P, assignment, dig.data());
+    run_one(*P, dig.data(), cache, static_cast<cudaStream_t>(stream), out_host, info);
+    if (info) info->assignment = assignment;
+  });
+}
+
+int stn_run_subtask_digits(stn_plan *P, const int32_t *digits, const stn_cache *cache,
+                           void *stream, double *out_host, stn_subtask_info *info) {
+  if (!P || !out_host || (!digits && !P->sliced_dims.empty()))
+    return set_error(STN_ERR_INVALID_ARGUMENT, "NULL argument");
+  return guarded([&] {
+    for (size_t i = 0; i < P->sliced_dims.size(); ++i)
+      require(digits[i] >= 0 && digits[i] < P->sliced_dims[i], STN_ERR_INDEX_OUT_OF_RANGE,
+              "slice digit out of range");
+    cuda_check(cudaSetDevice(P->device), "cudaSetDevice");
+    int32_t zero = 0;
+    run_one(*P, digits ? digits : &zero, cache, static_cast<cudaStream_t>(stream), out_host, info);
+    if (info) info->assignment = 0;
+  });
+}
+
+int stn_run_slices(stn_plan *P, const stn_cache *cache, uint64_t lo, uint64_t hi, void *stream,
+                   double *acc_dev, double *per_slice_dev) {
+  if (!P) return set_error(STN_ERR_INVALID_ARGUMENT, "NULL plan");
+  return guarded([&] {
+    require(lo <= hi && hi <= P->subtasks, STN_ERR_SUBTASK_FAILURE, "assignment out of range");
+    require(cache != nullptr, STN_ERR_INVALID_ARGUMENT, "stn_run_slices needs a branch cache");
+    check_cache(*P, cache);
+    cuda_check(cudaSetDevice(P->device), "cudaSetDevice");
+    run_slices_impl(
+        *P, cache, hi - lo, [&](uint64_t i, int32_t *d) { decode(*P, lo + i, d); },
+        static_cast<cudaStream_t>(stream), acc_dev, per_slice_dev);
+  });
+}
+
+int stn_run_slices_digits(stn_plan *P, const stn_cache *cache, const int32_t *digits,
+                          uint64_t n_slices, void *stream, double *acc_dev,
+                          double *per_slice_dev) {
+  if (!P || (!digits && n_slices && !P->sliced_dims.empty()))
+    return set_error(STN_ERR_INVALID_ARGUMENT, "NULL argument");
+  return guarded([&] {
+    require(cache != nullptr, STN_ERR_INVALID_ARGUMENT, "stn_run_slices needs a branch cache");
+    check_cache(*P, cache);
+    const size_t ns = P->sliced_dims.size();
+    for (uint64_t i = 0; i < n_slices * ns; ++i)
+      require(digits[i] >= 0 && digits[i] < P->sliced_dims[i % ns], STN_ERR_INDEX_OUT_OF_RANGE,
+              "slice digit out of range");
+    cuda_check(cudaSetDevice(P->device), "cudaSetDevice");
+    run_slices_impl(
+        *P, cache, n_slices,
+        [&](uint64_t i, int32_t *d) { std::copy(digits + i * ns, digits + (i + 1) * ns, d); },
+        static_cast<cudaStream_t>(stream), acc_dev, per_slice_dev);
+  });
+}
+
+int stn_run_scheme(stn_plan *P, int parallelism, double *out_host, stn_run_report *rep) {
+  if (!P || !out_host) return set_error(STN_ERR_INVALID_ARGUMENT, "NULL argument");
+  return guarded([&] {
+    require(parallelism >= 1, STN_ERR_SUBTASK_FAILURE, "parallelism must be positive");
+    require(P->subtasks >= 1, STN_ERR_SUBTASK_FAILURE,
+            "plan has no enumerable subtasks (uint64 subtask count overflowed)");
+    cuda_check(cudaSetDevice(P->device), "cudaSetDevice");
+    auto t0 = std::chrono::steady_clock::now();
+    P->kernel_launches = 0;
+    cudaStream_t st = nullptr;
+    stn_cache cache;
+    build_cache(*P, st, &cache);
+    DevBuf acc;
+    acc.reserve(16 * size_t(P->out_elements));
+    cuda_check(cudaMemsetAsync(acc.ptr, 0, 16 * size_t(P->out_elements), st), "memset");
+    std::vector<double> ms;
+    run_slices_impl(
+        *P, &cache, P->subtasks, [&](uint64_t i, int32_t *d) { decode(*P, i, d); }, st,
+        acc.as<double>(), nullptr, &ms);
+    cuda_check(cudaMemcpyAsync(out_host, acc.ptr, 16 * size_t(P->out_elements),
+                               cudaMemcpyDeviceToHost, st),
+               "result download");
+    cuda_check(cudaStreamSynchronize(st), "stream sync");
+    auto t1 = std::chrono::steady_clock::now();
+    if (rep) {
+      memset(rep, 0, sizeof *rep);
+      rep->subtasks = P->subtasks;
+      rep->branch_mults = cache.mults;
+      rep->mult_count = cache.mults + P->with_cache.mults * P->subtasks;
+      rep->wall_seconds = std::chrono::duration<double>(t1 - t0).count();
+      std::sort(ms.begin(), ms.end());
+      auto q = [&](double f) {
+        if (ms.empty()) return 0.0;
+        size_t i = size_t(f * double(ms.size() - 1) + 0.5);
+        return ms[std::min(i, ms.size() - 1)];
+      };
+      rep->p50_ms = q(0.5);
+      rep->p90_ms = q(0.9);
+      rep->p99_ms = q(0.99);
+      rep->parallelism = parallelism;
+      rep->precision = P->precision;
+      rep->peak_elements = P->with_cache.peak;
+      rep->merged_groups = P->merged_groups;
+      rep->slices_per_batch = auto_batch(*P, P->with_cache);
+      rep->kernel_launches = P->kernel_launches;
+    }
+  });
+}
+
+int stn_sum_slices_ordered(const double *per_slice_dev, uint64_t n_slices, int64_t out_elements,
+                           double *out_dev, void *stream) {
+  if (!per_slice_dev || !out_dev) return set_error(STN_ERR_INVALID_ARGUMENT, "NULL argument");
+  return guarded([&] {
+    cuda_check(stn::launch_sum_ordered(per_slice_dev, n_slices, out_elements, out_dev,
+                                       static_cast<cudaStream_t>(stream)),
+               "ordered sum");
+  });
+}
+
+}  // extern "C"

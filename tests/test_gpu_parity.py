@@ -1,0 +1,203 @@
+"""GPU parity of the B200 executor against the reference (through the C ABI).
+
+EXACT mode reproduces the reference loop order and rounding, so it must be
+bitwise identical to the reference CPU executor's own outputs (tests/golden,
+written by the reference via oracle/_ref/ref_tool). FAST mode (tcgen05
+split-TF32 GEMMs, FMA SIMT kernels) must agree within the stated tolerance:
+
+    |gpu - ref| <= RTOL * max|ref|,  RTOL = 1e-5      (single precision)
+
+the north star's amplitude tolerance; the reference's own single-precision
+path is ~2e-6 from exact at these sizes."""
+import numpy as np
+import pytest
+
+from golden_io import bits, cases, meta, plan_path, read_ref
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _needs_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def load(name, precision, mode):
+    from paper_2005_06787_b200 import ExecutablePlan
+    return ExecutablePlan.load(plan_path(name, precision), device=0, mode=mode)
+
+
+def rel_err(got, want):
+    scale = max(np.abs(want).max(), 1e-300)
+    return float(np.abs(np.asarray(got).ravel() - np.asarray(want).ravel()).max() / scale)
+
+
+SMALL = [c for c in cases() if not c.startswith(("cfg3", "cfg4", "cfg5"))]
+
+
+@pytest.mark.parametrize("precision", ["single", "double"])
+@pytest.mark.parametrize("name", SMALL)
+def test_exact_mode_is_bitwise_reference(name, precision):
+    from paper_2005_06787_b200 import build_branch_cache, run_scheme, run_subtask
+    try:
+        asg, vals, s, bk, info = read_ref(name, precision)
+    except FileNotFoundError:
+        pytest.skip("no reference values for this case/precision")
+    plan = load(name, precision, "exact")
+    cache = build_branch_cache(plan)
+    assert cache.plan_identity == plan.identity
+    assert (cache.mults, cache.elements) == (info["cache"]["mults"], info["cache"]["elements"])
+    for a, want in zip(asg, vals):
+        r = run_subtask(plan, int(a), cache)
+        assert np.array_equal(bits(r.value.ravel()), bits(want)), (name, precision, int(a))
+    assert (r.step_count, r.mults, r.peak_elements) == bk
+    # without a cache every step runs for the assignment; bitwise the same value
+    nc = run_subtask(plan, int(asg[0]), None)
+    assert np.array_equal(bits(nc.value.ravel()), bits(vals[0]))
+    u = info["uncached"]
+    assert (nc.step_count, nc.mults, nc.peak_elements) == (
+        u["step_count"], u["mults"], u["peak_elements"])
+    if s is not None:
+        total, rep = run_scheme(plan, 1)
+        assert np.array_equal(bits(total.ravel()), bits(s))
+        assert rep.subtasks == plan.subtasks
+        assert rep.kernel_launches > 0
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_fast_mode_within_tolerance(name):
+    from paper_2005_06787_b200 import build_branch_cache, run_scheme, run_subtask
+    try:
+        asg, vals, s, _, _ = read_ref(name, "single")
+    except FileNotFoundError:
+        pytest.skip("no reference values")
+    plan = load(name, "single", "fast")
+    cache = build_branch_cache(plan)
+    for a, want in zip(asg, vals):
+        got = run_subtask(plan, int(a), cache).value
+        assert rel_err(got, want) <= RTOL, (name, int(a))
+    if s is not None:
+        total, _ = run_scheme(plan, 1)
+        assert rel_err(total, s) <= RTOL
+
+
+@pytest.mark.parametrize("name", ["rt_grid3x4_m8_sliced", "cfg1_grid4x5_m14"])
+def test_fast_single_vs_reference_double(name):
+    """Accuracy against the reference's double path (the truth)."""
+    from paper_2005_06787_b200 import run_scheme
+    _, dv, ds, _, _ = read_ref(name, "double")
+    _, sv, ss, _, _ = read_ref(name, "single")
+    total, _ = run_scheme(load(name, "single", "fast"), 1)
+    ref_single_err = rel_err(ss, ds)
+    assert rel_err(total, ds) <= max(RTOL, 2 * ref_single_err)
+
+
+def test_results_bit_stable_across_parallelism_and_batching():
+    """runtime.hpp:552-554 / test_runtime.cpp:258-277: same bits for any
+    parallelism; here also for any slice batch size."""
+    from paper_2005_06787_b200 import run_scheme
+    plan = load("rt_grid3x4_m8_sliced", "single", "fast")
+    v1, r1 = run_scheme(plan, 1)
+    v8, r8 = run_scheme(plan, 8)
+    assert np.array_equal(bits(v1.ravel()), bits(v8.ravel()))
+    assert r1.deterministic_json() == r8.deterministic_json()
+    for nb in (1, 3, 32):
+        plan.set_max_batch(nb)
+        vb, _ = run_scheme(plan, 1)
+        assert np.array_equal(bits(vb.ravel()), bits(v1.ravel())), nb
+
+
+def test_run_slices_device_accumulation_matches_scheme():
+    import torch
+    from paper_2005_06787_b200 import build_branch_cache, run_scheme, run_slices, sum_slices_ordered
+    plan = load("rt_grid3x4_m8_sliced", "single", "fast")
+    cache = build_branch_cache(plan)
+    n, oe = plan.subtasks, plan.out_elements
+    acc = torch.zeros(2 * oe, dtype=torch.float64, device="cuda")
+    per = torch.zeros((n, 2 * oe), dtype=torch.float64, device="cuda")
+    run_slices(plan, cache, 0, n // 2, acc=acc, per_slice=per[: n // 2])
+    run_slices(plan, cache, n // 2, n, acc=acc, per_slice=per[n // 2:])
+    out = torch.zeros(2 * oe, dtype=torch.float64, device="cuda")
+    sum_slices_ordered(per, n, oe, out)
+    torch.cuda.synchronize()
+    total, _ = run_scheme(plan, 1)
+    want = total.ravel().view(np.float64)
+    assert np.array_equal(acc.cpu().numpy().view(np.uint64), want.view(np.uint64))
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), want.view(np.uint64))
+
+
+def test_digit_vector_entry_point_matches_assignment():
+    from paper_2005_06787_b200 import build_branch_cache, run_subtask, run_subtask_digits
+    from oracle.oracle import OraclePlan
+    plan = load("cfg1_grid4x5_m14", "single", "exact")
+    ref = OraclePlan(plan_path("cfg1_grid4x5_m14", "single"))
+    cache = build_branch_cache(plan)
+    for a in (0, 5, 15):
+        r1 = run_subtask(plan, a, cache)
+        r2 = run_subtask_digits(plan, ref.digits(a), cache)
+        assert np.array_equal(bits(r1.value.ravel()), bits(r2.value.ravel()))
+
+
+def test_errors_mirror_the_reference():
+    from paper_2005_06787_b200 import StnError, build_branch_cache, run_subtask
+    plan = load("rt_cache_sliced", "single", "fast")
+    other = load("rt_hyper_sliced", "single", "fast")
+    cache = build_branch_cache(plan)
+    with pytest.raises(StnError) as e:  # runtime.hpp:504
+        run_subtask(plan, plan.subtasks, cache)
+    assert e.value.kind == "SubtaskFailure"
+    with pytest.raises(StnError) as e:  # runtime.hpp:505-507
+        run_subtask(plan, 0, build_branch_cache(other))
+    assert e.value.kind == "SubtaskFailure"
+
+
+def test_leaf_update_invalidates_cache_and_changes_values():
+    """The sampler pokes projector tensors between batches (sampler.hpp:206-213)."""
+    from paper_2005_06787_b200 import StnError, build_branch_cache, run_subtask
+    from oracle.oracle import OraclePlan
+    name = "rt_grid3x4_m8_sliced"
+    plan = load(name, "single", "exact")
+    cache = build_branch_cache(plan)
+    ref = OraclePlan(plan_path(name, "single"))
+    d = ref.desc.contents
+    branch_inputs = set()
+    for i in range(d.n_steps):
+        st = d.steps[i]
+        if st.is_branch:
+            branch_inputs.update((st.lhs, st.rhs))
+    # flip the output projectors (rank-1 [1,0] leaves after the 12 input kets)
+    flipped, stale = 0, False
+    for i in range(d.n_leaves):
+        L = d.leaves[i]
+        if L.rank == 1 and L.n_sliced == 0 and L.vertex >= 12 and L.values[0] == 1.0:
+            plan.set_leaf_values(L.vertex, np.array([0, 1], np.complex128))
+            L.values[0], L.values[2] = 0.0, 1.0
+            flipped += 1
+            stale |= L.node in branch_inputs
+    assert flipped > 0
+    if stale:
+        with pytest.raises(StnError) as e:
+            run_subtask(plan, 0, cache)
+        assert e.value.kind == "SubtaskFailure"
+    fresh = build_branch_cache(plan)
+    got = run_subtask(plan, 0, fresh).value.ravel()
+    want, _ = ref.run_subtask(0, ref.build_cache())
+    assert np.array_equal(bits(got), bits(want))
+
+
+@pytest.mark.parametrize("name", ["cfg3_syc53_m12"])
+def test_large_config_fast_vs_exact(name):
+    """53-qubit slices: the CPU reference needs ~15 min per slice, so parity
+    runs against the exact mode (bitwise-equal to the reference on every case
+    above) on a few slices."""
+    from paper_2005_06787_b200 import build_branch_cache, run_subtask
+    fast = load(name, "single", "fast")
+    exact = load(name, "single", "exact")
+    cf, ce = build_branch_cache(fast), build_branch_cache(exact)
+    for a in (0, fast.subtasks - 1):
+        vf = run_subtask(fast, a, cf).value
+        ve = run_subtask(exact, a, ce).value
+        assert rel_err(vf, ve) <= RTOL, a

@@ -1,0 +1,77 @@
+"""The CPU oracle (oracle/stn_oracle.c) pinned against outputs of the reference
+itself (tests/golden, produced by the reference CPU executor via
+oracle/_ref/ref_tool). Bitwise: the oracle restates runtime.hpp operation for
+operation, so its per-slice values, scheme sums and bookkeeping must be
+identical, in both precisions."""
+import os
+
+import numpy as np
+import pytest
+
+from golden_io import bits, cases, plan_path, read_ref
+from oracle.oracle import OraclePlan
+
+
+@pytest.mark.parametrize("precision", ["single", "double"])
+@pytest.mark.parametrize("name", cases())
+def test_oracle_matches_reference_bitwise(name, precision):
+    if name.startswith("cfg2") and not os.environ.get("STN_SLOW"):
+        pytest.skip("cfg2 takes ~200 s per slice on the CPU oracle; set STN_SLOW=1")
+    try:
+        asg, vals, s, bk, info = read_ref(name, precision)
+    except FileNotFoundError:
+        pytest.skip("no reference values recorded for this case/precision")
+    p = OraclePlan(plan_path(name, precision))
+    cache = p.build_cache()
+    for a, want in zip(asg, vals):
+        got, sinfo = p.run_subtask(int(a), cache)
+        assert np.array_equal(bits(got), bits(want)), (name, precision, int(a))
+    # SubtaskResult bookkeeping with a cache (runtime.hpp:444-446)
+    assert (sinfo.step_count, sinfo.mults, sinfo.peak_elements) == bk
+    # ... and without one (every step runs, runtime.hpp:440)
+    nc, ninfo = p.run_subtask(int(asg[0]), None)
+    assert np.array_equal(bits(nc), bits(vals[0]))  # cache is bitwise sound
+    u = info["uncached"]
+    assert (ninfo.step_count, ninfo.mults, ninfo.peak_elements) == (
+        u["step_count"], u["mults"], u["peak_elements"])
+    if s is not None:
+        _, got_sum = p.run_slices(0, p.subtasks, cache, threads=4)
+        assert np.array_equal(bits(got_sum), bits(s))
+
+
+def test_oracle_digits_match_mixed_radix_decode():
+    # runtime.hpp:371-378: first sliced edge most significant
+    p = OraclePlan(plan_path("cfg1_grid4x5_m14", "single"))
+    dims = p.sliced_dims
+    for a in range(p.subtasks):
+        d = p.digits(a)
+        rebuilt = 0
+        for x, dim in zip(d, dims):
+            rebuilt = rebuilt * dim + x
+        assert rebuilt == a
+
+
+def test_oracle_rejects_out_of_range_and_foreign_cache():
+    from paper_2005_06787_b200.abi import StnError
+    p = OraclePlan(plan_path("rt_cache_sliced", "single"))
+    with pytest.raises(StnError) as e:
+        p.run_subtask(p.subtasks)
+    assert e.value.kind == "SubtaskFailure"
+    other = OraclePlan(plan_path("rt_hyper_sliced", "single"))
+    c = other.build_cache()
+    with pytest.raises(StnError) as e:
+        p.run_subtask(0, c)
+    assert e.value.kind == "SubtaskFailure"
+
+
+def test_feynman_value_of_random_networks():
+    """Unmerged/unsliced double plans equal the Feynman sum (test_runtime.cpp:54-72)."""
+    from golden_io import meta
+    for name in ("rt_hyper_unmerged", "rt_unsliced", "rt_hyper_sliced", "rt_mixed_dims"):
+        m = meta(name)
+        fv = np.array(m["feynman_value"], np.float64).view(np.complex128)
+        p = OraclePlan(plan_path(name, "double"))
+        c = p.build_cache()
+        _, s = p.run_slices(0, p.subtasks, c, threads=2)
+        scale = max(np.abs(fv).max(), 1e-300)
+        assert np.abs(s - fv).max() <= 1e-10 * scale, name
