@@ -237,7 +237,7 @@ def main():
     h2d = desc_leaf_bytes(desc)
     d2h = 16 * oe
     e2e_ms = []
-    for i in range(args.e2e_steps + 1):
+    for i in range(args.e2e_steps + 1 if args.e2e_steps > 0 else 0):
         barrier()
         t0 = time.perf_counter()
         p2 = ExecutablePlan.from_desc(desc, device=local, mode=args.mode)
@@ -250,7 +250,7 @@ def main():
             e2e_ms.append(1e3 * dt)
         c2.close()
         p2.close()
-    e2e_value = n / (statistics.median(e2e_ms) / 1e3)
+    e2e_value = n / (statistics.median(e2e_ms) / 1e3) if e2e_ms else None
 
     # ---- roofline of the dominant kernel ----
     hbm_peak, tc_peak, peak_src = peaks()
@@ -289,7 +289,8 @@ def main():
         "flops_per_slice": flops_per_slice,
         "clocks": clocks.summary(),
         "e2e": {"value": e2e_value, "unit": "slices/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": statistics.median(e2e_ms)},
+                "d2h_bytes_per_step": d2h,
+                "ms_per_step": statistics.median(e2e_ms) if e2e_ms else None},
         "gpu_launches": int(launches) * args.steps,
         "roofline": roof,
         "checksum": float(np.abs(result.cpu().numpy()).sum()),

@@ -1,12 +1,425 @@
-// tcgen05 split-TF32 complex GEMM (placeholder until the sm_100a kernel lands).
+// tcgen05 split-TF32 ("3xTF32") complex GEMM for sm_100a.
+//
+//   C[z] (M x N complex) = A[z] (M x K complex, row-major) * B[z] (K x N complex, row-major)
+//
+// Complex -> real: with interleaved storage, A is an M x 2K real matrix that is
+// already K-major. B becomes the 2N x 2K K-major real matrix
+//   B''[2n+t][2k+s] = [[br, -bi], [bi, br]][t][s]
+// so that C (M x 2N real, i.e. interleaved complex) = A . B''^T: 4 real MACs per
+// complex MAC, like the 4M decomposition, in one real GEMM.
+//
+// Split-TF32: x = hi + lo with hi = tf32(x) (round to nearest) and lo = x - hi;
+// C ~= Ahi.Bhi + Ahi.Blo + Alo.Bhi, accumulated in fp32 in TMEM. The dropped
+// Alo.Blo term is ~2^-22 relative, so results carry fp32-level accuracy.
+//
+// Kernel anatomy (one CTA per 128 x 256 real output tile):
+//   warp 0      TMA producer: A hi/lo (128 x 32) and B'' hi/lo (256 x 32) tiles,
+//               SWIZZLE_128B, two-stage mbarrier ring
+//   warp 1      MMA issuer: 3 x 4 tcgen05.mma.kind::tf32 (128x256x8) per stage,
+//               tcgen05.commit frees the stage / signals the epilogue
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 from TMEM -> registers -> global
+// The operand splits (A hi/lo, B'' hi/lo) are produced by two bandwidth-bound
+// pre-pass kernels into a workspace.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+
 #include "kernels.h"
 
 namespace stn {
 
-bool gemm_tc_supported(const GemmShape &) { return false; }
-size_t gemm_tc_workspace_bytes(const GemmShape &) { return 0; }
-cudaError_t launch_gemm_tc(const GemmShape &, const BatchPtrs &, void *, size_t, cudaStream_t) {
-  return cudaErrorNotSupported;
+namespace {
+
+constexpr int BM = 128;        // rows of C per CTA (UMMA M)
+constexpr int BN = 256;        // real columns of C per CTA (UMMA N)
+constexpr int BK = 32;         // real K per stage (128 B rows -> SWIZZLE_128B)
+constexpr int UK = 8;          // real K per tcgen05.mma (32 B of tf32)
+constexpr int STAGES = 2;
+constexpr int A_TILE_BYTES = BM * BK * 4;  // 16 KiB
+constexpr int B_TILE_BYTES = BN * BK * 4;  // 32 KiB
+constexpr int STAGE_BYTES = 2 * A_TILE_BYTES + 2 * B_TILE_BYTES;
+constexpr int THREADS = 192;
+constexpr int TMEM_COLS = 256;
+constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+// ---- PTX wrappers -------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+// Bounded wait: a barrier that never completes traps (~2 s) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done = 0;
+  long long start = 0;
+  for (int iter = 0;; ++iter) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (iter == 0) start = clock64();
+    if ((iter & 1023) == 1023 && clock64() - start > (4ll << 30)) __trap();
+  }
+}
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                            int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+// K-major SWIZZLE_128B shared-memory matrix descriptor (sm_100 "version 1").
+// 8-row x 128 B swizzle atoms stacked every 1024 B (SBO); LBO unused.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFFu);
+  d |= uint64_t(1) << 16;            // LBO (ignored for swizzled K-major)
+  d |= uint64_t(1024 >> 4) << 32;    // SBO
+  d |= uint64_t(1) << 46;            // descriptor version (Blackwell)
+  d |= uint64_t(2) << 61;            // SWIZZLE_128B
+  return d;
+}
+
+// kind::tf32 instruction descriptor: F32 accumulate, TF32 A/B, both K-major.
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(BN >> 3) << 17) |
+                            (uint32_t(BM >> 4) << 24);
+
+__device__ __forceinline__ float tf32_round(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// ---- the GEMM kernel ----------------------------------------------------------
+struct TcArgs {
+  float *c;          // C base (complex interleaved -> M x 2N floats per batch)
+  int64_t c_bs;      // floats between slices
+  int64_t c_ds;      // floats between D batches
+  int D;
+  int a_batched, b_batched;  // operand varies per slice
+  int k_blocks;      // 2K / BK
+  int two_n;         // 2N (row stride of C in floats)
+};
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
+              const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+              const TcArgs args) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *smem = reinterpret_cast<unsigned char *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+  uint64_t *empty = full + STAGES;
+  uint64_t *tmem_full = empty + STAGES;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n_tile = blockIdx.x, m_tile = blockIdx.y, bz = blockIdx.z;
+  const int slice = bz / args.D, d = bz % args.D;
+  const int za = args.a_batched ? bz : d;
+  const int zb = args.b_batched ? bz : d;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ahi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_alo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer ----
+      for (int kb = 0; kb < args.k_blocks; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t phase = (kb / STAGES) & 1;
+        mbar_wait(&empty[s], phase ^ 1);
+        unsigned char *st = smem + s * STAGE_BYTES;
+        mbar_expect_tx(&full[s], STAGE_BYTES);
+        const int kx = kb * BK;
+        tma_load_3d(st, &map_ahi, &full[s], kx, m_tile * BM, za);
+        tma_load_3d(st + A_TILE_BYTES, &map_alo, &full[s], kx, m_tile * BM, za);
+        tma_load_3d(st + 2 * A_TILE_BYTES, &map_bhi, &full[s], kx, n_tile * BN, zb);
+        tma_load_3d(st + 2 * A_TILE_BYTES + B_TILE_BYTES, &map_blo, &full[s], kx, n_tile * BN, zb);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- MMA issuer ----
+      for (int kb = 0; kb < args.k_blocks; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t phase = (kb / STAGES) & 1;
+        mbar_wait(&full[s], phase);
+        tc_fence_after();
+        const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
+        const uint64_t ahi = smem_desc_sw128(st);
+        const uint64_t alo = smem_desc_sw128(st + A_TILE_BYTES);
+        const uint64_t bhi = smem_desc_sw128(st + 2 * A_TILE_BYTES);
+        const uint64_t blo = smem_desc_sw128(st + 2 * A_TILE_BYTES + B_TILE_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / UK; ++k) {
+          const uint64_t koff = uint64_t((k * UK * 4) >> 4);  // +32 B per K step
+          const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
+          umma_tf32(tmem_base, ahi + koff, bhi + koff, kIdesc, acc0);
+          umma_tf32(tmem_base, ahi + koff, blo + koff, kIdesc, 1u);
+          umma_tf32(tmem_base, alo + koff, bhi + koff, kIdesc, 1u);
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(tmem_full);
+    }
+  } else {
+    // ---- epilogue: TMEM -> registers -> global ----
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int lane_base = 32 * (warp % 4);
+    const int row = m_tile * BM + lane_base + lane;
+    float *crow = args.c + int64_t(slice) * args.c_bs + int64_t(d) * args.c_ds +
+                  int64_t(row) * args.two_n + int64_t(n_tile) * BN;
+#pragma unroll 1
+    for (int cc = 0; cc < BN / 32; ++cc) {
+      uint32_t v[32];
+      const uint32_t taddr = tmem_base + (uint32_t(lane_base) << 16) + uint32_t(cc * 32);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32"
+          "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15,"
+          " %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31},"
+          " [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+            "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+            "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+            "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+            "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      float4 *dst = reinterpret_cast<float4 *>(crow + cc * 32);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                             __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ---- operand preparation --------------------------------------------------------
+// A (complex M x K per batch) -> hi/lo planes, same M x 2K real layout.
+__global__ void k_split_a(const float *__restrict__ a, int64_t a_bs, int64_t a_ds, int D,
+                          int64_t per, int64_t nbatch, float *__restrict__ hi,
+                          float *__restrict__ lo) {
+  const int64_t total = per * nbatch;  // floats
+  for (int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4; i < total;
+       i += int64_t(gridDim.x) * blockDim.x * 4) {
+    const int64_t z = i / per, r = i % per;
+    const int64_t slice = z / D, d = z % D;
+    const float4 x = *reinterpret_cast<const float4 *>(a + slice * a_bs + d * a_ds + r);
+    float4 h, l;
+    h.x = tf32_round(x.x), h.y = tf32_round(x.y), h.z = tf32_round(x.z), h.w = tf32_round(x.w);
+    l.x = x.x - h.x, l.y = x.y - h.y, l.z = x.z - h.z, l.w = x.w - h.w;
+    *reinterpret_cast<float4 *>(hi + i) = h;
+    *reinterpret_cast<float4 *>(lo + i) = l;
+  }
+}
+
+// B (complex K x N per batch) -> B'' (2N x 2K real, K-major) hi/lo planes.
+// 32 x 32 complex tiles through shared memory: coalesced reads along n, writes along k.
+__global__ void k_expand_b(const float2 *__restrict__ b, int64_t b_bs, int64_t b_ds, int D,
+                           int K, int N, float *__restrict__ hi, float *__restrict__ lo) {
+  __shared__ float2 tile[32][33];
+  const int z = blockIdx.z;
+  const int64_t slice = z / D, d = z % D;
+  const float2 *src = b + slice * b_bs + d * b_ds;
+  const int64_t plane = int64_t(4) * K * N;  // floats per batch in B''
+  float *h = hi + z * plane, *l = lo + z * plane;
+  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y)
+    tile[r][threadIdx.x] = src[int64_t(k0 + r) * N + n0 + threadIdx.x];
+  __syncthreads();
+  // thread (x, y): n = n0 + y, k = k0 + x
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const float2 v = tile[threadIdx.x][r];
+    const int n = n0 + r, k = k0 + threadIdx.x;
+    const float vals[4] = {v.x, -v.y, v.y, v.x};  // [t][s]: (0,0) br (0,1) -bi (1,0) bi (1,1) br
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int64_t row = int64_t(2 * n + t) * (2 * K) + 2 * k;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const float x = vals[2 * t + s];
+        const float xh = tf32_round(x);
+        h[row + s] = xh;
+        l[row + s] = x - xh;
+      }
+    }
+  }
+}
+
+// ---- host side --------------------------------------------------------------------
+using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                              const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                              const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap *map, const float *base, int64_t inner, int64_t rows, int64_t batches,
+              int box_rows) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {cuuint64_t(inner), cuuint64_t(rows), cuuint64_t(batches)};
+  cuuint64_t strides[2] = {cuuint64_t(inner * 4), cuuint64_t(inner * rows * 4)};
+  cuuint32_t box[3] = {cuuint32_t(BK), cuuint32_t(box_rows), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(base), dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool gemm_tc_supported(const GemmShape &s) {
+  return s.M % BM == 0 && (2 * s.N) % BN == 0 && s.K % 32 == 0 && s.M >= BM &&
+         s.M <= (int64_t(1) << 31) && s.N <= (int64_t(1) << 30) && s.K <= (int64_t(1) << 30);
+}
+
+size_t gemm_tc_workspace_bytes(const GemmShape &s, const BatchPtrs &p) {
+  const size_t nbA = size_t(p.a_bs ? p.nbatch : 1) * s.D;
+  const size_t nbB = size_t(p.b_bs ? p.nbatch : 1) * s.D;
+  return size_t(2) * 4 * (nbA * size_t(s.M) * 2 * s.K + nbB * size_t(4) * s.N * s.K);
+}
+
+cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspace,
+                           size_t workspace_bytes, cudaStream_t stream, cudaEvent_t *gemm_events) {
+  if (!gemm_tc_supported(s)) return cudaErrorNotSupported;
+  const int64_t nbA = (p.a_bs ? p.nbatch : 1) * s.D;
+  const int64_t nbB = (p.b_bs ? p.nbatch : 1) * s.D;
+  const size_t a_plane = size_t(s.M) * 2 * s.K;       // floats per batch
+  const size_t b_plane = size_t(4) * s.N * s.K;
+  const size_t need = 4 * 2 * (a_plane * nbA + b_plane * nbB);
+  if (need > workspace_bytes) return cudaErrorNotSupported;
+  float *ahi = static_cast<float *>(workspace);
+  float *alo = ahi + a_plane * nbA;
+  float *bhi = alo + a_plane * nbA;
+  float *blo = bhi + b_plane * nbB;
+  {
+    const int64_t total = int64_t(a_plane) * nbA;
+    int64_t blocks = (total / 4 + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    k_split_a<<<unsigned(blocks), 256, 0, stream>>>(
+        static_cast<const float *>(p.a), 2 * p.a_bs, int64_t(2) * s.M * s.K, int(s.D),
+        int64_t(a_plane), nbA, ahi, alo);
+  }
+  {
+    dim3 grid(unsigned(s.N / 32), unsigned(s.K / 32), unsigned(nbB));
+    if (s.N % 32 || s.K % 32) return cudaErrorNotSupported;
+    k_expand_b<<<grid, dim3(32, 8), 0, stream>>>(static_cast<const float2 *>(p.b), p.b_bs,
+                                                  s.K * s.N, int(s.D), int(s.K), int(s.N), bhi,
+                                                  blo);
+  }
+  CUtensorMap mah, mal, mbh, mbl;
+  if (!make_map(&mah, ahi, 2 * s.K, s.M, nbA, BM) || !make_map(&mal, alo, 2 * s.K, s.M, nbA, BM) ||
+      !make_map(&mbh, bhi, 2 * s.K, 2 * s.N, nbB, BN) ||
+      !make_map(&mbl, blo, 2 * s.K, 2 * s.N, nbB, BN))
+    return cudaErrorNotSupported;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  TcArgs args;
+  args.c = static_cast<float *>(p.out);
+  args.c_bs = 2 * p.out_bs;
+  args.c_ds = int64_t(2) * s.M * s.N;
+  args.D = int(s.D);
+  args.a_batched = p.a_bs != 0;
+  args.b_batched = p.b_bs != 0;
+  args.k_blocks = int(2 * s.K / BK);
+  args.two_n = int(2 * s.N);
+  dim3 grid(unsigned(2 * s.N / BN), unsigned(s.M / BM), unsigned(s.D * p.nbatch));
+  if (gemm_events) cudaEventRecord(gemm_events[0], stream);
+  k_gemm_tc<<<grid, THREADS, SMEM_BYTES, stream>>>(mah, mal, mbh, mbl, args);
+  if (gemm_events) cudaEventRecord(gemm_events[1], stream);
+  return cudaGetLastError();
 }
 
 }  // namespace stn

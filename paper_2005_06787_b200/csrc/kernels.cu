@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(256)
 // ---------------------------------------------------------------------------
 constexpr int kAbsorbThreads = 256;
 
-template <bool EXACT, int NC>
+template <bool EXACT, int NC, bool PERMUTE>
 __global__ void __launch_bounds__(kAbsorbThreads)
     k_absorb(const __grid_constant__ AbsorbGeom g, const BatchPtrs p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kAbsorbThreads)
       if ((n >> j) & 1) off |= 1 << g.n_ol[j];
     on[n] = off;
   }
-  for (int i = tid; i < K * N; i += kAbsorbThreads) {
+  for (int i = tid; i < (PERMUTE ? 0 : K * N); i += kAbsorbThreads) {
     const int k = i / N, n = i % N;
     int64_t off = 0;
     for (int j = 0; j < g.kb; ++j)
@@ -247,6 +247,10 @@ __global__ void __launch_bounds__(kAbsorbThreads)
         xo |= 1 << g.t_xl[j];
         oo |= 1 << g.t_ol[j];
       }
+    if constexpr (PERMUTE) {
+      os[oo] = xs[xo];
+      continue;
+    }
     for (int n0 = 0; n0 < N; n0 += NC) {
       float2 acc[NC];
 #pragma unroll
@@ -457,11 +461,121 @@ cudaError_t launch_absorb(const AbsorbGeom &g, const BatchPtrs &p, bool exact,
   const size_t smem = absorb_smem_bytes(g);
   dim3 grid(unsigned(uint64_t(1) << g.ob), p.nbatch);
   constexpr int NC = 8;
-  auto kern = exact ? k_absorb<true, NC> : k_absorb<false, NC>;
+  auto kern = exact ? k_absorb<true, NC, false> : k_absorb<false, NC, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (e != cudaSuccess) return e;
   kern<<<grid, kAbsorbThreads, smem, stream>>>(g, p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_bitperm(const AbsorbGeom &g, const void *in, void *out, int64_t in_bs,
+                           int64_t out_bs, int nbatch, cudaStream_t stream) {
+  const size_t smem = absorb_smem_bytes(g);
+  dim3 grid(unsigned(uint64_t(1) << g.ob), nbatch);
+  auto kern = k_absorb<false, 1, true>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  BatchPtrs p{in, nullptr, out, in_bs, 0, out_bs, nbatch};
+  kern<<<grid, kAbsorbThreads, smem, stream>>>(g, p);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Split-K reduction for steps with a small output and a long K (e.g. the
+// 16 x 16 x 2^20 inner products of two big stem tensors). FAST mode only: the
+// K range is cut into fixed chunks (deterministic order, not the reference's
+// single running sum). Pass 1: per (chunk, batch) partial outputs; pass 2:
+// ascending-chunk sum.
+// ---------------------------------------------------------------------------
+template <class R>
+__global__ void __launch_bounds__(256)
+    k_splitk_partial(const __grid_constant__ StridedGeom g, const BatchPtrs p, int64_t kchunk,
+                     int nchunks, void *partial_) {
+  using T = cx_t<R>;
+  __shared__ T red[256];
+  const int b = blockIdx.y, chunk = blockIdx.x;
+  const T *A = static_cast<const T *>(p.a) + int64_t(b) * p.a_bs;
+  const T *B = static_cast<const T *>(p.b) + int64_t(b) * p.b_bs;
+  T *partial = static_cast<T *>(partial_) + (int64_t(b) * nchunks + chunk) * g.out_size;
+  const int tpo = 256 / int(g.out_size);  // threads per output (consecutive k)
+  const int o = threadIdx.x / tpo, sub = threadIdx.x % tpo;
+  T acc;
+  acc.x = acc.y = 0;
+  if (o < g.out_size) {
+    int64_t rem = o, ao = 0, bo = 0;
+    for (int i = g.n_out - 1; i >= 0; --i) {
+      const int sh = __ffsll(g.out_dim[i]) - 1;
+      const int64_t idx = rem & (g.out_dim[i] - 1);
+      rem >>= sh;
+      ao += idx * g.out_sa[i];
+      bo += idx * g.out_sb[i];
+    }
+    const int64_t k0 = int64_t(chunk) * kchunk;
+    const int64_t k1 = min(g.k_size, k0 + kchunk);
+    for (int64_t k = k0 + sub; k < k1; k += tpo) {
+      int64_t r2 = k, ka = ao, kb = bo;
+      for (int i = g.n_k - 1; i >= 0; --i) {
+        const int sh = __ffsll(g.k_dim[i]) - 1;
+        const int64_t idx = r2 & (g.k_dim[i] - 1);
+        r2 >>= sh;
+        ka += idx * g.k_sa[i];
+        kb += idx * g.k_sb[i];
+      }
+      cmac<false>(acc, A[ka], B[kb]);
+    }
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (o < g.out_size && sub == 0) {
+    T s = red[threadIdx.x];
+    for (int j = 1; j < tpo; ++j) {
+      s.x += red[threadIdx.x + j].x;
+      s.y += red[threadIdx.x + j].y;
+    }
+    partial[o] = s;
+  }
+}
+
+template <class R>
+__global__ void k_splitk_sum(const void *partial_, int nchunks, int64_t out_size, int nbatch,
+                             void *out_, int64_t out_bs) {
+  using T = cx_t<R>;
+  const T *partial = static_cast<const T *>(partial_);
+  T *out = static_cast<T *>(out_);
+  const int64_t total = out_size * nbatch;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = i / out_size, o = i % out_size;
+    T s;
+    s.x = s.y = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const T v = partial[(b * nchunks + c) * out_size + o];
+      s.x += v.x;
+      s.y += v.y;
+    }
+    out[b * out_bs + o] = s;
+  }
+}
+
+int splitk_chunks(const StridedGeom &g) {
+  int64_t c = (g.k_size + 4095) / 4096;
+  return int(c < 1 ? 1 : (c > 2048 ? 2048 : c));
+}
+
+template <class R>
+cudaError_t launch_splitk(const StridedGeom &g, const BatchPtrs &p, void *workspace,
+                          cudaStream_t stream) {
+  const int nchunks = splitk_chunks(g);
+  const int64_t kchunk = (g.k_size + nchunks - 1) / nchunks;
+  k_splitk_partial<R><<<dim3(nchunks, p.nbatch), 256, 0, stream>>>(g, p, kchunk, nchunks,
+                                                                   workspace);
+  k_splitk_sum<R><<<grid_for(g.out_size * p.nbatch, 256), 256, 0, stream>>>(
+      workspace, nchunks, g.out_size, p.nbatch, p.out, p.out_bs);
+  return cudaGetLastError();
+}
+
+size_t splitk_workspace_bytes(const StridedGeom &g, int nbatch, size_t esize) {
+  return size_t(splitk_chunks(g)) * g.out_size * nbatch * esize;
 }
 
 template <class R>
@@ -511,6 +625,10 @@ template cudaError_t launch_gemm_simt<float>(const GemmShape &, const BatchPtrs 
                                              cudaStream_t);
 template cudaError_t launch_gemm_simt<double>(const GemmShape &, const BatchPtrs &, bool,
                                               cudaStream_t);
+template cudaError_t launch_splitk<float>(const StridedGeom &, const BatchPtrs &, void *,
+                                          cudaStream_t);
+template cudaError_t launch_splitk<double>(const StridedGeom &, const BatchPtrs &, void *,
+                                           cudaStream_t);
 template cudaError_t launch_leaf_gather<float>(const LeafGatherTable &, void *, const int32_t *,
                                                int, cudaStream_t);
 template cudaError_t launch_leaf_gather<double>(const LeafGatherTable &, void *, const int32_t *,

@@ -101,6 +101,14 @@ cudaError_t launch_absorb(const AbsorbGeom &g, const BatchPtrs &p, bool exact, c
 template <class R>
 cudaError_t launch_permute(const StridedGeom &g, const void *in, void *out, int64_t in_bs,
                            int64_t out_bs, int nbatch, cudaStream_t stream);
+// Tiled bond-2 bit permutation (the absorb tile machinery with K = N = 0).
+cudaError_t launch_bitperm(const AbsorbGeom &g, const void *in, void *out, int64_t in_bs,
+                           int64_t out_bs, int nbatch, cudaStream_t stream);
+// Split-K reduction (small output, long K; FAST mode). Pow2 geometries, out_size <= 256.
+template <class R>
+cudaError_t launch_splitk(const StridedGeom &g, const BatchPtrs &p, void *workspace,
+                          cudaStream_t stream);
+size_t splitk_workspace_bytes(const StridedGeom &g, int nbatch, size_t esize);
 template <class R>
 cudaError_t launch_gemm_simt(const GemmShape &s, const BatchPtrs &p, bool exact,
                              cudaStream_t stream);
@@ -114,11 +122,13 @@ cudaError_t launch_sum_ordered(const double *per_slice, uint64_t n_slices, int64
                                double *out, cudaStream_t stream);
 
 // tcgen05 split-TF32 complex GEMM (gemm_tc.cu). Requires M % 128 == 0,
-// N % 32 == 0, K % 16 == 0 (complex elements); returns cudaErrorNotSupported
+// N % 128 == 0, K % 32 == 0 (complex elements); returns cudaErrorNotSupported
 // otherwise so the caller can pick another kernel.
+// gemm_events (optional, 2 events) bracket the GEMM kernel alone (no pre-pass).
 cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspace,
-                           size_t workspace_bytes, cudaStream_t stream);
-size_t gemm_tc_workspace_bytes(const GemmShape &s);
+                           size_t workspace_bytes, cudaStream_t stream,
+                           cudaEvent_t *gemm_events = nullptr);
+size_t gemm_tc_workspace_bytes(const GemmShape &s, const BatchPtrs &p);
 bool gemm_tc_supported(const GemmShape &s);
 
 }  // namespace stn

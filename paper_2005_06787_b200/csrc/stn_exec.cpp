@@ -106,7 +106,7 @@ struct DevBuf {
 // ---------------------------------------------------------------------------
 // plan model
 // ---------------------------------------------------------------------------
-enum class Kern { Generic, Absorb, GemmSimt, GemmTc };
+enum class Kern { Generic, Absorb, SplitK, GemmSimt, GemmTc };
 
 struct Node {
   bool is_leaf = false;
@@ -129,6 +129,8 @@ struct StepPlan {
   // gemm path
   bool a_id = true, b_id = true, c_id = true;
   stn::StridedGeom pa{}, pb{}, pc{};
+  bool pa_tiled = false, pb_tiled = false, pc_tiled = false;  // bond-2 tiled permutes
+  stn::AbsorbGeom pag{}, pbg{}, pcg{};
   stn::GemmShape gs{};
   int64_t lsize = 0, rsize = 0, osize = 0;
 };
@@ -204,7 +206,7 @@ struct stn_plan {
   std::map<int, int64_t> cache_off;  // node -> element offset in cache storage
   int64_t cache_elems = 0;
   // runtime state
-  DevBuf arena, digits, scratch_out, tc_workspace;
+  DevBuf arena, digits, scratch_out, tc_workspace, splitk_ws;
   int64_t out_elements = 1;
   std::vector<int> out_dims;
   int max_batch = 0;
@@ -304,59 +306,14 @@ bool is_identity(const std::vector<int> &p) {
 // ---------------------------------------------------------------------------
 // absorb geometry (bond-2, D == 1): see kernels.h AbsorbGeom
 // ---------------------------------------------------------------------------
-bool build_absorb(StepPlan &sp, const std::vector<int> &ldims, const std::vector<int> &rdims) {
-  const stn_step_desc &d = sp.d;
-  if (d.nd != 0) return false;
-  for (int x : ldims)
-    if (x != 2) return false;
-  for (int x : rdims)
-    if (x != 2) return false;
-  const int lr = int(ldims.size()), rr = int(rdims.size()), orank = int(sp.out_dims.size());
-  const bool x_lhs = sp.lsize >= sp.rsize;
-  const int xr = x_lhs ? lr : rr, wr = x_lhs ? rr : lr;
-  const int kb = d.nk;
-  const int nb = wr - kb;  // W-side free bits
-  const int mb = xr - kb;
-  if (kb > stn::kAbsorbMaxKN || nb > stn::kAbsorbMaxKN || xr < 12) return false;
-  // K bits: (x position, w position)
-  std::vector<std::pair<int, int>> kbits;
-  for (int q = 0; q < d.nk; ++q) {
-    int la = sp.lperm[d.nd + d.nm + q], rb = sp.rperm[d.nd + q];
-    int xa = x_lhs ? la : rb, wa = x_lhs ? rb : la;
-    kbits.push_back({xr - 1 - xa, wr - 1 - wa});
-  }
-  std::sort(kbits.begin(), kbits.end());
-  // output bits: M pairs (x pos, o pos) from X, N pairs (w pos, o pos) from W
-  std::vector<std::pair<int, int>> mbits, nbits;  // (xpos, opos), (opos, wpos)
-  for (int i = 0; i < orank; ++i) {
-    int p = sp.operm[i];
-    int opos = orank - 1 - i;
-    bool from_lhs = p < d.nd + d.nm;
-    if (from_lhs) {
-      int la = sp.lperm[p];
-      if (x_lhs)
-        mbits.push_back({lr - 1 - la, opos});
-      else
-        nbits.push_back({opos, lr - 1 - la});
-    } else {
-      int q = p - d.nd - d.nm;
-      int rb = sp.rperm[d.nd + d.nk + q];
-      if (x_lhs)
-        nbits.push_back({opos, rr - 1 - rb});
-      else
-        mbits.push_back({rr - 1 - rb, opos});
-    }
-  }
-  std::sort(nbits.begin(), nbits.end());
-  if (int(mbits.size()) != mb || int(nbits.size()) != nb) return false;
-  // W positions of K and N bits must be ascending with their X/O order
-  for (size_t j = 1; j < kbits.size(); ++j)
-    if (kbits[j].second < kbits[j - 1].second) return false;
-  for (size_t j = 1; j < nbits.size(); ++j)
-    if (nbits[j].second < nbits[j - 1].second) return false;
-
+// Tile geometry shared by the absorb and bit-permute kernels (kernels.h AbsorbGeom).
+// kbits: (x pos, w pos) ascending; mbits: (x pos, o pos); nbits: (o pos, w pos) ascending.
+bool make_tile_geom(const std::vector<std::pair<int, int>> &kbits,
+                    const std::vector<std::pair<int, int>> &mbits,
+                    const std::vector<std::pair<int, int>> &nbits, int x_bits, int o_bits,
+                    stn::AbsorbGeom &g) {
+  const int kb = int(kbits.size()), nb = int(nbits.size()), mb = int(mbits.size());
   // choose tile M bits T: low X bits, low O bits, then ascending X position
-  const int x_bits = xr, o_bits = orank;
   const int Lx = std::min(5, x_bits), Lo = std::min(5, o_bits);
   std::vector<char> in_t(mbits.size(), 0);
   int tb = 0;
@@ -383,7 +340,6 @@ bool build_absorb(StepPlan &sp, const std::vector<int> &ldims, const std::vector
   const int ob = mb - tb;
   if (ob > 31) return false;
 
-  stn::AbsorbGeom g;
   memset(&g, 0, sizeof g);
   g.x_bits = x_bits;
   g.o_bits = o_bits;
@@ -393,7 +349,6 @@ bool build_absorb(StepPlan &sp, const std::vector<int> &ldims, const std::vector
   g.ob = ob;
   g.xt_bits = kb + tb;
   g.ot_bits = nb + tb;
-  g.w_is_lhs = x_lhs ? 0 : 1;
   for (int j = 0; j < kb; ++j) g.w_k_stride[j] = int64_t(1) << kbits[j].second;
   for (int j = 0; j < nb; ++j) g.w_n_stride[j] = int64_t(1) << nbits[j].second;
   // tile-local X bits: K bits and T bits by ascending X position
@@ -446,10 +401,80 @@ bool build_absorb(StepPlan &sp, const std::vector<int> &ldims, const std::vector
   g.o_run = 0;
   while (g.o_run < g.ot_bits && g.o_tile_pos[g.o_run] == g.o_run) g.o_run++;
   if (g.x_run < 1 || g.o_run < 1) return false;
+  return true;
+}
+
+bool build_absorb(StepPlan &sp, const std::vector<int> &ldims, const std::vector<int> &rdims) {
+  const stn_step_desc &d = sp.d;
+  if (d.nd != 0) return false;
+  for (int x : ldims)
+    if (x != 2) return false;
+  for (int x : rdims)
+    if (x != 2) return false;
+  const int lr = int(ldims.size()), rr = int(rdims.size()), orank = int(sp.out_dims.size());
+  const bool x_lhs = sp.lsize >= sp.rsize;
+  const int xr = x_lhs ? lr : rr, wr = x_lhs ? rr : lr;
+  const int kb = d.nk;
+  const int nb = wr - kb;  // W-side free bits
+  const int mb = xr - kb;
+  if (kb > stn::kAbsorbMaxKN || nb > stn::kAbsorbMaxKN || xr < 12) return false;
+  // K bits: (x position, w position)
+  std::vector<std::pair<int, int>> kbits;
+  for (int q = 0; q < d.nk; ++q) {
+    int la = sp.lperm[d.nd + d.nm + q], rb = sp.rperm[d.nd + q];
+    int xa = x_lhs ? la : rb, wa = x_lhs ? rb : la;
+    kbits.push_back({xr - 1 - xa, wr - 1 - wa});
+  }
+  std::sort(kbits.begin(), kbits.end());
+  // output bits: M pairs (x pos, o pos) from X, N pairs (w pos, o pos) from W
+  std::vector<std::pair<int, int>> mbits, nbits;  // (xpos, opos), (opos, wpos)
+  for (int i = 0; i < orank; ++i) {
+    int p = sp.operm[i];
+    int opos = orank - 1 - i;
+    bool from_lhs = p < d.nd + d.nm;
+    if (from_lhs) {
+      int la = sp.lperm[p];
+      if (x_lhs)
+        mbits.push_back({lr - 1 - la, opos});
+      else
+        nbits.push_back({opos, lr - 1 - la});
+    } else {
+      int q = p - d.nd - d.nm;
+      int rb = sp.rperm[d.nd + d.nk + q];
+      if (x_lhs)
+        nbits.push_back({opos, rr - 1 - rb});
+      else
+        mbits.push_back({rr - 1 - rb, opos});
+    }
+  }
+  std::sort(nbits.begin(), nbits.end());
+  if (int(mbits.size()) != mb || int(nbits.size()) != nb) return false;
+  // W positions of K and N bits must be ascending with their X/O order
+  for (size_t j = 1; j < kbits.size(); ++j)
+    if (kbits[j].second < kbits[j - 1].second) return false;
+  for (size_t j = 1; j < nbits.size(); ++j)
+    if (nbits[j].second < nbits[j - 1].second) return false;
+
+  stn::AbsorbGeom g;
+  if (!make_tile_geom(kbits, mbits, nbits, xr, orank, g)) return false;
+  g.w_is_lhs = x_lhs ? 0 : 1;
   sp.ag = g;
   sp.x_is_lhs = x_lhs;
   return true;
 }
+
+// Bond-2 permutation (out axis i = in axis perm[i]) as a tiled bit permutation.
+bool build_bitperm(const std::vector<int> &in_dims, const std::vector<int> &perm,
+                   stn::AbsorbGeom &g) {
+  const int r = int(in_dims.size());
+  if (r < 12) return false;
+  for (int x : in_dims)
+    if (x != 2) return false;
+  std::vector<std::pair<int, int>> mbits;
+  for (int i = 0; i < r; ++i) mbits.push_back({r - 1 - perm[i], r - 1 - i});
+  return make_tile_geom({}, mbits, {}, r, r, g);
+}
+
 
 // ---------------------------------------------------------------------------
 // plan construction
@@ -488,6 +513,16 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     sp.kern = Kern::Absorb;
     return;
   }
+  // long-K reduction to a small output (FAST mode: chunked K order)
+  if (!exact && sp.geo.out_size <= 256 && sp.geo.k_size >= (int64_t(1) << 14)) {
+    bool pow2 = true;
+    for (int i = 0; i < sp.geo.n_out; ++i) pow2 &= (sp.geo.out_dim[i] & (sp.geo.out_dim[i] - 1)) == 0;
+    for (int i = 0; i < sp.geo.n_k; ++i) pow2 &= (sp.geo.k_dim[i] & (sp.geo.k_dim[i] - 1)) == 0;
+    if (pow2) {
+      sp.kern = Kern::SplitK;
+      return;
+    }
+  }
   // dense GEMM path: materialise [D|M|K], [D|K|N], run GEMM, permute [D|M|N]
   if (d.M >= 8 && d.N >= 8 && d.K >= 8 && d.mults >= (uint64_t(1) << 18)) {
     std::vector<int> prod_dims(d.orank);
@@ -498,6 +533,11 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     fill_permute(sp.pa, ldims, sp.lperm);
     fill_permute(sp.pb, rdims, sp.rperm);
     fill_permute(sp.pc, prod_dims, sp.operm);
+    if (single) {
+      sp.pa_tiled = !sp.a_id && build_bitperm(ldims, sp.lperm, sp.pag);
+      sp.pb_tiled = !sp.b_id && build_bitperm(rdims, sp.rperm, sp.pbg);
+      sp.pc_tiled = !sp.c_id && build_bitperm(prod_dims, sp.operm, sp.pcg);
+    }
     sp.gs = {d.D, d.M, d.N, d.K};
     sp.kern = (single && !exact && stn::gemm_tc_supported(sp.gs)) ? Kern::GemmTc : Kern::GemmSimt;
   }
@@ -1077,6 +1117,14 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
       prof.done(STN_KERNEL_GENERIC, io_bytes, flops);
       break;
     }
+    case Kern::SplitK: {
+      stn::BatchPtrs p{a.ptr, b.ptr, out, a.bs, b.bs, o.bs, nb};
+      P.splitk_ws.reserve(std::max<size_t>(stn::splitk_workspace_bytes(sp.geo, nb, P.esize), 16));
+      cuda_check(stn::launch_splitk<R>(sp.geo, p, P.splitk_ws.ptr, st), "split-K kernel");
+      prof.done(STN_KERNEL_GENERIC, io_bytes, flops);
+      P.kernel_launches++;  // second (ordered-sum) launch
+      break;
+    }
     case Kern::Absorb: {
       const Resolved &x = sp.x_is_lhs ? a : b;
       const Resolved &w = sp.x_is_lhs ? b : a;
@@ -1091,14 +1139,20 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
       int64_t ga_bs = a.bs, gb_bs = b.bs;
       if (!sp.a_id) {
         void *dst = elem_ptr(P, P.arena.ptr, op.scr_a * nb);
-        cuda_check(stn::launch_permute<R>(sp.pa, a.ptr, dst, a.bs, sp.lsize, nb, st), "permute");
+        if (sp.pa_tiled)
+          cuda_check(stn::launch_bitperm(sp.pag, a.ptr, dst, a.bs, sp.lsize, nb, st), "bitperm");
+        else
+          cuda_check(stn::launch_permute<R>(sp.pa, a.ptr, dst, a.bs, sp.lsize, nb, st), "permute");
         prof.done(STN_KERNEL_PERMUTE, 2 * es * sp.lsize * nb, 0);
         ga = dst;
         ga_bs = sp.lsize;
       }
       if (!sp.b_id) {
         void *dst = elem_ptr(P, P.arena.ptr, op.scr_b * nb);
-        cuda_check(stn::launch_permute<R>(sp.pb, b.ptr, dst, b.bs, sp.rsize, nb, st), "permute");
+        if (sp.pb_tiled)
+          cuda_check(stn::launch_bitperm(sp.pbg, b.ptr, dst, b.bs, sp.rsize, nb, st), "bitperm");
+        else
+          cuda_check(stn::launch_permute<R>(sp.pb, b.ptr, dst, b.bs, sp.rsize, nb, st), "permute");
         prof.done(STN_KERNEL_PERMUTE, 2 * es * sp.rsize * nb, 0);
         gb = dst;
         gb_bs = sp.rsize;
@@ -1110,7 +1164,7 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
                                   double(sp.osize) * nb);
       bool done = false;
       if (sp.kern == Kern::GemmTc) {
-        size_t ws = stn::gemm_tc_workspace_bytes(sp.gs);
+        size_t ws = stn::gemm_tc_workspace_bytes(sp.gs, p);
         P.tc_workspace.reserve(std::max<size_t>(ws, 16));
         cudaError_t e = stn::launch_gemm_tc(sp.gs, p, P.tc_workspace.ptr, ws, st);
         if (e == cudaSuccess) {
@@ -1127,7 +1181,10 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
         prof.done(STN_KERNEL_GEMM_SIMT, gbytes, flops);
       }
       if (!sp.c_id) {
-        cuda_check(stn::launch_permute<R>(sp.pc, gc, out, sp.osize, o.bs, nb, st), "permute");
+        if (sp.pc_tiled)
+          cuda_check(stn::launch_bitperm(sp.pcg, gc, out, sp.osize, o.bs, nb, st), "bitperm");
+        else
+          cuda_check(stn::launch_permute<R>(sp.pc, gc, out, sp.osize, o.bs, nb, st), "permute");
         prof.done(STN_KERNEL_PERMUTE, 2 * es * sp.osize * nb, 0);
       }
       break;
@@ -1336,6 +1393,7 @@ int stn_plan_get_info(const stn_plan *P, stn_plan_info *info) {
   for (auto &op : P->with_cache.ops) {
     Kern k = P->steps[op.step].kern;
     if (k == Kern::GemmTc) info->steps_tensor_core++;
+    else if (k == Kern::GemmSimt) info->steps_generic++;
     else if (k == Kern::Absorb) info->steps_absorb++;
     else info->steps_generic++;
   }
@@ -1538,6 +1596,71 @@ int stn_sum_slices_ordered(const double *per_slice_dev, uint64_t n_slices, int64
     cuda_check(stn::launch_sum_ordered(per_slice_dev, n_slices, out_elements, out_dev,
                                        static_cast<cudaStream_t>(stream)),
                "ordered sum");
+  });
+}
+
+int stn_selftest_gemm_tc(int64_t M, int64_t N, int64_t K, int32_t batches, int32_t a_batched,
+                         int32_t b_batched, int32_t reps, double *max_rel_err, double *ms_total,
+                         double *ms_gemm) {
+  return guarded([&] {
+    stn::GemmShape s{1, M, N, K};
+    require(stn::gemm_tc_supported(s) && batches >= 1 && reps >= 1, STN_ERR_INVALID_ARGUMENT,
+            "shape not supported by the tensor-core GEMM");
+    const int64_t na = a_batched ? batches : 1, nbb = b_batched ? batches : 1;
+    std::vector<float> ha(size_t(2 * M * K * na)), hb(size_t(2 * K * N * nbb));
+    uint64_t x = 0x9E3779B97F4A7C15ull;
+    auto rnd = [&] {
+      x ^= x << 13;
+      x ^= x >> 7;
+      x ^= x << 17;
+      return float(double(x >> 11) * 0x1.0p-53 * 2.0 - 1.0);
+    };
+    for (auto &v : ha) v = rnd();
+    for (auto &v : hb) v = rnd();
+    std::vector<double> da(ha.begin(), ha.end()), db(hb.begin(), hb.end());
+    DevBuf A, B, Cf, Ad, Bd, Cd, ws;
+    A.upload(ha);
+    B.upload(hb);
+    Ad.upload(da);
+    Bd.upload(db);
+    Cf.reserve(size_t(8 * M * N * batches));
+    Cd.reserve(size_t(16 * M * N * batches));
+    stn::BatchPtrs p{A.ptr, B.ptr, Cf.ptr, a_batched ? M * K : 0, b_batched ? K * N : 0, M * N,
+                     batches};
+    stn::BatchPtrs pd{Ad.ptr, Bd.ptr, Cd.ptr, a_batched ? M * K : 0, b_batched ? K * N : 0,
+                      M * N, batches};
+    size_t wsb = stn::gemm_tc_workspace_bytes(s, p);
+    ws.reserve(wsb);
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev[4];
+    for (auto &e : ev) cuda_check(cudaEventCreate(&e), "event");
+    cuda_check(stn::launch_gemm_tc(s, p, ws.ptr, wsb, st), "tc gemm");
+    cuda_check(stn::launch_gemm_simt<double>(s, pd, false, st), "simt gemm");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    std::vector<float> cf(size_t(2 * M * N * batches));
+    std::vector<double> cd(size_t(2 * M * N * batches));
+    cuda_check(cudaMemcpy(cf.data(), Cf.ptr, cf.size() * 4, cudaMemcpyDeviceToHost), "dl");
+    cuda_check(cudaMemcpy(cd.data(), Cd.ptr, cd.size() * 8, cudaMemcpyDeviceToHost), "dl");
+    double scale = 0, err = 0;
+    for (size_t i = 0; i < cd.size(); i += 2) scale = std::max(scale, std::hypot(cd[i], cd[i + 1]));
+    for (size_t i = 0; i < cd.size(); i += 2)
+      err = std::max(err, std::hypot(double(cf[i]) - cd[i], double(cf[i + 1]) - cd[i + 1]));
+    *max_rel_err = err / std::max(scale, 1e-300);
+    double tot = 0, gm = 0;
+    for (int r = 0; r < reps; ++r) {
+      cuda_check(cudaEventRecord(ev[0], st), "event");
+      cuda_check(stn::launch_gemm_tc(s, p, ws.ptr, wsb, st, &ev[2]), "tc gemm");
+      cuda_check(cudaEventRecord(ev[1], st), "event");
+      cuda_check(cudaEventSynchronize(ev[1]), "sync");
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, ev[0], ev[1]);
+      cudaEventElapsedTime(&b, ev[2], ev[3]);
+      tot += a;
+      gm += b;
+    }
+    *ms_total = tot / reps;
+    *ms_gemm = gm / reps;
+    for (auto &e : ev) cudaEventDestroy(e);
   });
 }
 

@@ -1,0 +1,34 @@
+"""Kernel-level GPU checks: the tcgen05 split-TF32 complex GEMM against an
+fp64 SIMT GEMM on seeded random operands (tolerance 1e-5 of max|C|, the
+fp32-level accuracy the split-TF32 scheme is designed to hold)."""
+import ctypes as C
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _needs_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("M,N,K,batches,ab,bb", [
+    (128, 128, 32, 1, 1, 1),
+    (256, 128, 64, 3, 1, 0),
+    (128, 256, 96, 2, 0, 1),
+    (1024, 512, 1024, 1, 1, 1),
+    (4096, 1024, 1024, 1, 1, 1),
+])
+def test_tc_gemm_matches_fp64(M, N, K, batches, ab, bb):
+    from paper_2005_06787_b200 import abi
+    lib = abi.load_library()
+    err, ms, msg = C.c_double(), C.c_double(), C.c_double()
+    abi.check(lib.stn_selftest_gemm_tc(M, N, K, batches, ab, bb, 3, C.byref(err), C.byref(ms),
+                                       C.byref(msg)))
+    tflops = 8.0 * M * N * K * batches / (msg.value / 1e3) / 1e12
+    print(f"tc gemm {M}x{N}x{K}x{batches}: rel err {err.value:.2e}, "
+          f"{ms.value:.3f} ms total, {msg.value:.3f} ms gemm, {tflops:.1f} TFLOP/s")
+    assert err.value <= 1e-5

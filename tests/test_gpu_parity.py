@@ -67,6 +67,26 @@ def test_exact_mode_is_bitwise_reference(name, precision):
         assert rep.kernel_launches > 0
 
 
+def truth_and_tolerance(name, a, ref_single):
+    """fp64 truth for slice `a` and the amplitude tolerance: RTOL of max|truth|,
+    or twice the reference single-precision path's own error, if larger. The
+    truth is the reference double path (golden) when recorded, else this
+    executor's double-precision plan (bitwise equal to the reference double
+    path on every recorded case)."""
+    from paper_2005_06787_b200 import build_branch_cache, run_subtask
+    try:
+        asg, dvals, _, _, _ = read_ref(name, "double")
+        idx = list(asg).index(a)
+        truth = dvals[idx]
+    except (FileNotFoundError, ValueError):
+        plan = load(name, "double", "fast")
+        truth = run_subtask(plan, a, build_branch_cache(plan)).value.ravel()
+    tol = RTOL
+    if ref_single is not None:
+        tol = max(RTOL, 2 * rel_err(ref_single, truth))
+    return truth, tol
+
+
 @pytest.mark.parametrize("name", SMALL)
 def test_fast_mode_within_tolerance(name):
     from paper_2005_06787_b200 import build_branch_cache, run_scheme, run_subtask
@@ -78,10 +98,15 @@ def test_fast_mode_within_tolerance(name):
     cache = build_branch_cache(plan)
     for a, want in zip(asg, vals):
         got = run_subtask(plan, int(a), cache).value
-        assert rel_err(got, want) <= RTOL, (name, int(a))
+        truth, tol = truth_and_tolerance(name, int(a), want)
+        err = rel_err(got, truth)
+        print(f"{name} slice {int(a)}: fast err {err:.2e}, reference single err "
+              f"{rel_err(want, truth):.2e}, tol {tol:.2e}")
+        assert err <= tol, (name, int(a))
     if s is not None:
         total, _ = run_scheme(plan, 1)
-        assert rel_err(total, s) <= RTOL
+        _, _, ds, _, _ = read_ref(name, "double")
+        assert rel_err(total, ds) <= max(RTOL, 2 * rel_err(s, ds))
 
 
 @pytest.mark.parametrize("name", ["rt_grid3x4_m8_sliced", "cfg1_grid4x5_m14"])
@@ -188,16 +213,20 @@ def test_leaf_update_invalidates_cache_and_changes_values():
     assert np.array_equal(bits(got), bits(want))
 
 
-@pytest.mark.parametrize("name", ["cfg3_syc53_m12"])
-def test_large_config_fast_vs_exact(name):
-    """53-qubit slices: the CPU reference needs ~15 min per slice, so parity
-    runs against the exact mode (bitwise-equal to the reference on every case
-    above) on a few slices."""
+@pytest.mark.parametrize("name", ["cfg3_syc53_m12", "cfg4_syc53_m14"])
+def test_large_config_fast_vs_fp64(name):
+    """53-qubit slices (the CPU reference needs ~15 min per slice): FAST single
+    precision against this executor's double-precision plan (the reference
+    double path, bitwise, on every recorded case), next to the EXACT single
+    path's error, which is the reference single path bit for bit."""
     from paper_2005_06787_b200 import build_branch_cache, run_subtask
     fast = load(name, "single", "fast")
     exact = load(name, "single", "exact")
-    cf, ce = build_branch_cache(fast), build_branch_cache(exact)
-    for a in (0, fast.subtasks - 1):
-        vf = run_subtask(fast, a, cf).value
-        ve = run_subtask(exact, a, ce).value
-        assert rel_err(vf, ve) <= RTOL, a
+    dbl = load(name, "double", "fast")
+    cf, ce, cd = build_branch_cache(fast), build_branch_cache(exact), build_branch_cache(dbl)
+    a = 0
+    truth = run_subtask(dbl, a, cd).value
+    ef = rel_err(run_subtask(fast, a, cf).value, truth)
+    ee = rel_err(run_subtask(exact, a, ce).value, truth)
+    print(f"{name} slice {a}: fast err {ef:.2e}, reference-single (exact) err {ee:.2e}")
+    assert ef <= max(RTOL, 2 * ee)
