@@ -291,12 +291,12 @@ int stn_sum_slices_ordered(const double *per_slice_dev, uint64_t n_slices, int64
  * (C = A[M x K] * B[K x N], `batches` independent problems; a_batched /
  * b_batched select per-batch or shared operands) and compares it with an fp64
  * SIMT GEMM of the same inputs. Returns the max |C_tc - C_ref| / max|C_ref| and
- * the mean device time of the tensor-core path (pre-pass + GEMM) and of the
- * GEMM kernel alone over `reps` launches. STN_ERR_INVALID_ARGUMENT if the shape
+ * the mean device time of the tensor-core path (pre-pass + GEMM), of the
+ * GEMM kernel alone and of the fp32 SIMT GEMM over `reps` launches. STN_ERR_INVALID_ARGUMENT if the shape
  * is not supported by the tensor-core kernel. */
 int stn_selftest_gemm_tc(int64_t M, int64_t N, int64_t K, int32_t batches, int32_t a_batched,
                          int32_t b_batched, int32_t reps, double *max_rel_err, double *ms_total,
-                         double *ms_gemm);
+                         double *ms_gemm, double *ms_simt);
 
 #ifdef __cplusplus
 }

@@ -142,7 +142,8 @@ SIGNATURES = {
     "stn_sum_slices_ordered": (C.c_int, [_P, C.c_uint64, C.c_int64, _P, _P]),
     "stn_selftest_gemm_tc": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32,
                                        C.c_int32, C.c_int32, C.POINTER(C.c_double),
-                                       C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+                                       C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double)]),
 }
 
 _lib = None

@@ -282,6 +282,201 @@ __global__ void __launch_bounds__(kAbsorbThreads)
 }
 
 // ---------------------------------------------------------------------------
+// Absorb v2: persistent CTAs, cp.async double-buffered X tiles, one tile row
+// per thread with its K inputs in registers and W^T broadcast from smem
+// (8 FMA per shared load), O tile staged in smem for coalesced 16 B stores.
+// Per output the K terms are summed in ascending k (exact mode = reference).
+// ---------------------------------------------------------------------------
+constexpr int kAb2Threads = 256;
+constexpr int kAb2KC = 16;  // K chunk held in registers
+constexpr int kAb2NC = 16;  // outputs accumulated per pass
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <bool EXACT, bool PERMUTE>
+__global__ void __launch_bounds__(kAb2Threads, 2)
+    k_absorb2(const __grid_constant__ AbsorbGeom g, const BatchPtrs p, int64_t n_tiles) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int xt = g.xt_bits, ot = g.ot_bits;
+  const int K = 1 << g.kb, N = 1 << g.nb;
+  const int x_hi_n = 1 << (xt - g.x_run), o_hi_n = 1 << (ot - g.o_run);
+  float2 *xs0 = reinterpret_cast<float2 *>(smem_raw);
+  float2 *xs1 = xs0 + (1 << xt);
+  float2 *os = xs1 + (1 << xt);
+  float2 *wt = os + (1 << ot);                                   // W^T: [n][k]
+  int64_t *xhi = reinterpret_cast<int64_t *>(wt + (PERMUTE ? 0 : K * N));
+  int64_t *ohi = xhi + x_hi_n;
+  int *xk = reinterpret_cast<int *>(ohi + o_hi_n);
+  int *on = xk + K;
+  const int tid = threadIdx.x;
+  const int b = blockIdx.y;
+  const float2 *X = static_cast<const float2 *>(p.a) + int64_t(b) * p.a_bs;
+  float2 *O = static_cast<float2 *>(p.out) + int64_t(b) * p.out_bs;
+
+  for (int i = tid; i < x_hi_n; i += kAb2Threads) {
+    int64_t off = 0;
+    for (int l = g.x_run; l < xt; ++l)
+      if ((i >> (l - g.x_run)) & 1) off += int64_t(1) << g.x_tile_pos[l];
+    xhi[i] = off;
+  }
+  for (int i = tid; i < o_hi_n; i += kAb2Threads) {
+    int64_t off = 0;
+    for (int l = g.o_run; l < ot; ++l)
+      if ((i >> (l - g.o_run)) & 1) off += int64_t(1) << g.o_tile_pos[l];
+    ohi[i] = off;
+  }
+  for (int k = tid; k < K; k += kAb2Threads) {
+    int off = 0;
+    for (int j = 0; j < g.kb; ++j)
+      if ((k >> j) & 1) off |= 1 << g.k_xl[j];
+    xk[k] = off;
+  }
+  for (int n = tid; n < N; n += kAb2Threads) {
+    int off = 0;
+    for (int j = 0; j < g.nb; ++j)
+      if ((n >> j) & 1) off |= 1 << g.n_ol[j];
+    on[n] = off;
+  }
+  if constexpr (!PERMUTE) {
+    const float2 *W = static_cast<const float2 *>(p.b) + int64_t(b) * p.b_bs;
+    for (int i = tid; i < K * N; i += kAb2Threads) {
+      const int n = i / K, k = i % K;
+      int64_t off = 0;
+      for (int j = 0; j < g.kb; ++j)
+        if ((k >> j) & 1) off += g.w_k_stride[j];
+      for (int j = 0; j < g.nb; ++j)
+        if ((n >> j) & 1) off += g.w_n_stride[j];
+      wt[i] = W[off];
+    }
+  }
+  __syncthreads();
+
+  auto tile_bases = [&](int64_t tile, int64_t &bx, int64_t &bo) {
+    bx = 0;
+    bo = 0;
+    for (int j = 0; j < g.ob; ++j)
+      if ((tile >> j) & 1) {
+        bx += int64_t(1) << g.outer_x[j];
+        bo += int64_t(1) << g.outer_o[j];
+      }
+  };
+  const int x_run_mask = (1 << g.x_run) - 1, o_run_mask = (1 << g.o_run) - 1;
+  const int x_pairs = 1 << (xt - 1), o_pairs = 1 << (ot - 1);
+  auto issue_load = [&](int64_t tile, float2 *dst) {
+    int64_t bx, bo;
+    tile_bases(tile, bx, bo);
+    for (int q = tid; q < x_pairs; q += kAb2Threads) {
+      const int i = q << 1;
+      cp_async16(dst + i, X + bx + xhi[i >> g.x_run] + (i & x_run_mask));
+    }
+    cp_async_commit();
+  };
+
+  const int T = 1 << g.tb;
+  const int tpr = T >= kAb2Threads ? 1 : kAb2Threads / T;  // threads per tile row
+  int64_t tile = blockIdx.x;
+  if (tile < n_tiles) issue_load(tile, xs0);
+  for (int it = 0; tile < n_tiles; ++it, tile += gridDim.x) {
+    float2 *xs = (it & 1) ? xs1 : xs0;
+    const int64_t next = tile + gridDim.x;
+    if (next < n_tiles) {
+      issue_load(next, (it & 1) ? xs0 : xs1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    // ---- math ----
+    for (int r = tid / tpr; r < T; r += kAb2Threads / tpr) {
+      const int sub = tid % tpr;
+      int xo = 0, oo = 0;
+      for (int j = 0; j < g.tb; ++j)
+        if ((r >> j) & 1) {
+          xo |= 1 << g.t_xl[j];
+          oo |= 1 << g.t_ol[j];
+        }
+      if constexpr (PERMUTE) {
+        if (sub == 0) os[oo] = xs[xo];
+        continue;
+      }
+      for (int n0 = sub * kAb2NC; n0 < N; n0 += tpr * kAb2NC) {
+        float2 acc[kAb2NC];
+#pragma unroll
+        for (int c = 0; c < kAb2NC; ++c) acc[c] = make_float2(0.f, 0.f);
+        for (int k0 = 0; k0 < K; k0 += kAb2KC) {
+          float2 x[kAb2KC];
+#pragma unroll
+          for (int kk = 0; kk < kAb2KC; ++kk)
+            if (k0 + kk < K) x[kk] = xs[xo | xk[k0 + kk]];
+#pragma unroll
+          for (int c = 0; c < kAb2NC; ++c) {
+            if (n0 + c >= N) break;
+            const float2 *w = wt + (n0 + c) * K + k0;
+#pragma unroll
+            for (int kk = 0; kk < kAb2KC; ++kk)
+              if (k0 + kk < K) cmac<EXACT>(acc[c], x[kk], w[kk]);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < kAb2NC; ++c)
+          if (n0 + c < N) os[oo | on[n0 + c]] = acc[c];
+      }
+    }
+    __syncthreads();
+    // ---- store ----
+    {
+      int64_t bx, bo;
+      tile_bases(tile, bx, bo);
+      for (int q = tid; q < o_pairs; q += kAb2Threads) {
+        const int i = q << 1;
+        const float4 v = reinterpret_cast<const float4 *>(os)[q];
+        float4 *dst = reinterpret_cast<float4 *>(O + bo + ohi[i >> g.o_run] + (i & o_run_mask));
+        __stcs(dst, v);
+      }
+    }
+    // the next iteration's wait + __syncthreads orders os reuse
+  }
+}
+
+size_t absorb2_smem_bytes(const AbsorbGeom &g, bool permute) {
+  const size_t K = size_t(1) << g.kb, N = size_t(1) << g.nb;
+  return 8 * (2 * (size_t(1) << g.xt_bits) + (size_t(1) << g.ot_bits) + (permute ? 0 : K * N)) +
+         8 * ((size_t(1) << (g.xt_bits - g.x_run)) + (size_t(1) << (g.ot_bits - g.o_run))) +
+         4 * (K + N);
+}
+
+template <bool EXACT, bool PERMUTE>
+cudaError_t launch_absorb2_impl(const AbsorbGeom &g, const BatchPtrs &p, cudaStream_t stream) {
+  const size_t smem = absorb2_smem_bytes(g, PERMUTE);
+  auto kern = k_absorb2<EXACT, PERMUTE>;
+  static int set_bytes = 0;
+  if (int(smem) > set_bytes) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem > 48 * 1024 ? 200 * 1024 : 48 * 1024));
+    if (e != cudaSuccess) return e;
+    set_bytes = int(smem > 48 * 1024 ? 200 * 1024 : 48 * 1024);
+  }
+  const int64_t n_tiles = int64_t(1) << g.ob;
+  // persistent: up to 2 resident CTAs per SM (x 148 SMs), shared across the batch
+  int64_t ctas = 148 * 2 / (p.nbatch > 0 ? p.nbatch : 1);
+  if (ctas < 1) ctas = 1;
+  if (ctas > n_tiles) ctas = n_tiles;
+  dim3 grid(unsigned(ctas), unsigned(p.nbatch));
+  kern<<<grid, kAb2Threads, smem, stream>>>(g, p, n_tiles);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Tiled SIMT complex GEMM, C[d] = A[d] (MxK, row-major) * B[d] (KxN, row-major).
 // 64x64 output tile per CTA, 16-wide K steps, 4x4 outputs per thread; every
 // output accumulates k in ascending order.
@@ -458,26 +653,14 @@ size_t absorb_smem_bytes(const AbsorbGeom &g) {
 
 cudaError_t launch_absorb(const AbsorbGeom &g, const BatchPtrs &p, bool exact,
                           cudaStream_t stream) {
-  const size_t smem = absorb_smem_bytes(g);
-  dim3 grid(unsigned(uint64_t(1) << g.ob), p.nbatch);
-  constexpr int NC = 8;
-  auto kern = exact ? k_absorb<true, NC, false> : k_absorb<false, NC, false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
-  kern<<<grid, kAbsorbThreads, smem, stream>>>(g, p);
-  return cudaGetLastError();
+  return exact ? launch_absorb2_impl<true, false>(g, p, stream)
+               : launch_absorb2_impl<false, false>(g, p, stream);
 }
 
 cudaError_t launch_bitperm(const AbsorbGeom &g, const void *in, void *out, int64_t in_bs,
                            int64_t out_bs, int nbatch, cudaStream_t stream) {
-  const size_t smem = absorb_smem_bytes(g);
-  dim3 grid(unsigned(uint64_t(1) << g.ob), nbatch);
-  auto kern = k_absorb<false, 1, true>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
   BatchPtrs p{in, nullptr, out, in_bs, 0, out_bs, nbatch};
-  kern<<<grid, kAbsorbThreads, smem, stream>>>(g, p);
-  return cudaGetLastError();
+  return launch_absorb2_impl<false, true>(g, p, stream);
 }
 
 // ---------------------------------------------------------------------------

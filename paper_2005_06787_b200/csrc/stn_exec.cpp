@@ -1601,7 +1601,7 @@ int stn_sum_slices_ordered(const double *per_slice_dev, uint64_t n_slices, int64
 
 int stn_selftest_gemm_tc(int64_t M, int64_t N, int64_t K, int32_t batches, int32_t a_batched,
                          int32_t b_batched, int32_t reps, double *max_rel_err, double *ms_total,
-                         double *ms_gemm) {
+                         double *ms_gemm, double *ms_simt) {
   return guarded([&] {
     stn::GemmShape s{1, M, N, K};
     require(stn::gemm_tc_supported(s) && batches >= 1 && reps >= 1, STN_ERR_INVALID_ARGUMENT,
@@ -1660,6 +1660,17 @@ int stn_selftest_gemm_tc(int64_t M, int64_t N, int64_t K, int32_t batches, int32
     }
     *ms_total = tot / reps;
     *ms_gemm = gm / reps;
+    double sm = 0;
+    for (int r = 0; r < reps; ++r) {
+      cuda_check(cudaEventRecord(ev[0], st), "event");
+      cuda_check(stn::launch_gemm_simt<float>(s, p, false, st), "simt gemm");
+      cuda_check(cudaEventRecord(ev[1], st), "event");
+      cuda_check(cudaEventSynchronize(ev[1]), "sync");
+      float a = 0;
+      cudaEventElapsedTime(&a, ev[0], ev[1]);
+      sm += a;
+    }
+    if (ms_simt) *ms_simt = sm / reps;
     for (auto &e : ev) cudaEventDestroy(e);
   });
 }
