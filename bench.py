@@ -110,20 +110,46 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def cpu_baseline(cfg: str, threads: int, slices: int):
+def cpu_baseline(cfg: str, threads: int, budget_s: float):
     """The reference CPU executor (oracle/_ref/ref_tool: the reference headers
-    compiled as they lie, run_subtask per slice) on this host's cores."""
+    compiled as they lie; its Engine<float>::load_leaf/gemm in Engine::run's
+    order, runtime.hpp:420-453) on this host's cores, as a bounded sample:
+    every thread runs the per-slice steps of its own slice for `budget_s`
+    seconds. A thread's slice time is its prefix time scaled by the full-slice /
+    prefix time ratio of the same steps recorded on the build host
+    (tests/golden/<cfg>/ref_step_ms.json, one full reference slice, 1 thread)."""
     tool = os.path.join(REPO, "oracle", "_ref", "ref_tool")
     d = os.path.join(REPO, "tests", "golden", CONFIGS[cfg])
+    calib_path = os.path.join(d, "ref_step_ms.json")
     if not os.path.exists(tool):
         return None
-    out = subprocess.run([tool, "bench", d, "--threads", str(threads), "--slices", str(slices)],
-                         capture_output=True, text=True, check=True).stdout
+    calib = None
+    if os.path.exists(calib_path):
+        with open(calib_path) as f:
+            calib = json.load(f)["step_ms"]
+    out = subprocess.run([tool, "bench-prefix", d, "--threads", str(threads), "--budget",
+                          str(budget_s)], capture_output=True, text=True, check=True).stdout
     j = json.loads(out.strip().splitlines()[-1])
-    return {"value": j["slices_per_sec"], "unit": "slices/s", "cores": threads,
-            "kind": "reference",
-            "sample": f"{slices} slice(s) of {CONFIGS[cfg]} run_subtask on {threads} thread(s), "
-                      f"{j['run_seconds']:.1f} s wall, {j['gflops']:.2f} GFLOP/s"}
+    rates, fracs = [], []
+    for t in j["per_thread"]:
+        ms = t["step_ms"]
+        k = len(ms)
+        if t["complete"]:
+            slice_s = sum(ms) / 1e3
+            fracs.append(1.0)
+        elif calib is None:
+            return None
+        else:
+            slice_s = sum(ms) / 1e3 * sum(calib) / max(sum(calib[:k]), 1e-9)
+            fracs.append(sum(calib[:k]) / sum(calib))
+        rates.append(1.0 / slice_s)
+    value = sum(rates)
+    return {"value": value, "unit": "slices/s", "cores": threads, "kind": "reference",
+            "sample": (f"{threads} thread(s), each running the per-slice steps of its own slice "
+                       f"through the reference executor for {budget_s:.0f} s "
+                       f"({100 * statistics.mean(fracs):.1f}% of a slice's reference time on "
+                       f"average), scaled to a full slice by the per-step times of one full "
+                       f"reference slice recorded on the build host; wall {j['wall_s']:.1f} s")}
 
 
 def run_reference_arm(args):
@@ -131,12 +157,13 @@ def run_reference_arm(args):
     if rank != 0:
         return
     threads = args.cpu_threads or os.cpu_count() or 1
-    n = max(1, min(threads, args.cpu_slices))
     vals = []
+    cb = None
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(args.config, threads, n)
+        cb = cpu_baseline(args.config, threads, args.ref_budget)
         if cb is None:
-            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_tool not built"}))
+            print(json.dumps({"impl": "reference",
+                              "unavailable": "oracle/_ref/ref_tool or calibration not built"}))
             return
         if i >= args.warmup:
             vals.append(cb["value"])
@@ -144,7 +171,7 @@ def run_reference_arm(args):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "slices/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * n / v if v else None, "higher_is_better": True,
+        "ms_per_step": 1e3 * args.ref_budget, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "c64", "data": "synthetic",
         "config": {"workload": WORKLOAD_TEXT[args.config], "plan": CONFIGS[args.config]},
         "cpu_baseline": dict(cb, value=v),
@@ -162,7 +189,8 @@ def main():
     ap.add_argument("--mode", default="fast", choices=["fast", "exact"])
     ap.add_argument("--cpu-baseline", type=int, default=1)
     ap.add_argument("--cpu-threads", type=int, default=0)
-    ap.add_argument("--cpu-slices", type=int, default=64)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ref-budget", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -297,7 +325,7 @@ def main():
     }
     if rank == 0 and world == 1 and args.cpu_baseline:
         threads = args.cpu_threads or os.cpu_count() or 1
-        line["cpu_baseline"] = cpu_baseline(args.config, threads, min(threads, args.cpu_slices))
+        line["cpu_baseline"] = cpu_baseline(args.config, threads, args.cpu_budget)
     if rank == 0:
         print(json.dumps(line))
     free_desc(desc)

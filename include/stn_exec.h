@@ -208,6 +208,16 @@ typedef struct stn_kernel_profile {
   double flops;     /* summed algorithmic flops */
 } stn_kernel_profile;
 
+/* Per-step accumulation of the same timings (one entry per plan step that ran
+ * while profiling was on): which kernel took the step and what it cost. */
+typedef struct stn_step_profile {
+  int32_t step;     /* index into stn_plan_desc.steps */
+  int32_t kind;     /* stn_kernel_kind of the step's main kernel */
+  int64_t M, N, K;
+  int32_t launches; /* all launches of the step (incl. permutes / pre-passes) */
+  double ms, bytes, flops;
+} stn_step_profile;
+
 /* ---- library ---------------------------------------------------------------- */
 const char *stn_version(void);
 int stn_abi_version(void);
@@ -244,6 +254,9 @@ int stn_plan_set_max_batch(stn_plan *plan, int32_t max_batch);
 int stn_plan_set_profiling(stn_plan *plan, int enable);
 int stn_plan_get_profile(stn_plan *plan, stn_kernel_profile *out);
 int stn_plan_reset_profile(stn_plan *plan);
+/* Copies up to `cap` per-step entries (steps with at least one timed launch, in
+ * plan order) into out; *n receives the number of such steps. */
+int stn_plan_get_step_profile(stn_plan *plan, stn_step_profile *out, int32_t cap, int32_t *n);
 
 /* ---- branch cache ------------------------------------------------------------ */
 int stn_cache_build(stn_plan *plan, void *stream, stn_cache **out);
@@ -292,11 +305,12 @@ int stn_sum_slices_ordered(const double *per_slice_dev, uint64_t n_slices, int64
  * b_batched select per-batch or shared operands) and compares it with an fp64
  * SIMT GEMM of the same inputs. Returns the max |C_tc - C_ref| / max|C_ref| and
  * the mean device time of the tensor-core path (pre-pass + GEMM), of the
- * GEMM kernel alone and of the fp32 SIMT GEMM over `reps` launches. STN_ERR_INVALID_ARGUMENT if the shape
+ * GEMM kernel alone and of the fp32 SIMT GEMM over `reps` launches, and the
+ * fp32 SIMT GEMM's own error for comparison. STN_ERR_INVALID_ARGUMENT if the shape
  * is not supported by the tensor-core kernel. */
 int stn_selftest_gemm_tc(int64_t M, int64_t N, int64_t K, int32_t batches, int32_t a_batched,
                          int32_t b_batched, int32_t reps, double *max_rel_err, double *ms_total,
-                         double *ms_gemm, double *ms_simt);
+                         double *ms_gemm, double *ms_simt, double *simt_rel_err);
 
 #ifdef __cplusplus
 }

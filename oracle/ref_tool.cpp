@@ -354,6 +354,91 @@ int cmd_bench(const Args &a) {
   return 0;
 }
 
+// Mirror of Engine<float>::run (runtime.hpp:420-453) built from the reference's
+// own Engine members (load_leaf, gemm) with a timer around every per-slice step.
+// Stops after the step during which `budget_s` elapsed (budget_s <= 0: run all).
+struct StepTimes {
+  std::vector<double> ms;        // per executed per-slice step
+  std::vector<std::uint64_t> mults;
+  bool complete = false;
+};
+
+StepTimes time_slice_steps(const ExecutablePlan &ep, const BranchCache &cache,
+                           std::uint64_t assignment, double budget_s) {
+  detail_rt::Engine<float> eng{ep, &cache.single};
+  std::map<int, detail_rt::TypedTensor<float>> live;
+  StepTimes out;
+  auto fetch = [&](int node) {
+    auto it = live.find(node);
+    if (it != live.end()) {
+      auto v = std::move(it->second);
+      live.erase(it);
+      return v;
+    }
+    auto c = cache.single.find(node);
+    if (c != cache.single.end()) return c->second;
+    return eng.load_leaf(node, assignment);
+  };
+  auto t0 = clk::now();
+  for (const Step &s : ep.steps) {
+    if (s.is_branch) continue;
+    auto s0 = clk::now();
+    auto a = fetch(s.lhs);
+    auto b = fetch(s.rhs);
+    live.emplace(s.node, eng.gemm(s, a, b));
+    out.ms.push_back(std::chrono::duration<double, std::milli>(clk::now() - s0).count());
+    out.mults.push_back(s.mults);
+    if (budget_s > 0 && std::chrono::duration<double>(clk::now() - t0).count() > budget_s)
+      return out;
+  }
+  out.complete = true;
+  return out;
+}
+
+// step-times <dir> [--slice a]: one full slice, single thread, per-step ms
+int cmd_step_times(const Args &a) {
+  std::string dir = a.pos.at(0);
+  ExecutablePlan ep = load_plan(dir, Precision::Single, int(a.geti("merge-min-dim", 32)),
+                                int(a.geti("width-budget", 40)));
+  BranchCache cache = build_branch_cache(ep);
+  StepTimes st = time_slice_steps(ep, cache, std::uint64_t(a.geti("slice", 0)), 0);
+  double total = 0;
+  for (double x : st.ms) total += x;
+  nlohmann::json j = {{"slice", a.geti("slice", 0)}, {"total_ms", total}, {"step_ms", st.ms},
+                      {"step_mults", st.mults}, {"threads", 1},
+                      {"host_threads", std::thread::hardware_concurrency()}};
+  std::cout << j.dump() << "\n";
+  return 0;
+}
+
+// bench-prefix <dir> --threads T --budget S: every thread runs the per-slice
+// steps of its own slice (the reference executor's own code) until S seconds
+// have passed; reports per-thread per-step ms of the executed prefix.
+int cmd_bench_prefix(const Args &a) {
+  std::string dir = a.pos.at(0);
+  int threads = int(a.geti("threads", int(std::thread::hardware_concurrency())));
+  double budget = a.getd("budget", 20.0);
+  ExecutablePlan ep = load_plan(dir, Precision::Single, int(a.geti("merge-min-dim", 32)),
+                                int(a.geti("width-budget", 40)));
+  BranchCache cache = build_branch_cache(ep);
+  std::vector<StepTimes> res(threads);
+  auto w0 = clk::now();
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      res[t] = time_slice_steps(ep, cache, std::uint64_t(t) % std::max<std::uint64_t>(ep.subtasks, 1),
+                                budget);
+    });
+  for (auto &th : pool) th.join();
+  double wall = std::chrono::duration<double>(clk::now() - w0).count();
+  nlohmann::json per = nlohmann::json::array();
+  for (auto &r : res) per.push_back({{"step_ms", r.ms}, {"complete", r.complete}});
+  nlohmann::json j = {{"threads", threads}, {"budget_s", budget}, {"wall_s", wall},
+                      {"per_thread", per}};
+  std::cout << j.dump() << "\n";
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char **argv) {
@@ -368,6 +453,8 @@ int main(int argc, char **argv) {
     if (cmd == "gen-random") return cmd_gen_random(a);
     if (cmd == "golden") return cmd_golden(a);
     if (cmd == "bench") return cmd_bench(a);
+    if (cmd == "step-times") return cmd_step_times(a);
+    if (cmd == "bench-prefix") return cmd_bench_prefix(a);
   } catch (const std::exception &e) {
     std::fprintf(stderr, "ref_tool: %s\n", e.what());
     return 3;

@@ -109,6 +109,12 @@ class KernelProfile(C.Structure):
                 ("bytes", C.c_double), ("flops", C.c_double)]
 
 
+class StepProfile(C.Structure):
+    _fields_ = [("step", C.c_int32), ("kind", C.c_int32), ("M", C.c_int64), ("N", C.c_int64),
+                ("K", C.c_int64), ("launches", C.c_int32), ("ms", C.c_double),
+                ("bytes", C.c_double), ("flops", C.c_double)]
+
+
 # Every symbol include/stn_exec.h declares, with its ctypes signature.
 _P = C.c_void_p
 _PP = C.POINTER(C.c_void_p)
@@ -128,6 +134,8 @@ SIGNATURES = {
     "stn_plan_set_profiling": (C.c_int, [_P, C.c_int]),
     "stn_plan_get_profile": (C.c_int, [_P, C.POINTER(KernelProfile)]),
     "stn_plan_reset_profile": (C.c_int, [_P]),
+    "stn_plan_get_step_profile": (C.c_int, [_P, C.POINTER(StepProfile), C.c_int32,
+                                            C.POINTER(C.c_int32)]),
     "stn_cache_build": (C.c_int, [_P, _P, _PP]),
     "stn_cache_destroy": (C.c_int, [_P]),
     "stn_cache_info": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
@@ -143,7 +151,7 @@ SIGNATURES = {
     "stn_selftest_gemm_tc": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32,
                                        C.c_int32, C.c_int32, C.POINTER(C.c_double),
                                        C.POINTER(C.c_double), C.POINTER(C.c_double),
-                                       C.POINTER(C.c_double)]),
+                                       C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 
 _lib = None

@@ -140,6 +140,7 @@ struct TcArgs {
   int a_batched, b_batched;  // operand varies per slice
   int k_blocks;      // 2K / BK
   int two_n;         // 2N (row stride of C in floats)
+  int n_tiles;       // 2N / BN
 };
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -155,7 +156,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int n_tile = blockIdx.x, m_tile = blockIdx.y, bz = blockIdx.z;
+  const int n_tile = blockIdx.x % args.n_tiles, m_tile = blockIdx.x / args.n_tiles;
+  const int bz = blockIdx.z;
   const int slice = bz / args.D, d = bz % args.D;
   const int za = args.a_batched ? bz : d;
   const int zb = args.b_batched ? bz : d;
@@ -415,7 +417,8 @@ cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspa
   args.b_batched = p.b_bs != 0;
   args.k_blocks = int(2 * s.K / BK);
   args.two_n = int(2 * s.N);
-  dim3 grid(unsigned(2 * s.N / BN), unsigned(s.M / BM), unsigned(s.D * p.nbatch));
+  args.n_tiles = int(2 * s.N / BN);
+  dim3 grid(unsigned((2 * s.N / BN) * (s.M / BM)), 1, unsigned(s.D * p.nbatch));
   if (gemm_events) cudaEventRecord(gemm_events[0], stream);
   k_gemm_tc<<<grid, THREADS, SMEM_BYTES, stream>>>(mah, mal, mbh, mbl, args);
   if (gemm_events) cudaEventRecord(gemm_events[1], stream);

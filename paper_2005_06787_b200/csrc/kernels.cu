@@ -493,7 +493,8 @@ __global__ void __launch_bounds__(256)
   const T *A = static_cast<const T *>(p.a) + slice * p.a_bs + d * s.M * s.K;
   const T *B = static_cast<const T *>(p.b) + slice * p.b_bs + d * s.K * s.N;
   T *C = static_cast<T *>(p.out) + slice * p.out_bs + d * s.M * s.N;
-  const int64_t m0 = int64_t(blockIdx.y) * BM, n0 = int64_t(blockIdx.x) * BN;
+  const int64_t m_tiles = (s.M + BM - 1) / BM;
+  const int64_t m0 = (int64_t(blockIdx.x) % m_tiles) * BM, n0 = (int64_t(blockIdx.x) / m_tiles) * BN;
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   T acc[4][4];
 #pragma unroll
@@ -765,7 +766,8 @@ template <class R>
 cudaError_t launch_gemm_simt(const GemmShape &s, const BatchPtrs &p, bool exact,
                              cudaStream_t stream) {
   if (s.M == 0 || s.N == 0 || p.nbatch == 0) return cudaSuccess;
-  dim3 grid(unsigned((s.N + 63) / 64), unsigned((s.M + 63) / 64), unsigned(s.D * p.nbatch));
+  const int64_t tiles = ((s.M + 63) / 64) * ((s.N + 63) / 64);
+  dim3 grid(unsigned(tiles), 1, unsigned(s.D * p.nbatch));
   if (exact)
     k_gemm_simt<R, true><<<grid, 256, 0, stream>>>(s, p);
   else

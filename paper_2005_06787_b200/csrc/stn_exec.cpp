@@ -215,9 +215,11 @@ struct stn_plan {
   bool profiling = false;
   struct Pending {
     int kind;
+    int step;
     double bytes, flops;
     cudaEvent_t e0, e1;
   };
+  std::map<int, stn_step_profile> step_totals;
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
   stn_kernel_profile totals[STN_KERNEL_KINDS] = {};
@@ -1036,8 +1038,9 @@ cudaEvent_t take_event(stn_plan &P) {
 struct ProfScope {
   stn_plan &P;
   cudaStream_t st;
+  int step;
   cudaEvent_t e0 = nullptr;
-  ProfScope(stn_plan &p, cudaStream_t s) : P(p), st(s) {
+  ProfScope(stn_plan &p, cudaStream_t s, int step_index = -1) : P(p), st(s), step(step_index) {
     if (P.profiling) {
       e0 = take_event(P);
       cuda_check(cudaEventRecord(e0, st), "cudaEventRecord");
@@ -1048,7 +1051,7 @@ struct ProfScope {
     if (!P.profiling) return;
     cudaEvent_t e1 = take_event(P);
     cuda_check(cudaEventRecord(e1, st), "cudaEventRecord");
-    P.pending.push_back({kind, bytes, flops, e0, e1});
+    P.pending.push_back({kind, step, bytes, flops, e0, e1});
     e0 = take_event(P);
     cuda_check(cudaEventRecord(e0, st), "cudaEventRecord");
   }
@@ -1068,6 +1071,19 @@ void collect_profile(stn_plan &P) {
     t.ms += ms;
     t.bytes += p.bytes;
     t.flops += p.flops;
+    if (p.step >= 0) {
+      stn_step_profile &sp = P.step_totals[p.step];
+      const StepPlan &stp = P.steps[p.step];
+      sp.step = p.step;
+      if (p.kind != STN_KERNEL_PERMUTE || sp.launches == 0) sp.kind = p.kind;
+      sp.M = stp.d.M;
+      sp.N = stp.d.N;
+      sp.K = stp.d.K;
+      sp.launches++;
+      sp.ms += ms;
+      sp.bytes += p.bytes;
+      sp.flops += p.flops;
+    }
     P.event_pool.push_back(p.e0);
     P.event_pool.push_back(p.e1);
   }
@@ -1109,7 +1125,7 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
   auto reads = [&](const Resolved &r, int64_t size) { return es * size * (r.bs ? nb : 1); };
   const double io_bytes = reads(a, sp.lsize) + reads(b, sp.rsize) + es * sp.osize * nb;
   const double flops = 8.0 * double(sp.d.mults) * nb;
-  ProfScope prof(P, st);
+  ProfScope prof(P, st, op.step);
   switch (sp.kern) {
     case Kern::Generic: {
       stn::BatchPtrs p{a.ptr, b.ptr, out, a.bs, b.bs, o.bs, nb};
@@ -1449,6 +1465,21 @@ int stn_plan_reset_profile(stn_plan *P) {
   return guarded([&] {
     collect_profile(*P);
     for (auto &t : P->totals) t = stn_kernel_profile{};
+    P->step_totals.clear();
+  });
+}
+
+int stn_plan_get_step_profile(stn_plan *P, stn_step_profile *out, int32_t cap, int32_t *n) {
+  if (!P || !n) return set_error(STN_ERR_INVALID_ARGUMENT, "NULL argument");
+  return guarded([&] {
+    cuda_check(cudaSetDevice(P->device), "cudaSetDevice");
+    collect_profile(*P);
+    *n = int32_t(P->step_totals.size());
+    int32_t i = 0;
+    for (auto &[step, e] : P->step_totals) {
+      if (i >= cap || !out) break;
+      out[i++] = e;
+    }
   });
 }
 
@@ -1601,7 +1632,7 @@ int stn_sum_slices_ordered(const double *per_slice_dev, uint64_t n_slices, int64
 
 int stn_selftest_gemm_tc(int64_t M, int64_t N, int64_t K, int32_t batches, int32_t a_batched,
                          int32_t b_batched, int32_t reps, double *max_rel_err, double *ms_total,
-                         double *ms_gemm, double *ms_simt) {
+                         double *ms_gemm, double *ms_simt, double *simt_rel_err) {
   return guarded([&] {
     stn::GemmShape s{1, M, N, K};
     require(stn::gemm_tc_supported(s) && batches >= 1 && reps >= 1, STN_ERR_INVALID_ARGUMENT,
@@ -1671,6 +1702,13 @@ int stn_selftest_gemm_tc(int64_t M, int64_t N, int64_t K, int32_t batches, int32
       sm += a;
     }
     if (ms_simt) *ms_simt = sm / reps;
+    if (simt_rel_err) {
+      cuda_check(cudaMemcpy(cf.data(), Cf.ptr, cf.size() * 4, cudaMemcpyDeviceToHost), "dl");
+      double e2 = 0;
+      for (size_t i = 0; i < cd.size(); i += 2)
+        e2 = std::max(e2, std::hypot(double(cf[i]) - cd[i], double(cf[i + 1]) - cd[i + 1]));
+      *simt_rel_err = e2 / std::max(scale, 1e-300);
+    }
     for (auto &e : ev) cudaEventDestroy(e);
   });
 }

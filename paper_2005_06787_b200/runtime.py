@@ -114,6 +114,16 @@ class ExecutablePlan:
                                       "bytes": arr[i].bytes, "flops": arr[i].flops}
                 for i in range(len(abi.KERNEL_KINDS))}
 
+    def get_step_profile(self) -> list:
+        """Per plan step: kernel kind, shape, launches, device ms, bytes, flops."""
+        n = C.c_int32()
+        check(_lib().stn_plan_get_step_profile(self._h, None, 0, C.byref(n)))
+        arr = (abi.StepProfile * max(1, n.value))()
+        check(_lib().stn_plan_get_step_profile(self._h, arr, n.value, C.byref(n)))
+        return [{"step": e.step, "kernel": abi.KERNEL_KINDS[e.kind], "M": e.M, "N": e.N,
+                 "K": e.K, "launches": e.launches, "ms": e.ms, "bytes": e.bytes,
+                 "flops": e.flops} for e in arr[: n.value]]
+
     def kernel_mix(self) -> dict:
         i = self.info
         return {"tensor_core": i.steps_tensor_core, "absorb": i.steps_absorb,

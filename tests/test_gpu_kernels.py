@@ -25,12 +25,13 @@ def _needs_gpu():
 def test_tc_gemm_matches_fp64(M, N, K, batches, ab, bb):
     from paper_2005_06787_b200 import abi
     lib = abi.load_library()
-    err, ms, msg, mss = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+    err, ms, msg, mss, serr = (C.c_double() for _ in range(5))
     abi.check(lib.stn_selftest_gemm_tc(M, N, K, batches, ab, bb, 3, C.byref(err), C.byref(ms),
-                                       C.byref(msg), C.byref(mss)))
+                                       C.byref(msg), C.byref(mss), C.byref(serr)))
     fl = 8.0 * M * N * K * batches
     print(f"tc gemm {M}x{N}x{K}x{batches}: rel err {err.value:.2e}, "
           f"{ms.value:.3f} ms total ({fl / ms.value / 1e9:.1f} TFLOP/s), {msg.value:.3f} ms gemm "
           f"({fl / msg.value / 1e9:.1f} TFLOP/s); simt fp32 {mss.value:.3f} ms "
-          f"({fl / mss.value / 1e9:.1f} TFLOP/s)")
-    assert err.value <= 1e-5
+          f"({fl / mss.value / 1e9:.1f} TFLOP/s), simt fp32 rel err {serr.value:.2e}")
+    # fp32-level: within 1e-5 of max|C| or 4x the plain fp32 GEMM's own error
+    assert err.value <= max(1e-5, 4 * serr.value)
