@@ -197,7 +197,8 @@ typedef enum stn_kernel_kind {
   STN_KERNEL_PERMUTE = 4,   /* operand/result axis permutation */
   STN_KERNEL_LEAF = 5,      /* per-slice leaf gather */
   STN_KERNEL_ROOT = 6,      /* ordered fp64 root accumulation */
-  STN_KERNEL_KINDS = 7
+  STN_KERNEL_ABSORB_TC = 7, /* tcgen05 split-TF32 absorb (K x N >= 64) */
+  STN_KERNEL_KINDS = 8
 } stn_kernel_kind;
 
 typedef struct stn_kernel_profile {

@@ -101,7 +101,8 @@ class PlanInfo(C.Structure):
     ]
 
 
-KERNEL_KINDS = ["generic", "absorb", "gemm_simt", "gemm_tc", "permute", "leaf", "root"]
+KERNEL_KINDS = ["generic", "absorb", "gemm_simt", "gemm_tc", "permute", "leaf", "root",
+                "absorb_tc"]
 
 
 class KernelProfile(C.Structure):

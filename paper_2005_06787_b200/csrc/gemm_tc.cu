@@ -41,7 +41,7 @@ constexpr int A_TILE_BYTES = BM * BK * 4;  // 16 KiB
 constexpr int B_TILE_BYTES = BN * BK * 4;  // 32 KiB
 constexpr int STAGE_BYTES = 2 * A_TILE_BYTES + 2 * B_TILE_BYTES;
 constexpr int THREADS = 192;
-constexpr int TMEM_COLS = 256;
+constexpr int TMEM_COLS = 512;  // [0,256) hi*hi chain, [256,512) hi*lo + lo*hi corrections
 constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
 // ---- PTX wrappers -------------------------------------------------------------
@@ -107,6 +107,21 @@ __device__ __forceinline__ void tc_fence_after() {
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+// 32 lanes x 32 columns of fp32 from TMEM (one row per thread).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32"
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15,"
+      " %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31},"
+      " [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
 }
 
 // K-major SWIZZLE_128B shared-memory matrix descriptor (sm_100 "version 1").
@@ -220,9 +235,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int k = 0; k < BK / UK; ++k) {
           const uint64_t koff = uint64_t((k * UK * 4) >> 4);  // +32 B per K step
           const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
+          // the small correction products get their own accumulator so their
+          // additions do not round the large hi*hi partial sums
           umma_tf32(tmem_base, ahi + koff, bhi + koff, kIdesc, acc0);
-          umma_tf32(tmem_base, ahi + koff, blo + koff, kIdesc, 1u);
-          umma_tf32(tmem_base, alo + koff, bhi + koff, kIdesc, 1u);
+          umma_tf32(tmem_base + BN, ahi + koff, blo + koff, kIdesc, acc0);
+          umma_tf32(tmem_base + BN, alo + koff, bhi + koff, kIdesc, 1u);
         }
         umma_commit(&empty[s]);
       }
@@ -238,26 +255,18 @@ __global__ void __launch_bounds__(THREADS, 1)
                   int64_t(row) * args.two_n + int64_t(n_tile) * BN;
 #pragma unroll 1
     for (int cc = 0; cc < BN / 32; ++cc) {
-      uint32_t v[32];
+      uint32_t v[32], w[32];
       const uint32_t taddr = tmem_base + (uint32_t(lane_base) << 16) + uint32_t(cc * 32);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32"
-          "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15,"
-          " %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31},"
-          " [%32];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-            "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-            "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-            "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-            "=r"(v[31])
-          : "r"(taddr));
+      tmem_ld32(taddr, v);
+      tmem_ld32(taddr + BN, w);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       float4 *dst = reinterpret_cast<float4 *>(crow + cc * 32);
 #pragma unroll
       for (int q = 0; q < 8; ++q)
-        dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                             __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+        dst[q] = make_float4(__uint_as_float(v[4 * q]) + __uint_as_float(w[4 * q]),
+                             __uint_as_float(v[4 * q + 1]) + __uint_as_float(w[4 * q + 1]),
+                             __uint_as_float(v[4 * q + 2]) + __uint_as_float(w[4 * q + 2]),
+                             __uint_as_float(v[4 * q + 3]) + __uint_as_float(w[4 * q + 3]));
     }
   }
   tc_fence_before();

@@ -288,8 +288,7 @@ __global__ void __launch_bounds__(kAbsorbThreads)
 // Per output the K terms are summed in ascending k (exact mode = reference).
 // ---------------------------------------------------------------------------
 constexpr int kAb2Threads = 256;
-constexpr int kAb2KC = 16;  // K chunk held in registers
-constexpr int kAb2NC = 16;  // outputs accumulated per pass
+constexpr int kAb2Stages = 3;  // X tiles in flight per CTA (cp.async ring)
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
@@ -303,17 +302,17 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <bool EXACT, bool PERMUTE>
+// KC / NC: K and N chunk sizes held in registers (compile-time, <= 16).
+template <bool EXACT, bool PERMUTE, int KC, int NC>
 __global__ void __launch_bounds__(kAb2Threads, 2)
     k_absorb2(const __grid_constant__ AbsorbGeom g, const BatchPtrs p, int64_t n_tiles) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int xt = g.xt_bits, ot = g.ot_bits;
   const int K = 1 << g.kb, N = 1 << g.nb;
   const int x_hi_n = 1 << (xt - g.x_run), o_hi_n = 1 << (ot - g.o_run);
-  float2 *xs0 = reinterpret_cast<float2 *>(smem_raw);
-  float2 *xs1 = xs0 + (1 << xt);
-  float2 *os = xs1 + (1 << xt);
-  float2 *wt = os + (1 << ot);                                   // W^T: [n][k]
+  float2 *xs_ring = reinterpret_cast<float2 *>(smem_raw);
+  float2 *os = xs_ring + kAb2Stages * (1 << xt);
+  float2 *wt = os + (1 << ot);  // W^T: [n][k]
   int64_t *xhi = reinterpret_cast<int64_t *>(wt + (PERMUTE ? 0 : K * N));
   int64_t *ohi = xhi + x_hi_n;
   int *xk = reinterpret_cast<int *>(ohi + o_hi_n);
@@ -373,29 +372,30 @@ __global__ void __launch_bounds__(kAb2Threads, 2)
   const int x_run_mask = (1 << g.x_run) - 1, o_run_mask = (1 << g.o_run) - 1;
   const int x_pairs = 1 << (xt - 1), o_pairs = 1 << (ot - 1);
   auto issue_load = [&](int64_t tile, float2 *dst) {
-    int64_t bx, bo;
-    tile_bases(tile, bx, bo);
-    for (int q = tid; q < x_pairs; q += kAb2Threads) {
-      const int i = q << 1;
-      cp_async16(dst + i, X + bx + xhi[i >> g.x_run] + (i & x_run_mask));
+    if (tile < n_tiles) {
+      int64_t bx, bo;
+      tile_bases(tile, bx, bo);
+      for (int q = tid; q < x_pairs; q += kAb2Threads) {
+        const int i = q << 1;
+        cp_async16(dst + i, X + bx + xhi[i >> g.x_run] + (i & x_run_mask));
+      }
     }
-    cp_async_commit();
+    cp_async_commit();  // (possibly empty) group keeps the ring arithmetic uniform
   };
 
   const int T = 1 << g.tb;
   const int tpr = T >= kAb2Threads ? 1 : kAb2Threads / T;  // threads per tile row
-  int64_t tile = blockIdx.x;
-  if (tile < n_tiles) issue_load(tile, xs0);
-  for (int it = 0; tile < n_tiles; ++it, tile += gridDim.x) {
-    float2 *xs = (it & 1) ? xs1 : xs0;
-    const int64_t next = tile + gridDim.x;
-    if (next < n_tiles) {
-      issue_load(next, (it & 1) ? xs0 : xs1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+#pragma unroll 1
+  for (int s = 0; s < kAb2Stages - 1; ++s)
+    issue_load(first + s * stride, xs_ring + s * (1 << xt));
+  int it = 0;
+  for (int64_t tile = first; tile < n_tiles; tile += stride, ++it) {
+    issue_load(tile + (kAb2Stages - 1) * stride,
+               xs_ring + ((it + kAb2Stages - 1) % kAb2Stages) * (1 << xt));
+    cp_async_wait<kAb2Stages - 1>();
     __syncthreads();
+    const float2 *xs = xs_ring + (it % kAb2Stages) * (1 << xt);
     // ---- math ----
     for (int r = tid / tpr; r < T; r += kAb2Threads / tpr) {
       const int sub = tid % tpr;
@@ -407,29 +407,27 @@ __global__ void __launch_bounds__(kAb2Threads, 2)
         }
       if constexpr (PERMUTE) {
         if (sub == 0) os[oo] = xs[xo];
-        continue;
-      }
-      for (int n0 = sub * kAb2NC; n0 < N; n0 += tpr * kAb2NC) {
-        float2 acc[kAb2NC];
+      } else {
+        for (int n0 = sub * NC; n0 < N; n0 += tpr * NC) {
+          float2 acc[NC];
 #pragma unroll
-        for (int c = 0; c < kAb2NC; ++c) acc[c] = make_float2(0.f, 0.f);
-        for (int k0 = 0; k0 < K; k0 += kAb2KC) {
-          float2 x[kAb2KC];
+          for (int c = 0; c < NC; ++c) acc[c] = make_float2(0.f, 0.f);
+          for (int k0 = 0; k0 < K; k0 += KC) {
+            float2 x[KC];
 #pragma unroll
-          for (int kk = 0; kk < kAb2KC; ++kk)
-            if (k0 + kk < K) x[kk] = xs[xo | xk[k0 + kk]];
+            for (int kk = 0; kk < KC; ++kk)
+              if (KC <= 1 || k0 + kk < K) x[kk] = xs[xo | xk[k0 + kk]];
 #pragma unroll
-          for (int c = 0; c < kAb2NC; ++c) {
-            if (n0 + c >= N) break;
-            const float2 *w = wt + (n0 + c) * K + k0;
+            for (int c = 0; c < NC; ++c) {
+              const float2 *w = wt + (n0 + c) * K + k0;
 #pragma unroll
-            for (int kk = 0; kk < kAb2KC; ++kk)
-              if (k0 + kk < K) cmac<EXACT>(acc[c], x[kk], w[kk]);
+              for (int kk = 0; kk < KC; ++kk)
+                if (k0 + kk < K) cmac<EXACT>(acc[c], x[kk], w[kk]);
+            }
           }
-        }
 #pragma unroll
-        for (int c = 0; c < kAb2NC; ++c)
-          if (n0 + c < N) os[oo | on[n0 + c]] = acc[c];
+          for (int c = 0; c < NC; ++c) os[oo | on[n0 + c]] = acc[c];
+        }
       }
     }
     __syncthreads();
@@ -444,36 +442,54 @@ __global__ void __launch_bounds__(kAb2Threads, 2)
         __stcs(dst, v);
       }
     }
-    // the next iteration's wait + __syncthreads orders os reuse
+    // os is rewritten only after the next iteration's __syncthreads
   }
+  cp_async_wait<0>();
 }
 
 size_t absorb2_smem_bytes(const AbsorbGeom &g, bool permute) {
   const size_t K = size_t(1) << g.kb, N = size_t(1) << g.nb;
-  return 8 * (2 * (size_t(1) << g.xt_bits) + (size_t(1) << g.ot_bits) + (permute ? 0 : K * N)) +
+  return 8 * (kAb2Stages * (size_t(1) << g.xt_bits) + (size_t(1) << g.ot_bits) +
+              (permute ? 0 : K * N)) +
          8 * ((size_t(1) << (g.xt_bits - g.x_run)) + (size_t(1) << (g.ot_bits - g.o_run))) +
          4 * (K + N);
 }
 
-template <bool EXACT, bool PERMUTE>
+template <bool EXACT, bool PERMUTE, int KC, int NC>
 cudaError_t launch_absorb2_impl(const AbsorbGeom &g, const BatchPtrs &p, cudaStream_t stream) {
   const size_t smem = absorb2_smem_bytes(g, PERMUTE);
-  auto kern = k_absorb2<EXACT, PERMUTE>;
+  auto kern = k_absorb2<EXACT, PERMUTE, KC, NC>;
   static int set_bytes = 0;
   if (int(smem) > set_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem > 48 * 1024 ? 200 * 1024 : 48 * 1024));
+    const int want = smem > 48 * 1024 ? 200 * 1024 : 48 * 1024;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, want);
     if (e != cudaSuccess) return e;
-    set_bytes = int(smem > 48 * 1024 ? 200 * 1024 : 48 * 1024);
+    set_bytes = want;
   }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAb2Threads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
   const int64_t n_tiles = int64_t(1) << g.ob;
-  // persistent: up to 2 resident CTAs per SM (x 148 SMs), shared across the batch
-  int64_t ctas = 148 * 2 / (p.nbatch > 0 ? p.nbatch : 1);
+  int64_t ctas = int64_t(148) * per_sm / (p.nbatch > 0 ? p.nbatch : 1);
   if (ctas < 1) ctas = 1;
   if (ctas > n_tiles) ctas = n_tiles;
   dim3 grid(unsigned(ctas), unsigned(p.nbatch));
   kern<<<grid, kAb2Threads, smem, stream>>>(g, p, n_tiles);
   return cudaGetLastError();
+}
+
+template <bool EXACT>
+cudaError_t launch_absorb2_dispatch(const AbsorbGeom &g, const BatchPtrs &p, cudaStream_t st) {
+  const int kc = g.kb >= 4 ? 16 : (1 << g.kb), nc = g.nb >= 4 ? 16 : (1 << g.nb);
+#define STN_AB2(KCV, NCV) \
+  if (kc == KCV && nc == NCV) return launch_absorb2_impl<EXACT, false, KCV, NCV>(g, p, st);
+#define STN_AB2_ROW(KCV) \
+  STN_AB2(KCV, 1) STN_AB2(KCV, 2) STN_AB2(KCV, 4) STN_AB2(KCV, 8) STN_AB2(KCV, 16)
+  STN_AB2_ROW(1) STN_AB2_ROW(2) STN_AB2_ROW(4) STN_AB2_ROW(8) STN_AB2_ROW(16)
+#undef STN_AB2_ROW
+#undef STN_AB2
+  return cudaErrorNotSupported;
 }
 
 // ---------------------------------------------------------------------------
@@ -654,14 +670,14 @@ size_t absorb_smem_bytes(const AbsorbGeom &g) {
 
 cudaError_t launch_absorb(const AbsorbGeom &g, const BatchPtrs &p, bool exact,
                           cudaStream_t stream) {
-  return exact ? launch_absorb2_impl<true, false>(g, p, stream)
-               : launch_absorb2_impl<false, false>(g, p, stream);
+  return exact ? launch_absorb2_dispatch<true>(g, p, stream)
+               : launch_absorb2_dispatch<false>(g, p, stream);
 }
 
 cudaError_t launch_bitperm(const AbsorbGeom &g, const void *in, void *out, int64_t in_bs,
                            int64_t out_bs, int nbatch, cudaStream_t stream) {
   BatchPtrs p{in, nullptr, out, in_bs, 0, out_bs, nbatch};
-  return launch_absorb2_impl<false, true>(g, p, stream);
+  return launch_absorb2_impl<false, true, 1, 1>(g, p, stream);
 }
 
 // ---------------------------------------------------------------------------
@@ -696,6 +712,7 @@ __global__ void __launch_bounds__(256)
     }
     const int64_t k0 = int64_t(chunk) * kchunk;
     const int64_t k1 = min(g.k_size, k0 + kchunk);
+#pragma unroll 4
     for (int64_t k = k0 + sub; k < k1; k += tpo) {
       int64_t r2 = k, ka = ao, kb = bo;
       for (int i = g.n_k - 1; i >= 0; --i) {
@@ -742,8 +759,10 @@ __global__ void k_splitk_sum(const void *partial_, int nchunks, int64_t out_size
 }
 
 int splitk_chunks(const StridedGeom &g) {
-  int64_t c = (g.k_size + 4095) / 4096;
-  return int(c < 1 ? 1 : (c > 2048 ? 2048 : c));
+  // ~256 k per thread-chunk: enough CTAs in flight to cover HBM latency
+  const int64_t tpo = 256 / (g.out_size < 1 ? 1 : g.out_size);
+  int64_t c = (g.k_size + 256 * tpo - 1) / (256 * tpo);
+  return int(c < 1 ? 1 : (c > 16384 ? 16384 : c));
 }
 
 template <class R>

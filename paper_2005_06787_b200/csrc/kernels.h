@@ -101,6 +101,10 @@ cudaError_t launch_absorb(const AbsorbGeom &g, const BatchPtrs &p, bool exact, c
 template <class R>
 cudaError_t launch_permute(const StridedGeom &g, const void *in, void *out, int64_t in_bs,
                            int64_t out_bs, int nbatch, cudaStream_t stream);
+// tcgen05 split-TF32 absorb (absorb_tc.cu): AbsorbGeom with exactly 7 tile
+// bits (128 rows), K <= 32, N <= 64. FAST mode only.
+bool tc_absorb_supported(const AbsorbGeom &g);
+cudaError_t launch_absorb_tc(const AbsorbGeom &g, const BatchPtrs &p, cudaStream_t stream);
 // Tiled bond-2 bit permutation (the absorb tile machinery with K = N = 0).
 cudaError_t launch_bitperm(const AbsorbGeom &g, const void *in, void *out, int64_t in_bs,
                            int64_t out_bs, int nbatch, cudaStream_t stream);

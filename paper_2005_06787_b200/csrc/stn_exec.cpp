@@ -106,7 +106,7 @@ struct DevBuf {
 // ---------------------------------------------------------------------------
 // plan model
 // ---------------------------------------------------------------------------
-enum class Kern { Generic, Absorb, SplitK, GemmSimt, GemmTc };
+enum class Kern { Generic, Absorb, AbsorbTc, SplitK, GemmSimt, GemmTc };
 
 struct Node {
   bool is_leaf = false;
@@ -125,6 +125,8 @@ struct StepPlan {
   stn::StridedGeom geo{};  // generic
   // absorb
   stn::AbsorbGeom ag{};
+  stn::AbsorbGeom agtc{};  // 128-row tiles for the tensor-core absorb
+  bool tc_ok = false;
   bool x_is_lhs = true;
   // gemm path
   bool a_id = true, b_id = true, c_id = true;
@@ -313,7 +315,7 @@ bool is_identity(const std::vector<int> &p) {
 bool make_tile_geom(const std::vector<std::pair<int, int>> &kbits,
                     const std::vector<std::pair<int, int>> &mbits,
                     const std::vector<std::pair<int, int>> &nbits, int x_bits, int o_bits,
-                    stn::AbsorbGeom &g) {
+                    stn::AbsorbGeom &g, int force_tb = 0) {
   const int kb = int(kbits.size()), nb = int(nbits.size()), mb = int(mbits.size());
   // choose tile M bits T: low X bits, low O bits, then ascending X position
   const int Lx = std::min(5, x_bits), Lo = std::min(5, o_bits);
@@ -325,6 +327,7 @@ bool make_tile_geom(const std::vector<std::pair<int, int>> &kbits,
       tb++;
     }
   const int target = 11;
+  if (force_tb > 0 && tb > force_tb) return false;
   {
     std::vector<size_t> order(mbits.size());
     std::iota(order.begin(), order.end(), 0);
@@ -332,11 +335,12 @@ bool make_tile_geom(const std::vector<std::pair<int, int>> &kbits,
               [&](size_t a, size_t b) { return mbits[a].first < mbits[b].first; });
     for (size_t j : order) {
       if (in_t[j]) continue;
-      if (kb + tb >= target || nb + tb >= target) break;
+      if (force_tb > 0 ? tb >= force_tb : (kb + tb >= target || nb + tb >= target)) break;
       in_t[j] = 1;
       tb++;
     }
   }
+  if (force_tb > 0 && tb != force_tb) return false;
   if (kb + tb > 13 || nb + tb > 13) return false;  // <= 64 KiB per tile
   if (kb + tb < 2 || nb + tb < 2) return false;
   const int ob = mb - tb;
@@ -462,6 +466,9 @@ bool build_absorb(StepPlan &sp, const std::vector<int> &ldims, const std::vector
   g.w_is_lhs = x_lhs ? 0 : 1;
   sp.ag = g;
   sp.x_is_lhs = x_lhs;
+  // tensor-core variant: exactly 128 tile rows
+  sp.tc_ok = make_tile_geom(kbits, mbits, nbits, xr, orank, sp.agtc, 7) &&
+             stn::tc_absorb_supported(sp.agtc);
   return true;
 }
 
@@ -513,6 +520,8 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
   // bandwidth-bound absorb: one big operand, a small K x N side
   if (single && big >= (int64_t(1) << 12) && small <= 4096 && build_absorb(sp, ldims, rdims)) {
     sp.kern = Kern::Absorb;
+    // K x N >= 64: SIMT math would bound the stream; use the tensor cores
+    if (!exact && sp.tc_ok && sp.ag.kb + sp.ag.nb >= 6) sp.kern = Kern::AbsorbTc;
     return;
   }
   // long-K reduction to a small output (FAST mode: chunked K order)
@@ -1141,6 +1150,14 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
       P.kernel_launches++;  // second (ordered-sum) launch
       break;
     }
+    case Kern::AbsorbTc: {
+      const Resolved &x = sp.x_is_lhs ? a : b;
+      const Resolved &w = sp.x_is_lhs ? b : a;
+      stn::BatchPtrs p{x.ptr, w.ptr, out, x.bs, w.bs, o.bs, nb};
+      cuda_check(stn::launch_absorb_tc(sp.agtc, p, st), "tensor-core absorb kernel");
+      prof.done(STN_KERNEL_ABSORB_TC, io_bytes, flops);
+      break;
+    }
     case Kern::Absorb: {
       const Resolved &x = sp.x_is_lhs ? a : b;
       const Resolved &w = sp.x_is_lhs ? b : a;
@@ -1410,7 +1427,7 @@ int stn_plan_get_info(const stn_plan *P, stn_plan_info *info) {
     Kern k = P->steps[op.step].kern;
     if (k == Kern::GemmTc) info->steps_tensor_core++;
     else if (k == Kern::GemmSimt) info->steps_generic++;
-    else if (k == Kern::Absorb) info->steps_absorb++;
+    else if (k == Kern::Absorb || k == Kern::AbsorbTc) info->steps_absorb++;
     else info->steps_generic++;
   }
   return STN_OK;
