@@ -126,7 +126,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t *tk_lo = tk_hi + x_hi_n;                              // ... of the low run bits
   int *on = reinterpret_cast<int *>(tk_lo + (1 << g.x_run));
   int *oo_t = on + N;                                            // O-tile offset of row t
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(oo_t + kRows);
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(
+      (reinterpret_cast<uintptr_t>(oo_t + kRows) + 7) & ~uintptr_t(7));
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(mbar + 1);
 
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
@@ -222,18 +223,44 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int x_run_mask = (1 << g.x_run) - 1, o_run_mask = (1 << g.o_run) - 1;
   const int x_pairs = 1 << (xt - 1), o_pairs = 1 << (ot - 1);
   uint32_t phase = 0;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    int64_t bx = 0, bo = 0;
+  // X pairs are prefetched into registers one tile ahead, so the HBM latency
+  // of tile i+1 overlaps the MMA, epilogue and store of tile i.
+  constexpr int LD = KP == 16 ? 8 : 16;  // max float4 per thread (x_pairs / 128)
+  float4 pre[LD];
+  auto tile_base = [&](int64_t tile, int64_t &bx, int64_t &bo) {
+    bx = 0;
+    bo = 0;
     for (int j = 0; j < g.ob; ++j)
       if ((tile >> j) & 1) {
         bx += int64_t(1) << g.outer_x[j];
         bo += int64_t(1) << g.outer_o[j];
       }
-    // ---- gather X tile -> TF32 hi/lo planes ----
-    for (int q = tid; q < x_pairs; q += kThreads) {
+  };
+  auto prefetch = [&](int64_t tile) {
+    if (tile >= n_tiles) return;
+    int64_t bx, bo;
+    tile_base(tile, bx, bo);
+#pragma unroll
+    for (int u = 0; u < LD; ++u) {
+      const int q = tid + u * kThreads;
+      if (q < x_pairs) {
+        const int i = q << 1;
+        pre[u] = __ldcs(reinterpret_cast<const float4 *>(X + bx + xhi[i >> g.x_run] +
+                                                         (i & x_run_mask)));
+      }
+    }
+  };
+  prefetch(blockIdx.x);
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    int64_t bx, bo;
+    tile_base(tile, bx, bo);
+    // ---- prefetched X pairs -> TF32 hi/lo planes ----
+#pragma unroll
+    for (int u = 0; u < LD; ++u) {
+      const int q = tid + u * kThreads;
+      if (q >= x_pairs) break;
       const int i = q << 1;
-      const float4 v = __ldcs(reinterpret_cast<const float4 *>(
-          X + bx + xhi[i >> g.x_run] + (i & x_run_mask)));
+      const float4 v = pre[u];
       const uint32_t base_tk = tk_hi[i >> g.x_run];
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
@@ -268,6 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       umma_commit(mbar);
     }
+    prefetch(tile + gridDim.x);
     mbar_wait(mbar, phase);
     phase ^= 1;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -316,7 +344,7 @@ size_t tc_absorb_smem(const AbsorbGeom &g) {
   const size_t o_hi_n = size_t(1) << (g.ot_bits - g.o_run);
   return 1024 + 2 * size_t(L::A_PLANE) + 2 * size_t(L::B_PLANE) + 8 * (size_t(1) << g.ot_bits) +
          8 * (x_hi_n + o_hi_n) + 4 * (x_hi_n + (size_t(1) << g.x_run)) +
-         4 * ((size_t(1) << g.nb) + kRows) + 64;
+         4 * ((size_t(1) << g.nb) + kRows) + 64 + 8;
 }
 
 template <int KP, int NP>

@@ -12,12 +12,14 @@
 // C ~= Ahi.Bhi + Ahi.Blo + Alo.Bhi, accumulated in fp32 in TMEM. The dropped
 // Alo.Blo term is ~2^-22 relative, so results carry fp32-level accuracy.
 //
-// Kernel anatomy (one CTA per 128 x 256 real output tile):
-//   warp 0      TMA producer: A hi/lo (128 x 32) and B'' hi/lo (256 x 32) tiles,
-//               SWIZZLE_128B, two-stage mbarrier ring
-//   warp 1      MMA issuer: 3 x 4 tcgen05.mma.kind::tf32 (128x256x8) per stage,
-//               tcgen05.commit frees the stage / signals the epilogue
-//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 from TMEM -> registers -> global
+// Kernel anatomy (one CTA per 128 x 128 real output tile):
+//   warp 0      TMA producer: A hi/lo (128 x 32) and B'' hi/lo (128 x 32) tiles,
+//               SWIZZLE_128B, three-stage mbarrier ring
+//   warp 1      MMA issuer: 3 x 4 tcgen05.mma.kind::tf32 (128x128x8) per stage
+//               into one of two TMEM buffers (hi*hi chain + correction chain);
+//               tcgen05.commit frees the stage / hands a finished K chunk over
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 of each K chunk, fp32 RN
+//               accumulation in registers, then one row per thread to global
 // The operand splits (A hi/lo, B'' hi/lo) are produced by two bandwidth-bound
 // pre-pass kernels into a workspace.
 #include <cuda.h>
@@ -33,15 +35,16 @@ namespace stn {
 namespace {
 
 constexpr int BM = 128;        // rows of C per CTA (UMMA M)
-constexpr int BN = 256;        // real columns of C per CTA (UMMA N)
+constexpr int BN = 128;        // real columns of C per CTA (UMMA N)
 constexpr int BK = 32;         // real K per stage (128 B rows -> SWIZZLE_128B)
 constexpr int UK = 8;          // real K per tcgen05.mma (32 B of tf32)
-constexpr int STAGES = 2;
+constexpr int STAGES = 3;
+constexpr int CHUNK = 8;       // k-blocks accumulated in TMEM before an fp32 RN flush
 constexpr int A_TILE_BYTES = BM * BK * 4;  // 16 KiB
 constexpr int B_TILE_BYTES = BN * BK * 4;  // 32 KiB
 constexpr int STAGE_BYTES = 2 * A_TILE_BYTES + 2 * B_TILE_BYTES;
 constexpr int THREADS = 192;
-constexpr int TMEM_COLS = 512;  // [0,256) hi*hi chain, [256,512) hi*lo + lo*hi corrections
+constexpr int TMEM_COLS = 512;  // 2 buffers x {hi*hi chain, hi*lo + lo*hi corrections} x BN
 constexpr size_t SMEM_BYTES = size_t(STAGES) * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
 // ---- PTX wrappers -------------------------------------------------------------
@@ -76,6 +79,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     if (iter == 0) start = clock64();
     if ((iter & 1023) == 1023 && clock64() - start > (4ll << 30)) __trap();
   }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar,
@@ -167,8 +174,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
   uint64_t *empty = full + STAGES;
-  uint64_t *tmem_full = empty + STAGES;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+  uint64_t *tmem_full = empty + STAGES;   // [2]: chunk accumulated in TMEM buffer b
+  uint64_t *tmem_empty = tmem_full + 2;   // [2]: epilogue drained TMEM buffer b
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int n_tile = blockIdx.x % args.n_tiles, m_tile = blockIdx.x / args.n_tiles;
@@ -188,7 +196,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -221,9 +232,20 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // ---- MMA issuer ----
+      // K is accumulated in chunks of CHUNK k-blocks, alternating between two
+      // TMEM buffers; the epilogue adds each finished chunk into fp32
+      // registers with round-to-nearest, so long K chains do not accumulate the
+      // tensor core's truncating adds.
       for (int kb = 0; kb < args.k_blocks; ++kb) {
         const int s = kb % STAGES;
         const uint32_t phase = (kb / STAGES) & 1;
+        const int chunk = kb / CHUNK, buf = chunk & 1;
+        const bool chunk_first = kb % CHUNK == 0;
+        const bool chunk_last = kb % CHUNK == CHUNK - 1 || kb == args.k_blocks - 1;
+        if (chunk_first) {
+          mbar_wait(&tmem_empty[buf], ((chunk >> 1) & 1) ^ 1);
+          tc_fence_after();
+        }
         mbar_wait(&full[s], phase);
         tc_fence_after();
         const uint32_t st = smem_u32(smem + s * STAGE_BYTES);
@@ -231,43 +253,53 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint64_t alo = smem_desc_sw128(st + A_TILE_BYTES);
         const uint64_t bhi = smem_desc_sw128(st + 2 * A_TILE_BYTES);
         const uint64_t blo = smem_desc_sw128(st + 2 * A_TILE_BYTES + B_TILE_BYTES);
+        const uint32_t tmain = tmem_base + uint32_t(buf * 2 * BN), tcorr = tmain + BN;
 #pragma unroll
         for (int k = 0; k < BK / UK; ++k) {
           const uint64_t koff = uint64_t((k * UK * 4) >> 4);  // +32 B per K step
-          const uint32_t acc0 = (kb > 0 || k > 0) ? 1u : 0u;
+          const uint32_t acc0 = (!chunk_first || k > 0) ? 1u : 0u;
           // the small correction products get their own accumulator so their
           // additions do not round the large hi*hi partial sums
-          umma_tf32(tmem_base, ahi + koff, bhi + koff, kIdesc, acc0);
-          umma_tf32(tmem_base + BN, ahi + koff, blo + koff, kIdesc, acc0);
-          umma_tf32(tmem_base + BN, alo + koff, bhi + koff, kIdesc, 1u);
+          umma_tf32(tmain, ahi + koff, bhi + koff, kIdesc, acc0);
+          umma_tf32(tcorr, ahi + koff, blo + koff, kIdesc, acc0);
+          umma_tf32(tcorr, alo + koff, bhi + koff, kIdesc, 1u);
         }
         umma_commit(&empty[s]);
+        if (chunk_last) umma_commit(&tmem_full[buf]);
       }
-      umma_commit(tmem_full);
     }
   } else {
-    // ---- epilogue: TMEM -> registers -> global ----
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
+    // ---- epilogue: drain TMEM chunks into fp32 registers, then global ----
     const int lane_base = 32 * (warp % 4);
     const int row = m_tile * BM + lane_base + lane;
+    float acc[BN];
+#pragma unroll
+    for (int c = 0; c < BN; ++c) acc[c] = 0.f;
+    const int n_chunks = (args.k_blocks + CHUNK - 1) / CHUNK;
+    for (int chunk = 0; chunk < n_chunks; ++chunk) {
+      const int buf = chunk & 1;
+      mbar_wait(&tmem_full[buf], (chunk >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tmain = tmem_base + (uint32_t(lane_base) << 16) + uint32_t(buf * 2 * BN);
+#pragma unroll
+      for (int cc = 0; cc < 2 * BN / 32; ++cc) {  // main columns, then corrections
+        uint32_t v[32];
+        tmem_ld32(tmain + uint32_t(cc * 32), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int c0 = (cc * 32) % BN;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc[c0 + q] += __uint_as_float(v[q]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[buf]);
+    }
     float *crow = args.c + int64_t(slice) * args.c_bs + int64_t(d) * args.c_ds +
                   int64_t(row) * args.two_n + int64_t(n_tile) * BN;
-#pragma unroll 1
-    for (int cc = 0; cc < BN / 32; ++cc) {
-      uint32_t v[32], w[32];
-      const uint32_t taddr = tmem_base + (uint32_t(lane_base) << 16) + uint32_t(cc * 32);
-      tmem_ld32(taddr, v);
-      tmem_ld32(taddr + BN, w);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      float4 *dst = reinterpret_cast<float4 *>(crow + cc * 32);
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        dst[q] = make_float4(__uint_as_float(v[4 * q]) + __uint_as_float(w[4 * q]),
-                             __uint_as_float(v[4 * q + 1]) + __uint_as_float(w[4 * q + 1]),
-                             __uint_as_float(v[4 * q + 2]) + __uint_as_float(w[4 * q + 2]),
-                             __uint_as_float(v[4 * q + 3]) + __uint_as_float(w[4 * q + 3]));
-    }
+    for (int q = 0; q < BN / 4; ++q)
+      reinterpret_cast<float4 *>(crow)[q] =
+          make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
   }
   tc_fence_before();
   __syncthreads();

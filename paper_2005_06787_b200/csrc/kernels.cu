@@ -689,51 +689,50 @@ cudaError_t launch_bitperm(const AbsorbGeom &g, const void *in, void *out, int64
 // ---------------------------------------------------------------------------
 template <class R>
 __global__ void __launch_bounds__(256)
-    k_splitk_partial(const __grid_constant__ StridedGeom g, const BatchPtrs p, int64_t kchunk,
-                     int nchunks, void *partial_) {
+    k_splitk_partial(const __grid_constant__ StridedGeom g, const BatchPtrs p, DotTables t,
+                     int kc, int nchunks, void *partial_) {
   using T = cx_t<R>;
-  __shared__ T red[256];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T *sA = reinterpret_cast<T *>(smem_raw);  // [M][kc + 1]
+  T *sB = sA + t.M * (kc + 1);              // [N][kc + 1]
   const int b = blockIdx.y, chunk = blockIdx.x;
   const T *A = static_cast<const T *>(p.a) + int64_t(b) * p.a_bs;
   const T *B = static_cast<const T *>(p.b) + int64_t(b) * p.b_bs;
   T *partial = static_cast<T *>(partial_) + (int64_t(b) * nchunks + chunk) * g.out_size;
-  const int tpo = 256 / int(g.out_size);  // threads per output (consecutive k)
-  const int o = threadIdx.x / tpo, sub = threadIdx.x % tpo;
-  T acc;
-  acc.x = acc.y = 0;
-  if (o < g.out_size) {
-    int64_t rem = o, ao = 0, bo = 0;
-    for (int i = g.n_out - 1; i >= 0; --i) {
-      const int sh = __ffsll(g.out_dim[i]) - 1;
-      const int64_t idx = rem & (g.out_dim[i] - 1);
-      rem >>= sh;
-      ao += idx * g.out_sa[i];
-      bo += idx * g.out_sb[i];
+  const int64_t k0 = int64_t(chunk) * kc;
+  const int len = int(min(int64_t(kc), g.k_size - k0));
+  auto koff = [&](int64_t k, int64_t &ka, int64_t &kb) {
+    ka = 0;
+    kb = 0;
+    for (int i = g.n_k - 1; i >= 0; --i) {
+      const int sh = __ffsll(g.k_dim[i]) - 1;
+      const int64_t idx = k & (g.k_dim[i] - 1);
+      k >>= sh;
+      ka += idx * g.k_sa[i];
+      kb += idx * g.k_sb[i];
     }
-    const int64_t k0 = int64_t(chunk) * kchunk;
-    const int64_t k1 = min(g.k_size, k0 + kchunk);
-#pragma unroll 4
-    for (int64_t k = k0 + sub; k < k1; k += tpo) {
-      int64_t r2 = k, ka = ao, kb = bo;
-      for (int i = g.n_k - 1; i >= 0; --i) {
-        const int sh = __ffsll(g.k_dim[i]) - 1;
-        const int64_t idx = r2 & (g.k_dim[i] - 1);
-        r2 >>= sh;
-        ka += idx * g.k_sa[i];
-        kb += idx * g.k_sb[i];
-      }
-      cmac<false>(acc, A[ka], B[kb]);
+  };
+  // stage A[:, chunk] and B[:, chunk]: consecutive threads take consecutive k
+  for (int idx = threadIdx.x; idx < (t.M + t.N) * kc; idx += blockDim.x) {
+    const int row = idx / kc, kk = idx % kc;
+    T v;
+    v.x = v.y = 0;
+    if (kk < len) {
+      int64_t ka, kb;
+      koff(k0 + kk, ka, kb);
+      v = row < t.M ? A[t.a_row[row] + ka] : B[t.b_col[row - t.M] + kb];
     }
+    sA[row * (kc + 1) + kk] = v;  // sB follows sA contiguously
   }
-  red[threadIdx.x] = acc;
   __syncthreads();
-  if (o < g.out_size && sub == 0) {
-    T s = red[threadIdx.x];
-    for (int j = 1; j < tpo; ++j) {
-      s.x += red[threadIdx.x + j].x;
-      s.y += red[threadIdx.x + j].y;
-    }
-    partial[o] = s;
+  for (int o = threadIdx.x; o < g.out_size; o += blockDim.x) {
+    const int mn = t.o_mn[o];
+    const T *ra = sA + (mn & 0xFFFF) * (kc + 1);
+    const T *rb = sB + (mn >> 16) * (kc + 1);
+    T acc;
+    acc.x = acc.y = 0;
+    for (int kk = 0; kk < len; ++kk) cmac<false>(acc, ra[kk], rb[kk]);
+    partial[o] = acc;
   }
 }
 
@@ -758,27 +757,34 @@ __global__ void k_splitk_sum(const void *partial_, int nchunks, int64_t out_size
   }
 }
 
-int splitk_chunks(const StridedGeom &g) {
-  // ~256 k per thread-chunk: enough CTAs in flight to cover HBM latency
-  const int64_t tpo = 256 / (g.out_size < 1 ? 1 : g.out_size);
-  int64_t c = (g.k_size + 256 * tpo - 1) / (256 * tpo);
-  return int(c < 1 ? 1 : (c > 16384 ? 16384 : c));
+// k per chunk: A and B rows of the chunk fit in 48 KiB of shared memory
+int splitk_kc(const DotTables &t, size_t esize) {
+  int kc = 256;
+  while (kc > 8 && size_t(t.M + t.N) * (kc + 1) * esize > 48 * 1024) kc /= 2;
+  return kc;
+}
+
+int splitk_chunks(const StridedGeom &g, const DotTables &t, size_t esize) {
+  const int64_t kc = splitk_kc(t, esize);
+  return int((g.k_size + kc - 1) / kc);
 }
 
 template <class R>
-cudaError_t launch_splitk(const StridedGeom &g, const BatchPtrs &p, void *workspace,
-                          cudaStream_t stream) {
-  const int nchunks = splitk_chunks(g);
-  const int64_t kchunk = (g.k_size + nchunks - 1) / nchunks;
-  k_splitk_partial<R><<<dim3(nchunks, p.nbatch), 256, 0, stream>>>(g, p, kchunk, nchunks,
-                                                                   workspace);
+cudaError_t launch_splitk(const StridedGeom &g, const BatchPtrs &p, const DotTables &t,
+                          void *workspace, cudaStream_t stream) {
+  const int kc = splitk_kc(t, sizeof(cx_t<R>));
+  const int nchunks = splitk_chunks(g, t, sizeof(cx_t<R>));
+  const size_t smem = size_t(t.M + t.N) * (kc + 1) * sizeof(cx_t<R>);
+  k_splitk_partial<R><<<dim3(nchunks, p.nbatch), 256, smem, stream>>>(g, p, t, kc, nchunks,
+                                                                      workspace);
   k_splitk_sum<R><<<grid_for(g.out_size * p.nbatch, 256), 256, 0, stream>>>(
       workspace, nchunks, g.out_size, p.nbatch, p.out, p.out_bs);
   return cudaGetLastError();
 }
 
-size_t splitk_workspace_bytes(const StridedGeom &g, int nbatch, size_t esize) {
-  return size_t(splitk_chunks(g)) * g.out_size * nbatch * esize;
+size_t splitk_workspace_bytes(const StridedGeom &g, const DotTables &t, int nbatch,
+                              size_t esize) {
+  return size_t(splitk_chunks(g, t, esize)) * g.out_size * nbatch * esize;
 }
 
 template <class R>
@@ -829,10 +835,10 @@ template cudaError_t launch_gemm_simt<float>(const GemmShape &, const BatchPtrs 
                                              cudaStream_t);
 template cudaError_t launch_gemm_simt<double>(const GemmShape &, const BatchPtrs &, bool,
                                               cudaStream_t);
-template cudaError_t launch_splitk<float>(const StridedGeom &, const BatchPtrs &, void *,
-                                          cudaStream_t);
-template cudaError_t launch_splitk<double>(const StridedGeom &, const BatchPtrs &, void *,
-                                           cudaStream_t);
+template cudaError_t launch_splitk<float>(const StridedGeom &, const BatchPtrs &,
+                                          const DotTables &, void *, cudaStream_t);
+template cudaError_t launch_splitk<double>(const StridedGeom &, const BatchPtrs &,
+                                           const DotTables &, void *, cudaStream_t);
 template cudaError_t launch_leaf_gather<float>(const LeafGatherTable &, void *, const int32_t *,
                                                int, cudaStream_t);
 template cudaError_t launch_leaf_gather<double>(const LeafGatherTable &, void *, const int32_t *,

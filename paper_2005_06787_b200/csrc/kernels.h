@@ -109,10 +109,18 @@ cudaError_t launch_absorb_tc(const AbsorbGeom &g, const BatchPtrs &p, cudaStream
 cudaError_t launch_bitperm(const AbsorbGeom &g, const void *in, void *out, int64_t in_bs,
                            int64_t out_bs, int nbatch, cudaStream_t stream);
 // Split-K reduction (small output, long K; FAST mode). Pow2 geometries, out_size <= 256.
+// The output factorises into A rows (M) x B columns (N); o_mn[o] = m | n << 16.
+struct DotTables {
+  int M, N;
+  const int64_t *a_row;  // [M] A offset of row m
+  const int64_t *b_col;  // [N] B offset of column n
+  const int32_t *o_mn;   // [out_size]
+};
 template <class R>
-cudaError_t launch_splitk(const StridedGeom &g, const BatchPtrs &p, void *workspace,
-                          cudaStream_t stream);
-size_t splitk_workspace_bytes(const StridedGeom &g, int nbatch, size_t esize);
+cudaError_t launch_splitk(const StridedGeom &g, const BatchPtrs &p, const DotTables &t,
+                          void *workspace, cudaStream_t stream);
+size_t splitk_workspace_bytes(const StridedGeom &g, const DotTables &t, int nbatch,
+                              size_t esize);
 template <class R>
 cudaError_t launch_gemm_simt(const GemmShape &s, const BatchPtrs &p, bool exact,
                              cudaStream_t stream);

@@ -135,6 +135,9 @@ struct StepPlan {
   stn::AbsorbGeom pag{}, pbg{}, pcg{};
   stn::GemmShape gs{};
   int64_t lsize = 0, rsize = 0, osize = 0;
+  // split-K dot tables (device)
+  std::shared_ptr<DevBuf> dot_buf, dot_mn;
+  stn::DotTables dot{};
 };
 
 enum class Src { ConstLeaf, SliceLeaf, Cache, Arena, Persist };
@@ -529,7 +532,56 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     bool pow2 = true;
     for (int i = 0; i < sp.geo.n_out; ++i) pow2 &= (sp.geo.out_dim[i] & (sp.geo.out_dim[i] - 1)) == 0;
     for (int i = 0; i < sp.geo.n_k; ++i) pow2 &= (sp.geo.k_dim[i] & (sp.geo.k_dim[i] - 1)) == 0;
-    if (pow2) {
+    // factorise the output into A rows x B columns (no D axes)
+    bool factor = pow2;
+    std::vector<int> m_ax, n_ax;
+    for (int i = 0; i < sp.geo.n_out && factor; ++i) {
+      if (sp.geo.out_sa[i] != 0 && sp.geo.out_sb[i] != 0) factor = false;
+      else if (sp.geo.out_sb[i] == 0) m_ax.push_back(i);
+      else n_ax.push_back(i);
+    }
+    if (factor) {
+      auto enumerate = [&](const std::vector<int> &ax, bool use_a) {
+        std::vector<int64_t> offs{0};
+        for (int i : ax) {  // outermost first -> row-major enumeration
+          std::vector<int64_t> nx;
+          for (int64_t base : offs)
+            for (int64_t v = 0; v < sp.geo.out_dim[i]; ++v)
+              nx.push_back(base + v * (use_a ? sp.geo.out_sa[i] : sp.geo.out_sb[i]));
+          offs.swap(nx);
+        }
+        return offs;
+      };
+      std::vector<int64_t> a_row = enumerate(m_ax, true), b_col = enumerate(n_ax, false);
+      // output o -> (m, n): decompose o over the out axes
+      std::vector<int32_t> o_mn(size_t(sp.geo.out_size));
+      for (int64_t o = 0; o < sp.geo.out_size; ++o) {
+        int64_t rem = o, m = 0, n = 0, mstride = 1, nstride = 1;
+        for (int i = sp.geo.n_out - 1; i >= 0; --i) {
+          const int64_t idx = rem % sp.geo.out_dim[i];
+          rem /= sp.geo.out_dim[i];
+          if (sp.geo.out_sb[i] == 0) {
+            m += idx * mstride;
+            mstride *= sp.geo.out_dim[i];
+          } else {
+            n += idx * nstride;
+            nstride *= sp.geo.out_dim[i];
+          }
+        }
+        o_mn[size_t(o)] = int32_t(m | (n << 16));
+      }
+      std::vector<int64_t> packed(a_row);
+      packed.insert(packed.end(), b_col.begin(), b_col.end());
+      sp.dot_buf = std::make_shared<DevBuf>();
+      sp.dot_buf->upload(packed);
+      auto mn_buf = std::make_shared<DevBuf>();
+      mn_buf->upload(o_mn);
+      sp.dot.M = int(a_row.size());
+      sp.dot.N = int(b_col.size());
+      sp.dot.a_row = sp.dot_buf->as<int64_t>();
+      sp.dot.b_col = sp.dot_buf->as<int64_t>() + a_row.size();
+      sp.dot.o_mn = mn_buf->as<int32_t>();
+      sp.dot_mn = mn_buf;
       sp.kern = Kern::SplitK;
       return;
     }
@@ -1144,8 +1196,9 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
     }
     case Kern::SplitK: {
       stn::BatchPtrs p{a.ptr, b.ptr, out, a.bs, b.bs, o.bs, nb};
-      P.splitk_ws.reserve(std::max<size_t>(stn::splitk_workspace_bytes(sp.geo, nb, P.esize), 16));
-      cuda_check(stn::launch_splitk<R>(sp.geo, p, P.splitk_ws.ptr, st), "split-K kernel");
+      P.splitk_ws.reserve(
+          std::max<size_t>(stn::splitk_workspace_bytes(sp.geo, sp.dot, nb, P.esize), 16));
+      cuda_check(stn::launch_splitk<R>(sp.geo, p, sp.dot, P.splitk_ws.ptr, st), "split-K kernel");
       prof.done(STN_KERNEL_GENERIC, io_bytes, flops);
       P.kernel_launches++;  // second (ordered-sum) launch
       break;
