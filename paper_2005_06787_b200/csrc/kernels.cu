@@ -303,7 +303,9 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // KC / NC: K and N chunk sizes held in registers (compile-time, <= 16).
-template <bool EXACT, bool PERMUTE, int KC, int NC>
+// BLOCKED (large K x N): each thread owns a KC x NC = RB x CB block of (rows,
+// columns) and runs the k loop as an outer product (8 FMA per shared load).
+template <bool EXACT, bool PERMUTE, int KC, int NC, bool BLOCKED = false>
 __global__ void __launch_bounds__(kAb2Threads, 2)
     k_absorb2(const __grid_constant__ AbsorbGeom g, const BatchPtrs p, int64_t n_tiles) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -397,6 +399,45 @@ __global__ void __launch_bounds__(kAb2Threads, 2)
     __syncthreads();
     const float2 *xs = xs_ring + (it % kAb2Stages) * (1 << xt);
     // ---- math ----
+    if constexpr (BLOCKED) {
+      constexpr int RB = KC, CB = NC;
+      const int row_groups = T / RB, items = row_groups * (N / CB);
+      for (int item = tid; item < items; item += kAb2Threads) {
+        const int r0 = (item % row_groups) * RB, c0 = (item / row_groups) * CB;
+        int xo[RB], oo[RB];
+#pragma unroll
+        for (int i = 0; i < RB; ++i) {
+          xo[i] = 0;
+          oo[i] = 0;
+          for (int j = 0; j < g.tb; ++j)
+            if (((r0 + i) >> j) & 1) {
+              xo[i] |= 1 << g.t_xl[j];
+              oo[i] |= 1 << g.t_ol[j];
+            }
+        }
+        float2 acc[RB][CB];
+#pragma unroll
+        for (int i = 0; i < RB; ++i)
+#pragma unroll
+          for (int j = 0; j < CB; ++j) acc[i][j] = make_float2(0.f, 0.f);
+        for (int k = 0; k < K; ++k) {
+          const int xkk = xk[k];
+          float2 xv[RB], wv[CB];
+#pragma unroll
+          for (int i = 0; i < RB; ++i) xv[i] = xs[xo[i] | xkk];
+#pragma unroll
+          for (int j = 0; j < CB; ++j) wv[j] = wt[(c0 + j) * K + k];
+#pragma unroll
+          for (int i = 0; i < RB; ++i)
+#pragma unroll
+            for (int j = 0; j < CB; ++j) cmac<EXACT>(acc[i][j], xv[i], wv[j]);
+        }
+#pragma unroll
+        for (int i = 0; i < RB; ++i)
+#pragma unroll
+          for (int j = 0; j < CB; ++j) os[oo[i] | on[c0 + j]] = acc[i][j];
+      }
+    } else
     for (int r = tid / tpr; r < T; r += kAb2Threads / tpr) {
       const int sub = tid % tpr;
       int xo = 0, oo = 0;
@@ -455,10 +496,10 @@ size_t absorb2_smem_bytes(const AbsorbGeom &g, bool permute) {
          4 * (K + N);
 }
 
-template <bool EXACT, bool PERMUTE, int KC, int NC>
+template <bool EXACT, bool PERMUTE, int KC, int NC, bool BLOCKED = false>
 cudaError_t launch_absorb2_impl(const AbsorbGeom &g, const BatchPtrs &p, cudaStream_t stream) {
   const size_t smem = absorb2_smem_bytes(g, PERMUTE);
-  auto kern = k_absorb2<EXACT, PERMUTE, KC, NC>;
+  auto kern = k_absorb2<EXACT, PERMUTE, KC, NC, BLOCKED>;
   static int set_bytes = 0;
   if (int(smem) > set_bytes) {
     const int want = smem > 48 * 1024 ? 200 * 1024 : 48 * 1024;
@@ -481,6 +522,12 @@ cudaError_t launch_absorb2_impl(const AbsorbGeom &g, const BatchPtrs &p, cudaStr
 
 template <bool EXACT>
 cudaError_t launch_absorb2_dispatch(const AbsorbGeom &g, const BatchPtrs &p, cudaStream_t st) {
+  // large K x N: register-blocked outer products (4 rows x CB columns)
+  if (g.kb + g.nb >= 8 && g.tb >= 2) {
+    if (g.nb >= 2) return launch_absorb2_impl<EXACT, false, 4, 4, true>(g, p, st);
+    if (g.nb == 1) return launch_absorb2_impl<EXACT, false, 4, 2, true>(g, p, st);
+    return launch_absorb2_impl<EXACT, false, 4, 1, true>(g, p, st);
+  }
   const int kc = g.kb >= 4 ? 16 : (1 << g.kb), nc = g.nb >= 4 ? 16 : (1 << g.nb);
 #define STN_AB2(KCV, NCV) \
   if (kc == KCV && nc == NCV) return launch_absorb2_impl<EXACT, false, KCV, NCV>(g, p, st);
@@ -736,25 +783,34 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// One CTA per (batch, output): 256 threads sum strided chunk subsets, then a
+// fixed-shape tree in shared memory -- deterministic for a given chunk count.
 template <class R>
-__global__ void k_splitk_sum(const void *partial_, int nchunks, int64_t out_size, int nbatch,
-                             void *out_, int64_t out_bs) {
+__global__ void __launch_bounds__(256)
+    k_splitk_sum(const void *partial_, int nchunks, int64_t out_size, int nbatch, void *out_,
+                 int64_t out_bs) {
   using T = cx_t<R>;
+  __shared__ T red[256];
   const T *partial = static_cast<const T *>(partial_);
   T *out = static_cast<T *>(out_);
-  const int64_t total = out_size * nbatch;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t b = i / out_size, o = i % out_size;
-    T s;
-    s.x = s.y = 0;
-    for (int c = 0; c < nchunks; ++c) {
-      const T v = partial[(b * nchunks + c) * out_size + o];
-      s.x += v.x;
-      s.y += v.y;
-    }
-    out[b * out_bs + o] = s;
+  const int64_t b = blockIdx.x / out_size, o = blockIdx.x % out_size;
+  T s;
+  s.x = s.y = 0;
+  for (int c = threadIdx.x; c < nchunks; c += 256) {
+    const T v = partial[(b * nchunks + c) * out_size + o];
+    s.x += v.x;
+    s.y += v.y;
   }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      red[threadIdx.x].x += red[threadIdx.x + w].x;
+      red[threadIdx.x].y += red[threadIdx.x + w].y;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[b * out_bs + o] = red[0];
 }
 
 // k per chunk: A and B rows of the chunk fit in 48 KiB of shared memory
@@ -777,7 +833,7 @@ cudaError_t launch_splitk(const StridedGeom &g, const BatchPtrs &p, const DotTab
   const size_t smem = size_t(t.M + t.N) * (kc + 1) * sizeof(cx_t<R>);
   k_splitk_partial<R><<<dim3(nchunks, p.nbatch), 256, smem, stream>>>(g, p, t, kc, nchunks,
                                                                       workspace);
-  k_splitk_sum<R><<<grid_for(g.out_size * p.nbatch, 256), 256, 0, stream>>>(
+  k_splitk_sum<R><<<unsigned(g.out_size * p.nbatch), 256, 0, stream>>>(
       workspace, nchunks, g.out_size, p.nbatch, p.out, p.out_bs);
   return cudaGetLastError();
 }
