@@ -748,6 +748,10 @@ __global__ void __launch_bounds__(256)
   T *partial = static_cast<T *>(partial_) + (int64_t(b) * nchunks + chunk) * g.out_size;
   const int64_t k0 = int64_t(chunk) * kc;
   const int len = int(min(int64_t(kc), g.k_size - k0));
+  // pow2 axes: operand offsets are linear in the bits of k, so
+  // off(k0 + kk) = off(k0) + off(kk) for kk < kc (kc a power of two, k0 aligned)
+  int64_t *ka_tab = reinterpret_cast<int64_t *>(sB + t.N * (kc + 1));
+  int64_t *kb_tab = ka_tab + kc;
   auto koff = [&](int64_t k, int64_t &ka, int64_t &kb) {
     ka = 0;
     kb = 0;
@@ -759,16 +763,17 @@ __global__ void __launch_bounds__(256)
       kb += idx * g.k_sb[i];
     }
   };
+  for (int kk = threadIdx.x; kk < kc; kk += blockDim.x) koff(kk, ka_tab[kk], kb_tab[kk]);
+  int64_t ka0, kb0;
+  koff(k0, ka0, kb0);
+  __syncthreads();
   // stage A[:, chunk] and B[:, chunk]: consecutive threads take consecutive k
   for (int idx = threadIdx.x; idx < (t.M + t.N) * kc; idx += blockDim.x) {
     const int row = idx / kc, kk = idx % kc;
     T v;
     v.x = v.y = 0;
-    if (kk < len) {
-      int64_t ka, kb;
-      koff(k0 + kk, ka, kb);
-      v = row < t.M ? A[t.a_row[row] + ka] : B[t.b_col[row - t.M] + kb];
-    }
+    if (kk < len)
+      v = row < t.M ? A[t.a_row[row] + ka0 + ka_tab[kk]] : B[t.b_col[row - t.M] + kb0 + kb_tab[kk]];
     sA[row * (kc + 1) + kk] = v;  // sB follows sA contiguously
   }
   __syncthreads();
@@ -830,7 +835,7 @@ cudaError_t launch_splitk(const StridedGeom &g, const BatchPtrs &p, const DotTab
                           void *workspace, cudaStream_t stream) {
   const int kc = splitk_kc(t, sizeof(cx_t<R>));
   const int nchunks = splitk_chunks(g, t, sizeof(cx_t<R>));
-  const size_t smem = size_t(t.M + t.N) * (kc + 1) * sizeof(cx_t<R>);
+  const size_t smem = size_t(t.M + t.N) * (kc + 1) * sizeof(cx_t<R>) + 16 * size_t(kc);
   k_splitk_partial<R><<<dim3(nchunks, p.nbatch), 256, smem, stream>>>(g, p, t, kc, nchunks,
                                                                       workspace);
   k_splitk_sum<R><<<unsigned(g.out_size * p.nbatch), 256, 0, stream>>>(

@@ -20,6 +20,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <numeric>
@@ -523,8 +524,13 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
   // bandwidth-bound absorb: one big operand, a small K x N side
   if (single && big >= (int64_t(1) << 12) && small <= 4096 && build_absorb(sp, ldims, rdims)) {
     sp.kern = Kern::Absorb;
-    // K x N >= 64: SIMT math would bound the stream; use the tensor cores
-    if (!exact && sp.tc_ok && sp.ag.kb + sp.ag.nb >= 6) sp.kern = Kern::AbsorbTc;
+    // large K x N: SIMT math would bound the stream; use the tensor cores.
+    // STN_ABSORB_POLICY (experiments only): "simt" never, "tc" from K*N >= 64.
+    static const char *policy = std::getenv("STN_ABSORB_POLICY");
+    int tc_min_bits = 8;
+    if (policy && std::string(policy) == "simt") tc_min_bits = 99;
+    if (policy && std::string(policy) == "tc") tc_min_bits = 6;
+    if (!exact && sp.tc_ok && sp.ag.kb + sp.ag.nb >= tc_min_bits) sp.kern = Kern::AbsorbTc;
     return;
   }
   // long-K reduction to a small output (FAST mode: chunked K order)
