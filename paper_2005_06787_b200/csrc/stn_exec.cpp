@@ -527,7 +527,7 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     // large K x N: SIMT math would bound the stream; use the tensor cores.
     // STN_ABSORB_POLICY (experiments only): "simt" never, "tc" from K*N >= 64.
     static const char *policy = std::getenv("STN_ABSORB_POLICY");
-    int tc_min_bits = 8;
+    int tc_min_bits = 10;
     if (policy && std::string(policy) == "simt") tc_min_bits = 99;
     if (policy && std::string(policy) == "tc") tc_min_bits = 6;
     if (!exact && sp.tc_ok && sp.ag.kb + sp.ag.nb >= tc_min_bits) sp.kern = Kern::AbsorbTc;
