@@ -313,6 +313,13 @@ int stn_selftest_gemm_tc(int64_t M, int64_t N, int64_t K, int32_t batches, int32
                          int32_t b_batched, int32_t reps, double *max_rel_err, double *ms_total,
                          double *ms_gemm, double *ms_simt, double *simt_rel_err);
 
+/* Memory-pipeline check: a 2^log2_elems complex64 tensor is bit-permuted by
+ * the tiled absorb kernel (perm[i] = source bit of output bit i; identity when
+ * NULL) and copied with cudaMemcpyAsync; returns GB/s (read + write) of both
+ * and whether the permutation result is correct. */
+int stn_selftest_bitperm(int32_t log2_elems, const int32_t *perm, int32_t reps, double *gbs_kernel,
+                         double *gbs_memcpy, int32_t *correct);
+
 #ifdef __cplusplus
 }
 #endif

@@ -149,6 +149,9 @@ SIGNATURES = {
     "stn_run_slices_digits": (C.c_int, [_P, _P, C.POINTER(C.c_int32), C.c_uint64, _P, _P, _P]),
     "stn_run_scheme": (C.c_int, [_P, C.c_int, C.POINTER(C.c_double), C.POINTER(RunReport)]),
     "stn_sum_slices_ordered": (C.c_int, [_P, C.c_uint64, C.c_int64, _P, _P]),
+    "stn_selftest_bitperm": (C.c_int, [C.c_int32, C.POINTER(C.c_int32), C.c_int32,
+                                       C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_int32)]),
     "stn_selftest_gemm_tc": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32,
                                        C.c_int32, C.c_int32, C.POINTER(C.c_double),
                                        C.POINTER(C.c_double), C.POINTER(C.c_double),

@@ -1789,4 +1789,62 @@ int stn_selftest_gemm_tc(int64_t M, int64_t N, int64_t K, int32_t batches, int32
   });
 }
 
+int stn_selftest_bitperm(int32_t log2_elems, const int32_t *perm, int32_t reps, double *gbs_kernel,
+                         double *gbs_memcpy, int32_t *correct) {
+  return guarded([&] {
+    require(log2_elems >= 12 && log2_elems <= 31 && reps >= 1, STN_ERR_INVALID_ARGUMENT,
+            "bad size");
+    const int r = log2_elems;
+    // out bit i (position) <- in bit perm[i]; as axes: out axis a = in axis p
+    std::vector<int> dims(r, 2), axis_perm(r);
+    for (int i = 0; i < r; ++i) {
+      const int src_bit = perm ? perm[i] : i;
+      axis_perm[r - 1 - i] = r - 1 - src_bit;
+    }
+    stn::AbsorbGeom g;
+    require(build_bitperm(dims, axis_perm, g), STN_ERR_INVALID_ARGUMENT, "no tile geometry");
+    const size_t n = size_t(1) << r, bytes = n * 8;
+    DevBuf in, out, ref;
+    in.reserve(bytes);
+    out.reserve(bytes);
+    ref.reserve(bytes);
+    std::vector<uint32_t> host(2 * n);
+    for (size_t i = 0; i < n; ++i) host[2 * i] = uint32_t(i), host[2 * i + 1] = uint32_t(~i);
+    cuda_check(cudaMemcpy(in.ptr, host.data(), bytes, cudaMemcpyHostToDevice), "upload");
+    cudaStream_t st = nullptr;
+    cudaEvent_t e0, e1;
+    cuda_check(cudaEventCreate(&e0), "event");
+    cuda_check(cudaEventCreate(&e1), "event");
+    cuda_check(stn::launch_bitperm(g, in.ptr, out.ptr, 0, 0, 1, st), "bitperm");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    std::vector<uint32_t> got(2 * n);
+    cuda_check(cudaMemcpy(got.data(), out.ptr, bytes, cudaMemcpyDeviceToHost), "download");
+    bool ok = true;
+    for (size_t o = 0; o < n && ok; ++o) {
+      size_t src = 0;
+      for (int i = 0; i < r; ++i)
+        if ((o >> i) & 1) src |= size_t(1) << (perm ? perm[i] : i);
+      ok = got[2 * o] == uint32_t(src) && got[2 * o + 1] == uint32_t(~src);
+    }
+    *correct = ok ? 1 : 0;
+    cuda_check(cudaEventRecord(e0, st), "event");
+    for (int i = 0; i < reps; ++i)
+      cuda_check(stn::launch_bitperm(g, in.ptr, out.ptr, 0, 0, 1, st), "bitperm");
+    cuda_check(cudaEventRecord(e1, st), "event");
+    cuda_check(cudaEventSynchronize(e1), "sync");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *gbs_kernel = 2.0 * bytes * reps / (ms / 1e3) / 1e9;
+    cuda_check(cudaEventRecord(e0, st), "event");
+    for (int i = 0; i < reps; ++i)
+      cuda_check(cudaMemcpyAsync(ref.ptr, in.ptr, bytes, cudaMemcpyDeviceToDevice, st), "memcpy");
+    cuda_check(cudaEventRecord(e1, st), "event");
+    cuda_check(cudaEventSynchronize(e1), "sync");
+    cudaEventElapsedTime(&ms, e0, e1);
+    *gbs_memcpy = 2.0 * bytes * reps / (ms / 1e3) / 1e9;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
+}
+
 }  // extern "C"
