@@ -764,6 +764,91 @@ cudaError_t launch_absorb2_dispatch(const AbsorbGeom &g, const BatchPtrs &p, cud
 }
 
 // ---------------------------------------------------------------------------
+// Direct absorb (kernels.h DirectGeom): every thread owns a pair of consecutive
+// m (one 16-byte vector per k and per n) and walks R consecutive m_hi values
+// with pdep increments; W lives in shared memory. Loads and stores of a warp
+// cover 512 contiguous bytes per k / per n; no tiles, no barriers in the loop.
+// ---------------------------------------------------------------------------
+constexpr int kDirThreads = 256;
+constexpr int kDirR = 8;  // m_hi values per thread
+
+__device__ __forceinline__ uint64_t pdep_mask(uint64_t v, uint64_t mask) {
+  uint64_t r = 0;
+  for (uint64_t bit = 1; mask; bit <<= 1) {
+    const uint64_t low = mask & (0 - mask);
+    if (v & bit) r |= low;
+    mask ^= low;
+  }
+  return r;
+}
+
+template <bool EXACT, int K, int N>
+__global__ void __launch_bounds__(kDirThreads)
+    k_absorb_direct(const __grid_constant__ DirectGeom g, const BatchPtrs p) {
+  __shared__ float2 w[N][K];
+  const int b = blockIdx.y;
+  const float2 *X = static_cast<const float2 *>(p.a) + int64_t(b) * p.a_bs;
+  const float2 *Wg = static_cast<const float2 *>(p.b) + int64_t(b) * p.b_bs;
+  float2 *O = static_cast<float2 *>(p.out) + int64_t(b) * p.out_bs;
+  for (int i = threadIdx.x; i < K * N; i += kDirThreads) w[i % N][i / N] = Wg[g.w_off[(i / N) * 16 + (i % N)]];
+  __syncthreads();
+  const int pairs_lo = 1 << (g.L - 1);                     // m pairs per m_hi
+  const int64_t t = int64_t(blockIdx.x) * kDirThreads + threadIdx.x;
+  const int lo = int(t % pairs_lo) * 2;
+  const int64_t hi0 = (t / pairs_lo) * kDirR;
+  const int64_t n_hi = int64_t(1) << g.mh_bits;
+  if (hi0 >= n_hi) return;
+  uint64_t px = pdep_mask(uint64_t(hi0), g.hi_x_mask);
+  uint64_t po = pdep_mask(uint64_t(hi0), g.hi_o_mask);
+  for (int r = 0; r < kDirR && hi0 + r < n_hi; ++r) {
+    const float4 *xs = reinterpret_cast<const float4 *>(X + px + lo);
+    float4 xv[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) xv[k] = __ldcs(xs + g.x_koff[k] / 2);
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const float2 wk = w[n][k];
+        cmac<EXACT>(a0, make_float2(xv[k].x, xv[k].y), wk);
+        cmac<EXACT>(a1, make_float2(xv[k].z, xv[k].w), wk);
+      }
+      __stcs(reinterpret_cast<float4 *>(O + po + lo + g.o_noff[n]),
+             make_float4(a0.x, a0.y, a1.x, a1.y));
+    }
+    // next subset of the high-bit masks (pdep(v + 1) from pdep(v))
+    px = ((px | ~g.hi_x_mask) + 1) & g.hi_x_mask;
+    po = ((po | ~g.hi_o_mask) + 1) & g.hi_o_mask;
+  }
+}
+
+bool direct_ok_impl(const DirectGeom &g) { return g.L >= 2 && g.kb <= 4 && g.nb <= 4; }
+
+template <bool EXACT>
+cudaError_t launch_direct_exact(const DirectGeom &g, const BatchPtrs &p, cudaStream_t st) {
+  const int64_t threads = (int64_t(1) << (g.L - 1)) *
+                          (((int64_t(1) << g.mh_bits) + kDirR - 1) / kDirR);
+  dim3 grid(unsigned((threads + kDirThreads - 1) / kDirThreads), unsigned(p.nbatch));
+#define STN_DIR(KV, NV)                                                        \
+  if ((1 << g.kb) == KV && (1 << g.nb) == NV) {                                \
+    k_absorb_direct<EXACT, KV, NV><<<grid, kDirThreads, 0, st>>>(g, p);       \
+    return cudaGetLastError();                                                 \
+  }
+#define STN_DIR_ROW(KV) STN_DIR(KV, 1) STN_DIR(KV, 2) STN_DIR(KV, 4) STN_DIR(KV, 8) STN_DIR(KV, 16)
+  STN_DIR_ROW(1) STN_DIR_ROW(2) STN_DIR_ROW(4) STN_DIR_ROW(8) STN_DIR_ROW(16)
+#undef STN_DIR_ROW
+#undef STN_DIR
+  return cudaErrorNotSupported;
+}
+
+cudaError_t launch_direct_impl(const DirectGeom &g, const BatchPtrs &p, bool exact,
+                               cudaStream_t stream) {
+  if (!direct_ok_impl(g)) return cudaErrorNotSupported;
+  return exact ? launch_direct_exact<true>(g, p, stream) : launch_direct_exact<false>(g, p, stream);
+}
+
+// ---------------------------------------------------------------------------
 // Tiled SIMT complex GEMM, C[d] = A[d] (MxK, row-major) * B[d] (KxN, row-major).
 // 64x64 output tile per CTA, 16-wide K steps, 4x4 outputs per thread; every
 // output accumulates k in ascending order.
@@ -899,6 +984,13 @@ bool all_pow2(const StridedGeom &g) {
 }
 
 }  // namespace
+
+bool direct_absorb_launchable(const DirectGeom &g) { return direct_ok_impl(g); }
+
+cudaError_t launch_absorb_direct(const DirectGeom &g, const BatchPtrs &p, bool exact,
+                                 cudaStream_t stream) {
+  return launch_direct_impl(g, p, exact, stream);
+}
 
 template <class R>
 cudaError_t launch_generic(const StridedGeom &g, const BatchPtrs &p, bool exact,

@@ -70,6 +70,24 @@ struct AbsorbGeom {
   uint8_t outer_o[34];               // O position of outer M bit j
 };
 
+// "Direct" bond-2 absorb: no shared-memory tile. Valid when the lowest L bits
+// of X are M bits that are also the lowest L bits of O (same order), so a warp
+// streams 16-byte pairs of consecutive m straight from X to O for every k / n.
+// M index m = m_hi << L | m_lo; the high M bits scatter to positions given by
+// the bit masks hi_x (in X) and hi_o (in O), enumerated with pdep increments.
+struct DirectGeom {
+  int L;                     // identity low bits (>= 2)
+  int kb, nb;                // K and N bits (<= 4 each)
+  int mh_bits;               // high M bits
+  uint64_t hi_x_mask, hi_o_mask;
+  int64_t x_koff[16];        // X offset of k (k < 2^kb)
+  int64_t o_noff[16];        // O offset of n
+  int64_t w_off[16 * 16];    // W offset of (k, n): k * 16 + n
+};
+bool direct_absorb_launchable(const DirectGeom &g);
+cudaError_t launch_absorb_direct(const DirectGeom &g, const BatchPtrs &p, bool exact,
+                                 cudaStream_t stream);
+
 // Dense batched complex GEMM on materialised operands:
 //   C[d] (M x N) = A[d] (M x K, row-major) * B[d] (K x N, row-major)
 struct GemmShape {

@@ -107,7 +107,7 @@ struct DevBuf {
 // ---------------------------------------------------------------------------
 // plan model
 // ---------------------------------------------------------------------------
-enum class Kern { Generic, Absorb, AbsorbTc, SplitK, GemmSimt, GemmTc };
+enum class Kern { Generic, Absorb, AbsorbTc, AbsorbDirect, SplitK, GemmSimt, GemmTc };
 
 struct Node {
   bool is_leaf = false;
@@ -128,6 +128,8 @@ struct StepPlan {
   stn::AbsorbGeom ag{};
   stn::AbsorbGeom agtc{};  // 128-row tiles for the tensor-core absorb
   bool tc_ok = false;
+  stn::DirectGeom dg{};     // tile-free variant (identity low bits)
+  bool direct_ok = false;
   bool x_is_lhs = true;
   // gemm path
   bool a_id = true, b_id = true, c_id = true;
@@ -465,8 +467,45 @@ bool build_absorb(StepPlan &sp, const std::vector<int> &ldims, const std::vector
   for (size_t j = 1; j < nbits.size(); ++j)
     if (nbits[j].second < nbits[j - 1].second) return false;
 
+  sp.x_is_lhs = x_lhs;
+  // tile-free geometry: the lowest L bits of X are M bits at the same O positions
+  {
+    std::map<int, int> o_of_x;
+    for (auto &[xp, op] : mbits) o_of_x[xp] = op;
+    int L = 0;
+    while (o_of_x.count(L) && o_of_x[L] == L) ++L;
+    stn::DirectGeom &dg = sp.dg;
+    memset(&dg, 0, sizeof dg);
+    dg.L = L;
+    dg.kb = kb;
+    dg.nb = nb;
+    dg.mh_bits = mb - L;
+    for (auto &[xp, op] : mbits)
+      if (xp >= L) {
+        dg.hi_x_mask |= uint64_t(1) << xp;
+        dg.hi_o_mask |= uint64_t(1) << op;
+      }
+    if (kb <= 4 && nb <= 4) {
+      for (int k = 0; k < (1 << kb); ++k)
+        for (int j = 0; j < kb; ++j)
+          if ((k >> j) & 1) dg.x_koff[k] += int64_t(1) << kbits[j].first;
+      for (int n = 0; n < (1 << nb); ++n)
+        for (int j = 0; j < nb; ++j)
+          if ((n >> j) & 1) dg.o_noff[n] += int64_t(1) << nbits[j].first;
+      for (int k = 0; k < (1 << kb); ++k)
+        for (int n = 0; n < (1 << nb); ++n) {
+          int64_t off = 0;
+          for (int j = 0; j < kb; ++j)
+            if ((k >> j) & 1) off += int64_t(1) << kbits[j].second;
+          for (int j = 0; j < nb; ++j)
+            if ((n >> j) & 1) off += int64_t(1) << nbits[j].second;
+          dg.w_off[k * 16 + n] = off;
+        }
+    }
+    sp.direct_ok = L >= 2 && stn::direct_absorb_launchable(dg) && dg.mh_bits <= 40;
+  }
   stn::AbsorbGeom g;
-  if (!make_tile_geom(kbits, mbits, nbits, xr, orank, g)) return false;
+  if (!make_tile_geom(kbits, mbits, nbits, xr, orank, g)) return sp.direct_ok;
   g.w_is_lhs = x_lhs ? 0 : 1;
   sp.ag = g;
   sp.x_is_lhs = x_lhs;
@@ -524,6 +563,18 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
   // bandwidth-bound absorb: one big operand, a small K x N side
   if (single && big >= (int64_t(1) << 12) && small <= 4096 && build_absorb(sp, ldims, rdims)) {
     sp.kern = Kern::Absorb;
+    // tile-free streaming when the low bits line up (K x N <= 2^STN_DIRECT_MAX_BITS)
+    static const char *dmax = std::getenv("STN_DIRECT_MAX_BITS");
+    const int direct_max = dmax ? std::atoi(dmax) : 6;
+    const int direct_min_L = 4;
+    if (sp.direct_ok && sp.dg.L >= direct_min_L && sp.dg.kb + sp.dg.nb <= direct_max) {
+      sp.kern = Kern::AbsorbDirect;
+      return;
+    }
+    if (!sp.tc_ok && sp.ag.xt_bits == 0) {  // no tile geometry: direct or generic
+      sp.kern = sp.direct_ok ? Kern::AbsorbDirect : Kern::Generic;
+      return;
+    }
     // large K x N: SIMT math would bound the stream; use the tensor cores.
     // STN_ABSORB_POLICY (experiments only): "simt" never, "tc" from K*N >= 64.
     static const char *policy = std::getenv("STN_ABSORB_POLICY");
@@ -1217,6 +1268,14 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
       prof.done(STN_KERNEL_ABSORB_TC, io_bytes, flops);
       break;
     }
+    case Kern::AbsorbDirect: {
+      const Resolved &x = sp.x_is_lhs ? a : b;
+      const Resolved &w = sp.x_is_lhs ? b : a;
+      stn::BatchPtrs p{x.ptr, w.ptr, out, x.bs, w.bs, o.bs, nb};
+      cuda_check(stn::launch_absorb_direct(sp.dg, p, exact, st), "direct absorb kernel");
+      prof.done(STN_KERNEL_ABSORB, io_bytes, flops);
+      break;
+    }
     case Kern::Absorb: {
       const Resolved &x = sp.x_is_lhs ? a : b;
       const Resolved &w = sp.x_is_lhs ? b : a;
@@ -1486,7 +1545,8 @@ int stn_plan_get_info(const stn_plan *P, stn_plan_info *info) {
     Kern k = P->steps[op.step].kern;
     if (k == Kern::GemmTc) info->steps_tensor_core++;
     else if (k == Kern::GemmSimt) info->steps_generic++;
-    else if (k == Kern::Absorb || k == Kern::AbsorbTc) info->steps_absorb++;
+    else if (k == Kern::Absorb || k == Kern::AbsorbTc || k == Kern::AbsorbDirect)
+      info->steps_absorb++;
     else info->steps_generic++;
   }
   return STN_OK;
