@@ -782,17 +782,27 @@ __device__ __forceinline__ uint64_t pdep_mask(uint64_t v, uint64_t mask) {
   return r;
 }
 
-template <bool EXACT, int K, int N>
+// KC / NC: K and N chunks held in registers; K and N are runtime multiples.
+template <bool EXACT, int KC, int NC>
 __global__ void __launch_bounds__(kDirThreads)
     k_absorb_direct(const __grid_constant__ DirectGeom g, const BatchPtrs p) {
-  __shared__ float2 w[N][K];
+  extern __shared__ __align__(16) float2 wsm[];  // [N][K]
+  const int K = 1 << g.kb, N = 1 << g.nb;
   const int b = blockIdx.y;
   const float2 *X = static_cast<const float2 *>(p.a) + int64_t(b) * p.a_bs;
   const float2 *Wg = static_cast<const float2 *>(p.b) + int64_t(b) * p.b_bs;
   float2 *O = static_cast<float2 *>(p.out) + int64_t(b) * p.out_bs;
-  for (int i = threadIdx.x; i < K * N; i += kDirThreads) w[i % N][i / N] = Wg[g.w_off[(i / N) * 16 + (i % N)]];
+  for (int i = threadIdx.x; i < K * N; i += kDirThreads) {
+    const int n = i / K, k = i % K;
+    int64_t off = 0;
+    for (int j = 0; j < g.kb; ++j)
+      if ((k >> j) & 1) off += g.w_k_stride[j];
+    for (int j = 0; j < g.nb; ++j)
+      if ((n >> j) & 1) off += g.w_n_stride[j];
+    wsm[i] = Wg[off];
+  }
   __syncthreads();
-  const int pairs_lo = 1 << (g.L - 1);                     // m pairs per m_hi
+  const int pairs_lo = 1 << (g.L - 1);  // m pairs per m_hi
   const int64_t t = int64_t(blockIdx.x) * kDirThreads + threadIdx.x;
   const int lo = int(t % pairs_lo) * 2;
   const int64_t hi0 = (t / pairs_lo) * kDirR;
@@ -802,20 +812,29 @@ __global__ void __launch_bounds__(kDirThreads)
   uint64_t po = pdep_mask(uint64_t(hi0), g.hi_o_mask);
   for (int r = 0; r < kDirR && hi0 + r < n_hi; ++r) {
     const float4 *xs = reinterpret_cast<const float4 *>(X + px + lo);
-    float4 xv[K];
+    for (int n0 = 0; n0 < N; n0 += NC) {
+      float2 a0[NC], a1[NC];
 #pragma unroll
-    for (int k = 0; k < K; ++k) xv[k] = __ldcs(xs + g.x_koff[k] / 2);
+      for (int c = 0; c < NC; ++c) a0[c] = a1[c] = make_float2(0.f, 0.f);
+      for (int k0 = 0; k0 < K; k0 += KC) {
+        float4 xv[KC];
 #pragma unroll
-    for (int n = 0; n < N; ++n) {
-      float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+        for (int k = 0; k < KC; ++k) xv[k] = __ldcs(xs + g.x_koff[k0 + k] / 2);
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const float2 wk = w[n][k];
-        cmac<EXACT>(a0, make_float2(xv[k].x, xv[k].y), wk);
-        cmac<EXACT>(a1, make_float2(xv[k].z, xv[k].w), wk);
+        for (int c = 0; c < NC; ++c) {
+          const float2 *wr = wsm + (n0 + c) * K + k0;
+#pragma unroll
+          for (int k = 0; k < KC; ++k) {
+            const float2 wk = wr[k];
+            cmac<EXACT>(a0[c], make_float2(xv[k].x, xv[k].y), wk);
+            cmac<EXACT>(a1[c], make_float2(xv[k].z, xv[k].w), wk);
+          }
+        }
       }
-      __stcs(reinterpret_cast<float4 *>(O + po + lo + g.o_noff[n]),
-             make_float4(a0.x, a0.y, a1.x, a1.y));
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        __stcs(reinterpret_cast<float4 *>(O + po + lo + g.o_noff[n0 + c]),
+               make_float4(a0[c].x, a0[c].y, a1[c].x, a1[c].y));
     }
     // next subset of the high-bit masks (pdep(v + 1) from pdep(v))
     px = ((px | ~g.hi_x_mask) + 1) & g.hi_x_mask;
@@ -823,17 +842,22 @@ __global__ void __launch_bounds__(kDirThreads)
   }
 }
 
-bool direct_ok_impl(const DirectGeom &g) { return g.L >= 2 && g.kb <= 4 && g.nb <= 4; }
+bool direct_ok_impl(const DirectGeom &g) { return g.L >= 2 && g.kb <= 6 && g.nb <= 6; }
 
 template <bool EXACT>
 cudaError_t launch_direct_exact(const DirectGeom &g, const BatchPtrs &p, cudaStream_t st) {
   const int64_t threads = (int64_t(1) << (g.L - 1)) *
                           (((int64_t(1) << g.mh_bits) + kDirR - 1) / kDirR);
   dim3 grid(unsigned((threads + kDirThreads - 1) / kDirThreads), unsigned(p.nbatch));
-#define STN_DIR(KV, NV)                                                        \
-  if ((1 << g.kb) == KV && (1 << g.nb) == NV) {                                \
-    k_absorb_direct<EXACT, KV, NV><<<grid, kDirThreads, 0, st>>>(g, p);       \
-    return cudaGetLastError();                                                 \
+  const size_t smem = size_t(8) << (g.kb + g.nb);
+  const int kc = g.kb >= 4 ? 16 : (1 << g.kb), nc = g.nb >= 4 ? 16 : (1 << g.nb);
+#define STN_DIR(KV, NV)                                                          \
+  if (kc == KV && nc == NV) {                                                    \
+    if (smem > 48 * 1024)                                                        \
+      cudaFuncSetAttribute(k_absorb_direct<EXACT, KV, NV>,                      \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
+    k_absorb_direct<EXACT, KV, NV><<<grid, kDirThreads, smem, st>>>(g, p);      \
+    return cudaGetLastError();                                                   \
   }
 #define STN_DIR_ROW(KV) STN_DIR(KV, 1) STN_DIR(KV, 2) STN_DIR(KV, 4) STN_DIR(KV, 8) STN_DIR(KV, 16)
   STN_DIR_ROW(1) STN_DIR_ROW(2) STN_DIR_ROW(4) STN_DIR_ROW(8) STN_DIR_ROW(16)

@@ -77,12 +77,13 @@ struct AbsorbGeom {
 // the bit masks hi_x (in X) and hi_o (in O), enumerated with pdep increments.
 struct DirectGeom {
   int L;                     // identity low bits (>= 2)
-  int kb, nb;                // K and N bits (<= 4 each)
+  int kb, nb;                // K and N bits (<= 6 each)
   int mh_bits;               // high M bits
   uint64_t hi_x_mask, hi_o_mask;
-  int64_t x_koff[16];        // X offset of k (k < 2^kb)
-  int64_t o_noff[16];        // O offset of n
-  int64_t w_off[16 * 16];    // W offset of (k, n): k * 16 + n
+  int64_t x_koff[64];        // X offset of k (k < 2^kb)
+  int64_t o_noff[64];        // O offset of n
+  int64_t w_k_stride[6];     // W stride of K bit j
+  int64_t w_n_stride[6];     // W stride of N bit j
 };
 bool direct_absorb_launchable(const DirectGeom &g);
 cudaError_t launch_absorb_direct(const DirectGeom &g, const BatchPtrs &p, bool exact,

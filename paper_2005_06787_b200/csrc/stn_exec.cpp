@@ -485,22 +485,15 @@ bool build_absorb(StepPlan &sp, const std::vector<int> &ldims, const std::vector
         dg.hi_x_mask |= uint64_t(1) << xp;
         dg.hi_o_mask |= uint64_t(1) << op;
       }
-    if (kb <= 4 && nb <= 4) {
+    if (kb <= 6 && nb <= 6) {
       for (int k = 0; k < (1 << kb); ++k)
         for (int j = 0; j < kb; ++j)
           if ((k >> j) & 1) dg.x_koff[k] += int64_t(1) << kbits[j].first;
       for (int n = 0; n < (1 << nb); ++n)
         for (int j = 0; j < nb; ++j)
           if ((n >> j) & 1) dg.o_noff[n] += int64_t(1) << nbits[j].first;
-      for (int k = 0; k < (1 << kb); ++k)
-        for (int n = 0; n < (1 << nb); ++n) {
-          int64_t off = 0;
-          for (int j = 0; j < kb; ++j)
-            if ((k >> j) & 1) off += int64_t(1) << kbits[j].second;
-          for (int j = 0; j < nb; ++j)
-            if ((n >> j) & 1) off += int64_t(1) << nbits[j].second;
-          dg.w_off[k * 16 + n] = off;
-        }
+      for (int j = 0; j < kb; ++j) dg.w_k_stride[j] = int64_t(1) << kbits[j].second;
+      for (int j = 0; j < nb; ++j) dg.w_n_stride[j] = int64_t(1) << nbits[j].second;
     }
     sp.direct_ok = L >= 2 && stn::direct_absorb_launchable(dg) && dg.mh_bits <= 40;
   }
@@ -565,7 +558,7 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     sp.kern = Kern::Absorb;
     // tile-free streaming when the low bits line up (K x N <= 2^STN_DIRECT_MAX_BITS)
     static const char *dmax = std::getenv("STN_DIRECT_MAX_BITS");
-    const int direct_max = dmax ? std::atoi(dmax) : 6;
+    const int direct_max = dmax ? std::atoi(dmax) : 12;
     const int direct_min_L = 4;
     if (sp.direct_ok && sp.dg.L >= direct_min_L && sp.dg.kb + sp.dg.nb <= direct_max) {
       sp.kern = Kern::AbsorbDirect;
