@@ -77,13 +77,13 @@ struct AbsorbGeom {
 // the bit masks hi_x (in X) and hi_o (in O), enumerated with pdep increments.
 struct DirectGeom {
   int L;                     // identity low bits (>= 2)
-  int kb, nb;                // K and N bits (<= 6 each)
+  int kb, nb;                // K bits (<= 6), N bits (<= 12), K*N <= 4096
   int mh_bits;               // high M bits
   uint64_t hi_x_mask, hi_o_mask;
-  int64_t x_koff[64];        // X offset of k (k < 2^kb)
-  int64_t o_noff[64];        // O offset of n
+  uint8_t k_xpos[6];         // X position of K bit j (ascending)
+  uint8_t n_opos[12];        // O position of N bit j (ascending)
   int64_t w_k_stride[6];     // W stride of K bit j
-  int64_t w_n_stride[6];     // W stride of N bit j
+  int64_t w_n_stride[12];    // W stride of N bit j
 };
 bool direct_absorb_launchable(const DirectGeom &g);
 cudaError_t launch_absorb_direct(const DirectGeom &g, const BatchPtrs &p, bool exact,

@@ -429,7 +429,7 @@ bool build_absorb(StepPlan &sp, const std::vector<int> &ldims, const std::vector
   const int kb = d.nk;
   const int nb = wr - kb;  // W-side free bits
   const int mb = xr - kb;
-  if (kb > stn::kAbsorbMaxKN || nb > stn::kAbsorbMaxKN || xr < 12) return false;
+  if (kb > stn::kAbsorbMaxKN || nb > 12 || xr < 12) return false;
   // K bits: (x position, w position)
   std::vector<std::pair<int, int>> kbits;
   for (int q = 0; q < d.nk; ++q) {
@@ -485,18 +485,19 @@ bool build_absorb(StepPlan &sp, const std::vector<int> &ldims, const std::vector
         dg.hi_x_mask |= uint64_t(1) << xp;
         dg.hi_o_mask |= uint64_t(1) << op;
       }
-    if (kb <= 6 && nb <= 6) {
-      for (int k = 0; k < (1 << kb); ++k)
-        for (int j = 0; j < kb; ++j)
-          if ((k >> j) & 1) dg.x_koff[k] += int64_t(1) << kbits[j].first;
-      for (int n = 0; n < (1 << nb); ++n)
-        for (int j = 0; j < nb; ++j)
-          if ((n >> j) & 1) dg.o_noff[n] += int64_t(1) << nbits[j].first;
-      for (int j = 0; j < kb; ++j) dg.w_k_stride[j] = int64_t(1) << kbits[j].second;
-      for (int j = 0; j < nb; ++j) dg.w_n_stride[j] = int64_t(1) << nbits[j].second;
+    if (kb <= 6 && nb <= 12) {
+      for (int j = 0; j < kb; ++j) {
+        dg.k_xpos[j] = uint8_t(kbits[j].first);
+        dg.w_k_stride[j] = int64_t(1) << kbits[j].second;
+      }
+      for (int j = 0; j < nb; ++j) {
+        dg.n_opos[j] = uint8_t(nbits[j].first);
+        dg.w_n_stride[j] = int64_t(1) << nbits[j].second;
+      }
     }
     sp.direct_ok = L >= 2 && stn::direct_absorb_launchable(dg) && dg.mh_bits <= 40;
   }
+  if (nb > stn::kAbsorbMaxKN) return sp.direct_ok;  // tiled kernels: N <= 64
   stn::AbsorbGeom g;
   if (!make_tile_geom(kbits, mbits, nbits, xr, orank, g)) return sp.direct_ok;
   g.w_is_lhs = x_lhs ? 0 : 1;
