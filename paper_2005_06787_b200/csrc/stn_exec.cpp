@@ -560,7 +560,8 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     // tile-free streaming when the low bits line up (K x N <= 2^STN_DIRECT_MAX_BITS)
     static const char *dmax = std::getenv("STN_DIRECT_MAX_BITS");
     const int direct_max = dmax ? std::atoi(dmax) : 12;
-    const int direct_min_L = 4;
+    static const char *dminl = std::getenv("STN_DIRECT_MIN_L");
+    const int direct_min_L = dminl ? std::atoi(dminl) : 4;
     if (sp.direct_ok && sp.dg.L >= direct_min_L && sp.dg.kb + sp.dg.nb <= direct_max) {
       sp.kern = Kern::AbsorbDirect;
       return;
