@@ -561,7 +561,7 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     static const char *dmax = std::getenv("STN_DIRECT_MAX_BITS");
     const int direct_max = dmax ? std::atoi(dmax) : 12;
     static const char *dminl = std::getenv("STN_DIRECT_MIN_L");
-    const int direct_min_L = dminl ? std::atoi(dminl) : 4;
+    const int direct_min_L = dminl ? std::atoi(dminl) : 2;
     if (sp.direct_ok && sp.dg.L >= direct_min_L && sp.dg.kb + sp.dg.nb <= direct_max) {
       sp.kern = Kern::AbsorbDirect;
       return;
