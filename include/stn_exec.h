@@ -182,6 +182,8 @@ typedef struct stn_plan_info {
   int32_t steps_tensor_core;     /* per-slice steps on the tcgen05 GEMM */
   int32_t steps_absorb;          /* per-slice steps on the bandwidth absorb kernel */
   int32_t steps_generic;         /* per-slice steps on the generic SIMT kernel */
+  int32_t sweeps;                /* fused stem sweeps in the per-slice program */
+  int32_t steps_in_sweeps;       /* per-slice steps executed inside sweeps */
 } stn_plan_info;
 
 /* Per-kernel-class timing of the launches made while profiling is on (CUDA
@@ -198,7 +200,8 @@ typedef enum stn_kernel_kind {
   STN_KERNEL_LEAF = 5,      /* per-slice leaf gather */
   STN_KERNEL_ROOT = 6,      /* ordered fp64 root accumulation */
   STN_KERNEL_ABSORB_TC = 7, /* tcgen05 split-TF32 absorb (K x N >= 64) */
-  STN_KERNEL_KINDS = 8
+  STN_KERNEL_SWEEP = 8,     /* fused chain of stem absorbs (one HBM pass) */
+  STN_KERNEL_KINDS = 9
 } stn_kernel_kind;
 
 typedef struct stn_kernel_profile {

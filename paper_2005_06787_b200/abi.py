@@ -97,12 +97,12 @@ class PlanInfo(C.Structure):
         ("branch_mults", C.c_uint64), ("peak_elements", C.c_uint64),
         ("arena_bytes_per_slice", C.c_uint64), ("cache_bytes", C.c_uint64),
         ("steps_tensor_core", C.c_int32), ("steps_absorb", C.c_int32),
-        ("steps_generic", C.c_int32),
+        ("steps_generic", C.c_int32), ("sweeps", C.c_int32), ("steps_in_sweeps", C.c_int32),
     ]
 
 
 KERNEL_KINDS = ["generic", "absorb", "gemm_simt", "gemm_tc", "permute", "leaf", "root",
-                "absorb_tc"]
+                "absorb_tc", "sweep"]
 
 
 class KernelProfile(C.Structure):

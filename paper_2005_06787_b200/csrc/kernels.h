@@ -89,6 +89,39 @@ bool direct_absorb_launchable(const DirectGeom &g);
 cudaError_t launch_absorb_direct(const DirectGeom &g, const BatchPtrs &p, bool exact,
                                  cudaStream_t stream);
 
+// Fused stem sweep: a chain of consecutive bond-2 absorbs S_{j+1} = S_j x W_j
+// executed tile by tile in shared memory. Only S_0 is read from and S_r written
+// to HBM; the intermediate stems never exist in memory. Every stage sums its K
+// terms in ascending k exactly like the single-step kernels, so a sweep is
+// bitwise identical to running its steps one by one.
+constexpr int kSweepMaxStages = 24;
+constexpr int kSweepMaxTileBits = 12;
+struct SweepStage {
+  int in_bits, out_bits;  // tile bits before / after the stage
+  int kb, nb;             // K and N bits of the stage
+  int nc_log;             // outputs per thread along N (register tile), log2
+  int rb_log;             // M indices per thread (register tile), log2; rb+nc <= 5
+  const uint16_t *rb;     // [2^(out_bits-nb)] input tile offset of M index r
+  const uint16_t *ro;     // [2^(out_bits-nb)] output tile offset of M index r
+  const uint16_t *koff;   // [2^kb] input tile offset of k
+  const uint16_t *nofs;   // [2^nb] output tile offset of n
+  const int64_t *w_idx;   // [K*N] W element offset of (k, n), k-major
+  int w_smem;             // offset of this stage's W^T in the smem W area (elements)
+  int t_smem;             // offset of this stage's koff/nofs in the smem table area
+};
+struct SweepGeom {
+  AbsorbGeom io;            // input tile (x_*) / output tile (o_*) / outer bits; kb = nb = 0
+  int n_stages;
+  int max_bits;             // largest tile over all stages
+  int w_total;              // W elements of all stages
+  int t_total;              // koff + nofs entries of all stages
+  SweepStage st[kSweepMaxStages];
+  const void *w[kSweepMaxStages];  // per-launch W pointers
+  int64_t w_bs[kSweepMaxStages];   // and batch strides
+};
+cudaError_t launch_sweep(const SweepGeom &g, const BatchPtrs &p, bool exact, cudaStream_t stream);
+size_t sweep_smem_bytes(const SweepGeom &g);  // dynamic shared memory of one CTA
+
 // Dense batched complex GEMM on materialised operands:
 //   C[d] (M x N) = A[d] (M x K, row-major) * B[d] (K x N, row-major)
 struct GemmShape {

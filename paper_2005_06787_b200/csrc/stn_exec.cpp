@@ -21,9 +21,11 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <functional>
 #include <map>
 #include <memory>
 #include <numeric>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -130,6 +132,10 @@ struct StepPlan {
   bool tc_ok = false;
   stn::DirectGeom dg{};     // tile-free variant (identity low bits)
   bool direct_ok = false;
+  // absorb bit geometry (positions in X / W / O), kept for stem-sweep fusion
+  bool has_bits = false;
+  int xr = 0, wr = 0, orank_ = 0;
+  std::vector<std::pair<int, int>> kbits, mbits, nbits;  // (x,w), (x,o), (o,w)
   bool x_is_lhs = true;
   // gemm path
   bool a_id = true, b_id = true, c_id = true;
@@ -154,12 +160,15 @@ struct Ref {
 
 struct Op {
   int step = -1;
+  int sweep = -1;          // >= 0: fused stem sweep over several steps
+  std::vector<Ref> wrefs;  // sweep: W operand of every stage
   Ref a, b, out;
   int64_t scr_a = -1, scr_b = -1, scr_c = -1;  // arena scratch offsets (gemm path)
 };
 
 struct Program {
   std::vector<Op> ops;
+  int n_steps = 0;  // plan steps covered (a sweep op covers several)
   int64_t arena_elems = 0;  // per slice
   std::vector<int> slice_leaves;           // leaf node ids gathered per slice
   std::map<int, int64_t> slice_leaf_off;   // node -> arena offset
@@ -209,6 +218,15 @@ struct stn_plan {
   // sliced leaves: double values, concatenated
   std::map<int, int64_t> sliced_val_off;  // leaf node -> complex offset into sliced_vals
   DevBuf sliced_vals;
+  // fused stem sweeps (chains of skinny absorbs)
+  struct Sweep {
+    std::vector<int> steps;
+    stn::SweepGeom geom{};
+    std::shared_ptr<DevBuf> tables;
+    double io_bytes = 0;  // S_0 + S_r + W's per slice, in elements
+  };
+  std::vector<Sweep> sweeps;
+  std::map<int, int> sweep_of_step;
   // programs
   Program build, with_cache, no_cache;
   std::map<int, int64_t> cache_off;  // node -> element offset in cache storage
@@ -468,6 +486,13 @@ bool build_absorb(StepPlan &sp, const std::vector<int> &ldims, const std::vector
     if (nbits[j].second < nbits[j - 1].second) return false;
 
   sp.x_is_lhs = x_lhs;
+  sp.has_bits = true;
+  sp.xr = xr;
+  sp.wr = wr;
+  sp.orank_ = orank;
+  sp.kbits = kbits;
+  sp.mbits = mbits;
+  sp.nbits = nbits;
   // tile-free geometry: the lowest L bits of X are M bits at the same O positions
   {
     std::map<int, int> o_of_x;
@@ -658,6 +683,287 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Stem sweeps: fuse chains of consecutive skinny absorbs (kernels.h SweepGeom)
+// ---------------------------------------------------------------------------
+bool sweep_candidate(const stn_plan &P, const StepPlan &sp) {
+  return P.precision == STN_SINGLE && !sp.d.is_branch && sp.has_bits &&
+         (sp.kern == Kern::Absorb || sp.kern == Kern::AbsorbDirect || sp.kern == Kern::AbsorbTc) &&
+         sp.kbits.size() <= 6 && sp.nbits.size() <= 6;
+}
+
+// Tile-buffer swizzle of kernels_sweep.cu (linear over GF(2)).
+int sweep_phys(int l) { return l ^ (((l >> 4) ^ (l >> 8)) & 15); }
+
+// Builds the sweep geometry of chain steps [steps]; false if a tile does not fit.
+bool build_sweep(const stn_plan &P, const std::vector<int> &steps, int max_bits,
+                 stn_plan::Sweep *out) {
+  if (steps.size() < 2 || int(steps.size()) > stn::kSweepMaxStages) return false;
+  // labels by position, stage by stage
+  std::vector<std::vector<int>> lab;  // lab[j][pos] for S_j
+  const StepPlan &s0 = P.steps[steps[0]];
+  std::vector<int> cur(s0.xr);
+  for (int i = 0; i < s0.xr; ++i) cur[i] = i;
+  int next_label = s0.xr;
+  lab.push_back(cur);
+  std::vector<std::vector<int>> klab(steps.size()), nlab(steps.size());
+  std::set<int> touched;
+  for (size_t j = 0; j < steps.size(); ++j) {
+    const StepPlan &sp = P.steps[steps[j]];
+    if (int(cur.size()) != sp.xr) return false;
+    std::vector<int> nx(sp.orank_, -1);
+    for (auto &[xp, wp] : sp.kbits) {
+      klab[j].push_back(cur[xp]);
+      touched.insert(cur[xp]);
+    }
+    for (auto &[xp, op] : sp.mbits) nx[op] = cur[xp];
+    for (auto &[op, wp] : sp.nbits) {
+      nx[op] = next_label;
+      nlab[j].push_back(next_label);
+      touched.insert(next_label++);
+    }
+    for (int x : nx)
+      if (x < 0) return false;
+    cur = nx;
+    lab.push_back(cur);
+  }
+  std::set<int> keep = touched;  // + the lowest positions of S_0 and S_r (coalescing)
+  for (int pos = 0; pos < 5; ++pos) {
+    if (pos < int(lab.front().size())) keep.insert(lab.front()[pos]);
+    if (pos < int(lab.back().size())) keep.insert(lab.back()[pos]);
+  }
+  // tile label lists per stage, in ascending position of that stage's tensor
+  std::vector<std::vector<int>> tile(lab.size());
+  int maxb = 0;
+  for (size_t j = 0; j < lab.size(); ++j) {
+    for (int pos = 0; pos < int(lab[j].size()); ++pos)
+      if (keep.count(lab[j][pos])) tile[j].push_back(lab[j][pos]);
+    maxb = std::max(maxb, int(tile[j].size()));
+  }
+  if (maxb > max_bits || maxb > stn::kSweepMaxTileBits) return false;
+  // outer (pass-through) labels: in S_0 and S_r at their positions
+  std::map<int, int> pos_first, pos_last;
+  for (int pos = 0; pos < int(lab.front().size()); ++pos) pos_first[lab.front()[pos]] = pos;
+  for (int pos = 0; pos < int(lab.back().size()); ++pos) pos_last[lab.back()[pos]] = pos;
+  stn::SweepGeom g;
+  memset(&g, 0, sizeof g);
+  stn::AbsorbGeom &io = g.io;
+  io.x_bits = int(lab.front().size());
+  io.o_bits = int(lab.back().size());
+  io.xt_bits = int(tile.front().size());
+  io.ot_bits = int(tile.back().size());
+  for (int i = 0; i < io.xt_bits; ++i) io.x_tile_pos[i] = uint8_t(pos_first.at(tile.front()[i]));
+  for (int i = 0; i < io.ot_bits; ++i) io.o_tile_pos[i] = uint8_t(pos_last.at(tile.back()[i]));
+  int ob = 0;
+  for (int pos = 0; pos < int(lab.front().size()); ++pos) {
+    const int l = lab.front()[pos];
+    if (keep.count(l)) continue;
+    if (!pos_last.count(l) || ob >= 34) return false;
+    io.outer_x[ob] = uint8_t(pos);
+    io.outer_o[ob] = uint8_t(pos_last.at(l));
+    ob++;
+  }
+  io.ob = ob;
+  if (ob > 31) return false;
+  while (io.x_run < io.xt_bits && io.x_tile_pos[io.x_run] == io.x_run) io.x_run++;
+  while (io.o_run < io.ot_bits && io.o_tile_pos[io.o_run] == io.o_run) io.o_run++;
+  if (io.x_run < 1 || io.o_run < 1) return false;
+  // per-stage tables
+  std::vector<uint16_t> u16;
+  std::vector<int64_t> i64;
+  struct Off {
+    size_t rb, ro, koff, nofs, w_idx;
+  };
+  std::vector<Off> offs;
+  int w_total = 0, t_total = 0;
+  g.n_stages = int(steps.size());
+  g.max_bits = maxb;
+  for (size_t j = 0; j < steps.size(); ++j) {
+    const StepPlan &sp = P.steps[steps[j]];
+    std::map<int, int> local_in, local_out;
+    for (int i = 0; i < int(tile[j].size()); ++i) local_in[tile[j][i]] = i;
+    for (int i = 0; i < int(tile[j + 1].size()); ++i) local_out[tile[j + 1][i]] = i;
+    std::set<int> nset(nlab[j].begin(), nlab[j].end());
+    std::vector<int> mlab;  // M labels of the stage tile, ascending output position
+    for (int l : tile[j + 1])
+      if (!nset.count(l)) mlab.push_back(l);
+    {  // lane bits r0..r3: labels whose positions cover distinct swizzled bank bits
+      const int m = int(mlab.size());
+      int best_score = -1;
+      std::vector<int> best;
+      std::vector<int> pick;
+      std::function<void(int)> rec = [&](int from) {
+        if (int(pick.size()) == std::min(4, m)) {
+          int in_mask = 0, out_mask = 0;
+          for (int q : pick) {
+            in_mask |= 1 << (local_in.at(mlab[q]) & 3);
+            out_mask |= 1 << (local_out.at(mlab[q]) & 3);
+          }
+          const int score = __builtin_popcount(in_mask) + __builtin_popcount(out_mask);
+          if (score > best_score) best_score = score, best = pick;
+          return;
+        }
+        for (int q = from; q < m; ++q) {
+          pick.push_back(q);
+          rec(q + 1);
+          pick.pop_back();
+        }
+      };
+      rec(0);
+      std::vector<int> order;
+      for (int q : best) order.push_back(mlab[q]);
+      for (int q = 0; q < m; ++q)
+        if (std::find(best.begin(), best.end(), q) == best.end()) order.push_back(mlab[q]);
+      mlab = order;
+    }
+    stn::SweepStage &st = g.st[j];
+    st.in_bits = int(tile[j].size());
+    st.out_bits = int(tile[j + 1].size());
+    st.kb = int(klab[j].size());
+    st.nb = int(nlab[j].size());
+    const int R = 1 << int(mlab.size());
+    // register tile RB x NC: up to 32 outputs per thread while all 128 threads have work
+    {
+      const int mbits_n = int(mlab.size());
+      const int tile_log = std::max(0, std::min(5, st.out_bits - 7));
+      st.nc_log = std::min({st.nb, 3, tile_log});
+      st.rb_log = std::max(0, std::min({mbits_n - 4, 3, tile_log - st.nc_log}));
+      st.nc_log = std::min({st.nb, 3, tile_log - st.rb_log});
+      if (st.rb_log == 3) st.nc_log = std::min(st.nc_log, 2);
+    }
+    Off o;
+    o.rb = u16.size();
+    for (int r = 0; r < R; ++r) {
+      int v = 0;
+      for (int i = 0; i < int(mlab.size()); ++i)
+        if ((r >> i) & 1) v |= 1 << local_in.at(mlab[i]);
+      u16.push_back(uint16_t(sweep_phys(v)));
+    }
+    o.ro = u16.size();
+    for (int r = 0; r < R; ++r) {
+      int v = 0;
+      for (int i = 0; i < int(mlab.size()); ++i)
+        if ((r >> i) & 1) v |= 1 << local_out.at(mlab[i]);
+      u16.push_back(uint16_t(sweep_phys(v)));
+    }
+    o.koff = u16.size();
+    for (int k = 0; k < (1 << st.kb); ++k) {
+      int v = 0;
+      for (int i = 0; i < st.kb; ++i)
+        if ((k >> i) & 1) v |= 1 << local_in.at(klab[j][i]);
+      u16.push_back(uint16_t(sweep_phys(v)));
+    }
+    o.nofs = u16.size();
+    for (int n = 0; n < (1 << st.nb); ++n) {
+      int v = 0;
+      for (int i = 0; i < st.nb; ++i)
+        if ((n >> i) & 1) v |= 1 << local_out.at(nlab[j][i]);
+      u16.push_back(uint16_t(sweep_phys(v)));
+    }
+    while (u16.size() % 4) u16.push_back(0);
+    o.w_idx = i64.size();
+    const int K = 1 << st.kb, N = 1 << st.nb;
+    for (int k = 0; k < K; ++k)
+      for (int n = 0; n < N; ++n) {
+        int64_t off = 0;
+        for (int i = 0; i < st.kb; ++i)
+          if ((k >> i) & 1) off += int64_t(1) << sp.kbits[i].second;
+        for (int i = 0; i < st.nb; ++i)
+          if ((n >> i) & 1) off += int64_t(1) << sp.nbits[i].second;
+        i64.push_back(off);
+      }
+    st.w_smem = w_total;
+    w_total += (K * N + 1) & ~1;  // 16-byte aligned rows for the float4 W loads
+    st.t_smem = t_total;
+    t_total += K + N;
+    offs.push_back(o);
+  }
+  g.w_total = w_total;
+  g.t_total = t_total;
+  if (stn::sweep_smem_bytes(g) > 110 * 1024) return false;  // >= 2 CTAs per SM
+  if (!out) return true;
+  // one device buffer: int64 w_idx first, then the uint16 tables
+  std::vector<unsigned char> blob(i64.size() * 8 + u16.size() * 2);
+  memcpy(blob.data(), i64.data(), i64.size() * 8);
+  memcpy(blob.data() + i64.size() * 8, u16.data(), u16.size() * 2);
+  out->tables = std::make_shared<DevBuf>();
+  out->tables->upload(blob);
+  const int64_t *d64 = out->tables->as<int64_t>();
+  const uint16_t *d16 = reinterpret_cast<const uint16_t *>(d64 + i64.size());
+  for (size_t j = 0; j < steps.size(); ++j) {
+    g.st[j].rb = d16 + offs[j].rb;
+    g.st[j].ro = d16 + offs[j].ro;
+    g.st[j].koff = d16 + offs[j].koff;
+    g.st[j].nofs = d16 + offs[j].nofs;
+    g.st[j].w_idx = d64 + offs[j].w_idx;
+  }
+  out->steps = steps;
+  out->geom = g;
+  return true;
+}
+
+void plan_sweeps(stn_plan &P) {
+  P.sweeps.clear();
+  P.sweep_of_step.clear();
+  static const char *env_bits = std::getenv("STN_SWEEP_BITS");  // experiments: 0 disables
+  const int max_bits = env_bits ? std::atoi(env_bits) : 12;
+  if (max_bits <= 0) return;
+  const int n = int(P.steps.size());
+  std::vector<int> next(n, -1), has_prev(n, 0);
+  for (int i = 0; i < n; ++i) {
+    const StepPlan &sp = P.steps[i];
+    if (!sweep_candidate(P, sp)) continue;
+    const int c = P.nodes[sp.d.node].consumer;
+    if (c < 0 || !sweep_candidate(P, P.steps[c])) continue;
+    const StepPlan &cp = P.steps[c];
+    if ((cp.x_is_lhs ? cp.d.lhs : cp.d.rhs) != sp.d.node) continue;
+    next[i] = c;
+    has_prev[c] = 1;
+  }
+  for (int i = 0; i < n; ++i) {
+    if (has_prev[i] || next[i] < 0) continue;
+    std::vector<int> chain{i};
+    while (next[chain.back()] >= 0) chain.push_back(next[chain.back()]);
+    size_t a = 0;
+    while (a < chain.size()) {
+      size_t best = a;
+      for (size_t b = a + 1; b < chain.size(); ++b) {
+        std::vector<int> seg(chain.begin() + a, chain.begin() + b + 1);
+        if (build_sweep(P, seg, max_bits, nullptr))
+          best = b;
+        else
+          break;
+      }
+      if (best > a) {
+        stn_plan::Sweep sw;
+        std::vector<int> seg(chain.begin() + a, chain.begin() + best + 1);
+        static const char *env_only = std::getenv("STN_SWEEP_ONLY");  // profiling aid
+        static int seen = 0;
+        const bool take = !env_only || std::atoi(env_only) == seen;
+        ++seen;
+        if (take && build_sweep(P, seg, max_bits, &sw)) {
+          const int id = int(P.sweeps.size());
+          if (std::getenv("STN_SWEEP_DEBUG")) {
+            const stn::SweepGeom &g = sw.geom;
+            fprintf(stderr, "sweep %d: steps", id);
+            for (int q : seg) fprintf(stderr, " %d", q);
+            fprintf(stderr, " | xt %d ot %d max %d ob %d xrun %d orun %d smem %zu\n",
+                    g.io.xt_bits, g.io.ot_bits, g.max_bits, g.io.ob, g.io.x_run, g.io.o_run,
+                    stn::sweep_smem_bytes(g));
+            for (int q = 0; q < g.n_stages; ++q)
+              fprintf(stderr, "   stage %d: in %d out %d kb %d nb %d nc_log %d rb_log %d\n", q,
+                      g.st[q].in_bits, g.st[q].out_bits, g.st[q].kb, g.st[q].nb, g.st[q].nc_log,
+                      g.st[q].rb_log);
+          }
+          for (int st : seg) P.sweep_of_step[st] = id;
+          P.sweeps.push_back(std::move(sw));
+        }
+      }
+      a = best + 1;
+    }
+  }
+}
+
 void build_program(stn_plan &P, Program &prog, int which /*0 build, 1 cache, 2 no cache*/) {
   prog.ops.clear();
   prog.slice_leaves.clear();
@@ -683,15 +989,34 @@ void build_program(stn_plan &P, Program &prog, int which /*0 build, 1 cache, 2 n
     if (which == 1 && !br) run.push_back(i);
     if (which == 2) run.push_back(i);
   }
-  std::map<int, int> op_of_step;
-  for (int k = 0; k < int(run.size()); ++k) op_of_step[run[k]] = k;
-  const int64_t n_ops = int64_t(run.size());
-  // consumer op of each node within this program
-  std::map<int, int64_t> consumer_op;
+  // units: single steps, or a fused sweep emitted at the position of its last step
+  std::vector<std::vector<int>> units;
+  std::vector<int> unit_sweep;
   for (int k = 0; k < int(run.size()); ++k) {
-    const StepPlan &sp = P.steps[run[k]];
-    consumer_op[sp.d.lhs] = k;
-    consumer_op[sp.d.rhs] = k;
+    const int st = run[k];
+    auto sw = which == 0 ? P.sweep_of_step.end() : P.sweep_of_step.find(st);
+    if (sw == P.sweep_of_step.end()) {
+      units.push_back({st});
+      unit_sweep.push_back(-1);
+    } else if (P.sweeps[sw->second].steps.back() == st) {
+      units.push_back(P.sweeps[sw->second].steps);
+      unit_sweep.push_back(sw->second);
+    }
+  }
+  std::map<int, int> op_of_step;
+  for (int u = 0; u < int(units.size()); ++u)
+    for (int st : units[u]) op_of_step[st] = u;
+  const int64_t n_ops = int64_t(units.size());
+  // consumer op of each node within this program (chain-internal stems excluded)
+  std::map<int, int64_t> consumer_op;
+  for (int u = 0; u < int(units.size()); ++u) {
+    std::set<int> internal;
+    for (int st : units[u]) internal.insert(P.steps[st].d.node);
+    for (int st : units[u]) {
+      const StepPlan &sp = P.steps[st];
+      for (int in : {sp.d.lhs, sp.d.rhs})
+        if (!internal.count(in)) consumer_op[in] = u;
+    }
   }
   auto end_of = [&](int node) -> int64_t {
     auto it = consumer_op.find(node);
@@ -733,29 +1058,43 @@ void build_program(stn_plan &P, Program &prog, int which /*0 build, 1 cache, 2 n
     }
     return r;
   };
-  for (int k = 0; k < int(run.size()); ++k) {
-    const StepPlan &sp = P.steps[run[k]];
+  for (int u = 0; u < int(units.size()); ++u) {
+    const StepPlan &last = P.steps[units[u].back()];
     Op op;
-    op.step = run[k];
-    op.a = make_input(sp.d.lhs);
-    op.b = make_input(sp.d.rhs);
-    op.out.node = sp.d.node;
-    op.out.size = sp.osize;
-    if (which == 0 && P.cache_off.count(sp.d.node)) {
+    op.step = units[u].back();
+    op.sweep = unit_sweep[u];
+    if (op.sweep >= 0) {
+      const StepPlan &first = P.steps[units[u].front()];
+      op.a = make_input(first.x_is_lhs ? first.d.lhs : first.d.rhs);
+      for (int st : units[u]) {
+        const StepPlan &sp = P.steps[st];
+        op.wrefs.push_back(make_input(sp.x_is_lhs ? sp.d.rhs : sp.d.lhs));
+      }
+    } else {
+      op.a = make_input(last.d.lhs);
+      op.b = make_input(last.d.rhs);
+    }
+    op.out.node = last.d.node;
+    op.out.size = last.osize;
+    if (which == 0 && P.cache_off.count(last.d.node)) {
       op.out.kind = Src::Persist;
-      op.out.off = P.cache_off.at(sp.d.node);
+      op.out.off = P.cache_off.at(last.d.node);
     } else {
       op.out.kind = Src::Arena;
-      out_off_ptr[sp.d.node] = new_item(sp.osize, k, end_of(sp.d.node));
+      out_off_ptr[last.d.node] = new_item(last.osize, u, end_of(last.d.node));
     }
     prog.ops.push_back(op);
-    prog.mults += sp.d.mults;
-    prog.peak = std::max<uint64_t>(prog.peak, uint64_t(sp.osize));
+    for (int st : units[u]) {  // SubtaskResult bookkeeping counts every step
+      prog.mults += P.steps[st].d.mults;
+      prog.peak = std::max<uint64_t>(prog.peak, uint64_t(P.steps[st].osize));
+    }
   }
+  prog.n_steps = int(run.size());
   // gemm-path scratch (lifetime: the op itself)
   std::vector<std::array<int64_t *, 3>> scr(prog.ops.size(), {nullptr, nullptr, nullptr});
   for (size_t k = 0; k < prog.ops.size(); ++k) {
     const StepPlan &sp = P.steps[prog.ops[k].step];
+    if (prog.ops[k].sweep >= 0) continue;
     if (sp.kern != Kern::GemmSimt && sp.kern != Kern::GemmTc) continue;
     if (!sp.a_id) scr[k][0] = new_item(sp.lsize, int64_t(k), int64_t(k));
     if (!sp.b_id) scr[k][1] = new_item(sp.rsize, int64_t(k), int64_t(k));
@@ -790,7 +1129,10 @@ void build_program(stn_plan &P, Program &prog, int which /*0 build, 1 cache, 2 n
   prog.arena_elems = arena;
   for (size_t k = 0; k < prog.ops.size(); ++k) {
     Op &op = prog.ops[k];
-    for (Ref *r : {&op.a, &op.b})
+    std::vector<Ref *> refs{&op.a};
+    if (op.sweep < 0) refs.push_back(&op.b);
+    for (Ref &w : op.wrefs) refs.push_back(&w);
+    for (Ref *r : refs)
       if (r->kind == Src::Arena)
         r->off = *out_off_ptr.at(r->node);
       else if (r->kind == Src::SliceLeaf)
@@ -1128,6 +1470,7 @@ void create_plan(const stn_plan_desc *desc, int device, int mode, stn_plan *P) {
       }
     P->cache_elems = off;
   }
+  plan_sweeps(*P);
   build_program(*P, P->build, 0);
   build_program(*P, P->with_cache, 1);
   build_program(*P, P->no_cache, 2);
@@ -1226,8 +1569,27 @@ Resolved resolve(stn_plan &P, const Ref &r, const stn_cache *cache, int nb) {
   return {nullptr, 0};
 }
 
+void launch_sweep_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaStream_t st) {
+  const stn_plan::Sweep &sw = P.sweeps[op.sweep];
+  stn::SweepGeom g = sw.geom;
+  Resolved x = resolve(P, op.a, cache, nb), o = resolve(P, op.out, cache, nb);
+  double bytes = 8.0 * (x.bs ? nb : 1) * op.a.size + 8.0 * nb * op.out.size, flops = 0;
+  for (size_t j = 0; j < op.wrefs.size(); ++j) {
+    Resolved w = resolve(P, op.wrefs[j], cache, nb);
+    g.w[j] = w.ptr;
+    g.w_bs[j] = w.bs;
+    bytes += 8.0 * (w.bs ? nb : 1) * op.wrefs[j].size;
+  }
+  for (int stp : sw.steps) flops += 8.0 * double(P.steps[stp].d.mults) * nb;
+  ProfScope prof(P, st, sw.steps.front());
+  stn::BatchPtrs p{x.ptr, nullptr, const_cast<void *>(o.ptr), x.bs, 0, o.bs, nb};
+  cuda_check(stn::launch_sweep(g, p, P.mode == STN_MODE_EXACT, st), "stem sweep kernel");
+  prof.done(STN_KERNEL_SWEEP, bytes, flops);
+}
+
 template <class R>
 void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaStream_t st) {
+  if (op.sweep >= 0) return launch_sweep_op(P, op, cache, nb, st);
   const StepPlan &sp = P.steps[op.step];
   Resolved a = resolve(P, op.a, cache, nb), b = resolve(P, op.b, cache, nb);
   Resolved o = resolve(P, op.out, cache, nb);
@@ -1464,7 +1826,7 @@ void run_one(stn_plan &P, const int32_t *digits, const stn_cache *cache, cudaStr
              "result download");
   cuda_check(cudaStreamSynchronize(st), "stream sync");
   if (info) {
-    info->step_count = int32_t(prog.ops.size());
+    info->step_count = int32_t(prog.n_steps);
     info->mults = prog.mults;
     info->peak_elements = prog.peak;
   }
@@ -1529,7 +1891,7 @@ int stn_plan_get_info(const stn_plan *P, stn_plan_info *info) {
   info->out_rank = int32_t(P->out_dims.size());
   info->out_elements = P->out_elements;
   for (size_t i = 0; i < P->out_dims.size() && i < 64; ++i) info->out_dims[i] = P->out_dims[i];
-  info->per_slice_steps = int32_t(P->with_cache.ops.size());
+  info->per_slice_steps = int32_t(P->with_cache.n_steps);
   info->per_slice_mults = P->with_cache.mults;
   for (auto &sp : P->steps)
     if (sp.d.is_branch) info->branch_mults += sp.d.mults;
@@ -1537,6 +1899,11 @@ int stn_plan_get_info(const stn_plan *P, stn_plan_info *info) {
   info->arena_bytes_per_slice = uint64_t(P->with_cache.arena_elems) * P->esize;
   info->cache_bytes = uint64_t(P->cache_elems) * P->esize;
   for (auto &op : P->with_cache.ops) {
+    if (op.sweep >= 0) {
+      info->sweeps++;
+      info->steps_in_sweeps += int32_t(P->sweeps[op.sweep].steps.size());
+      continue;
+    }
     Kern k = P->steps[op.step].kern;
     if (k == Kern::GemmTc) info->steps_tensor_core++;
     else if (k == Kern::GemmSimt) info->steps_generic++;

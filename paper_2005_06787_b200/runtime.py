@@ -127,7 +127,8 @@ class ExecutablePlan:
     def kernel_mix(self) -> dict:
         i = self.info
         return {"tensor_core": i.steps_tensor_core, "absorb": i.steps_absorb,
-                "generic": i.steps_generic}
+                "generic": i.steps_generic, "sweeps": i.sweeps,
+                "steps_in_sweeps": i.steps_in_sweeps}
 
 
 def load_desc(path: str):

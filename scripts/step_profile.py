@@ -21,6 +21,7 @@ run_slices(plan, cache, 0, n, acc=acc)
 torch.cuda.synchronize()
 rows = plan.get_step_profile()
 tot = sum(r["ms"] for r in rows)
+print(plan.kernel_mix())
 print(f"{cfg} {mode}: {n} slices, {tot / n:.3f} ms/slice over {len(rows)} steps")
 print("step kernel     M          N          K        ms/slice  share   GB/s    TFLOP/s")
 for r in sorted(rows, key=lambda r: -r["ms"]):
