@@ -110,8 +110,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_absorb_tc(const __grid_constant__ AbsorbGeom g, const BatchPtrs p, int64_t n_tiles) {
   using L = TcAbsorbLayout<KP, NP>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char *smem = reinterpret_cast<unsigned char *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align inside the shared window (keeps the pointer in the shared address
+  // space, so the compiler emits STS/LDS rather than generic ST/LD)
+  unsigned char *smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   unsigned char *a_hi = smem;
   unsigned char *a_lo = a_hi + L::A_PLANE;
   unsigned char *b_hi = a_lo + L::A_PLANE;

@@ -156,6 +156,9 @@ cudaError_t launch_permute(const StridedGeom &g, const void *in, void *out, int6
 // tcgen05 split-TF32 absorb (absorb_tc.cu): AbsorbGeom with exactly 7 tile
 // bits (128 rows), K <= 32, N <= 64. FAST mode only.
 bool tc_absorb_supported(const AbsorbGeom &g);
+// tcgen05 direct absorb (absorb_mma.cu, FAST mode): DirectGeom with 4 <= K <= 64, N <= 64
+bool mma_absorb_supported(const DirectGeom &g);
+cudaError_t launch_absorb_mma(const DirectGeom &g, const BatchPtrs &p, cudaStream_t stream);
 cudaError_t launch_absorb_tc(const AbsorbGeom &g, const BatchPtrs &p, cudaStream_t stream);
 // Tiled bond-2 bit permutation (the absorb tile machinery with K = N = 0).
 cudaError_t launch_bitperm(const AbsorbGeom &g, const void *in, void *out, int64_t in_bs,

@@ -109,7 +109,7 @@ struct DevBuf {
 // ---------------------------------------------------------------------------
 // plan model
 // ---------------------------------------------------------------------------
-enum class Kern { Generic, Absorb, AbsorbTc, AbsorbDirect, SplitK, GemmSimt, GemmTc };
+enum class Kern { Generic, Absorb, AbsorbTc, AbsorbDirect, AbsorbMma, SplitK, GemmSimt, GemmTc };
 
 struct Node {
   bool is_leaf = false;
@@ -587,6 +587,14 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     const int direct_max = dmax ? std::atoi(dmax) : 12;
     static const char *dminl = std::getenv("STN_DIRECT_MIN_L");
     const int direct_min_L = dminl ? std::atoi(dminl) : 2;
+    // FAST mode, K x N >= 2^STN_MMA_MIN_BITS: tensor-core direct absorb
+    const char *mmin = std::getenv("STN_MMA_MIN_BITS");
+    const int mma_min = mmin ? std::atoi(mmin) : 10;
+    if (!exact && sp.direct_ok && stn::mma_absorb_supported(sp.dg) &&
+        sp.dg.kb + sp.dg.nb >= mma_min) {
+      sp.kern = Kern::AbsorbMma;
+      return;
+    }
     if (sp.direct_ok && sp.dg.L >= direct_min_L && sp.dg.kb + sp.dg.nb <= direct_max) {
       sp.kern = Kern::AbsorbDirect;
       return;
@@ -905,8 +913,12 @@ bool build_sweep(const stn_plan &P, const std::vector<int> &steps, int max_bits,
 void plan_sweeps(stn_plan &P) {
   P.sweeps.clear();
   P.sweep_of_step.clear();
-  static const char *env_bits = std::getenv("STN_SWEEP_BITS");  // experiments: 0 disables
-  const int max_bits = env_bits ? std::atoi(env_bits) : 12;
+  // Off by default: measured on B200 (profiles/r01_sweep_vs_unfused.txt) the
+  // per-tile stage math of a sweep is FFMA-issue bound and loses to the
+  // unfused HBM-rate direct / tensor-core absorbs. STN_SWEEP_BITS=<tile bits>
+  // (e.g. 12) enables it; read per plan so tests can toggle it.
+  const char *env_bits = std::getenv("STN_SWEEP_BITS");
+  const int max_bits = env_bits ? std::atoi(env_bits) : 0;
   if (max_bits <= 0) return;
   const int n = int(P.steps.size());
   std::vector<int> next(n, -1), has_prev(n, 0);
@@ -1625,6 +1637,14 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
       prof.done(STN_KERNEL_ABSORB_TC, io_bytes, flops);
       break;
     }
+    case Kern::AbsorbMma: {
+      const Resolved &x = sp.x_is_lhs ? a : b;
+      const Resolved &w = sp.x_is_lhs ? b : a;
+      stn::BatchPtrs p{x.ptr, w.ptr, out, x.bs, w.bs, o.bs, nb};
+      cuda_check(stn::launch_absorb_mma(sp.dg, p, st), "tensor-core direct absorb kernel");
+      prof.done(STN_KERNEL_ABSORB_TC, io_bytes, flops);
+      break;
+    }
     case Kern::AbsorbDirect: {
       const Resolved &x = sp.x_is_lhs ? a : b;
       const Resolved &w = sp.x_is_lhs ? b : a;
@@ -1907,7 +1927,8 @@ int stn_plan_get_info(const stn_plan *P, stn_plan_info *info) {
     Kern k = P->steps[op.step].kern;
     if (k == Kern::GemmTc) info->steps_tensor_core++;
     else if (k == Kern::GemmSimt) info->steps_generic++;
-    else if (k == Kern::Absorb || k == Kern::AbsorbTc || k == Kern::AbsorbDirect)
+    else if (k == Kern::Absorb || k == Kern::AbsorbTc || k == Kern::AbsorbDirect ||
+             k == Kern::AbsorbMma)
       info->steps_absorb++;
     else info->steps_generic++;
   }

@@ -230,3 +230,41 @@ def test_large_config_fast_vs_fp64(name):
     ee = rel_err(run_subtask(exact, a, ce).value, truth)
     print(f"{name} slice {a}: fast err {ef:.2e}, reference-single (exact) err {ee:.2e}")
     assert ef <= max(RTOL, 2 * ee)
+
+
+@pytest.mark.parametrize("name", ["cfg1_grid4x5_m14", "cfg2_grid5x6_m16"])
+def test_stem_sweeps_are_bitwise_the_unfused_steps(name, monkeypatch):
+    """Fused stem sweeps (STN_SWEEP_BITS) keep every output's operation order:
+    EXACT mode stays bitwise equal to the reference, FAST mode within tolerance."""
+    from paper_2005_06787_b200 import build_branch_cache, run_subtask
+    monkeypatch.setenv("STN_SWEEP_BITS", "12")
+    asg, vals, _, _, _ = read_ref(name, "single")
+    plan = load(name, "single", "exact")
+    assert plan.kernel_mix()["sweeps"] > 0
+    cache = build_branch_cache(plan)
+    for a, want in list(zip(asg, vals))[:2]:
+        r = run_subtask(plan, int(a), cache)
+        assert np.array_equal(bits(r.value.ravel()), bits(want)), (name, int(a))
+    fast = load(name, "single", "fast")
+    cache = build_branch_cache(fast)
+    a, want = int(asg[0]), vals[0]
+    truth, tol = truth_and_tolerance(name, a, want)
+    assert rel_err(run_subtask(fast, a, cache).value, truth) <= tol
+
+
+def test_tensor_core_absorbs_run_and_meet_tolerance():
+    """cfg2's K=N=64 and K=64,N=16 stem absorbs run on the tcgen05 direct
+    absorb (absorb_mma.cu) in FAST mode; the slice stays within tolerance."""
+    from paper_2005_06787_b200 import build_branch_cache, run_subtask
+    name = "cfg2_grid5x6_m16"
+    asg, vals, _, _, _ = read_ref(name, "single")
+    plan = load(name, "single", "fast")
+    plan.set_profiling(True)
+    cache = build_branch_cache(plan)
+    plan.reset_profile()
+    got = run_subtask(plan, int(asg[0]), cache).value
+    rows = plan.get_step_profile()
+    tc = [r for r in rows if r["kernel"] == "absorb_tc" and r["K"] == 64]
+    assert len(tc) >= 2, rows
+    truth, tol = truth_and_tolerance(name, int(asg[0]), vals[0])
+    assert rel_err(got, truth) <= tol
