@@ -10,6 +10,9 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <utility>
+#include <vector>
+
 namespace stn {
 
 constexpr int kMaxAxes = 40;
@@ -160,6 +163,31 @@ bool tc_absorb_supported(const AbsorbGeom &g);
 bool mma_absorb_supported(const DirectGeom &g);
 cudaError_t launch_absorb_mma(const DirectGeom &g, const BatchPtrs &p, cudaStream_t stream);
 cudaError_t launch_absorb_tc(const AbsorbGeom &g, const BatchPtrs &p, cudaStream_t stream);
+// Gather-fed tcgen05 absorb (absorb_tma.cu, FAST mode): 8 <= K <= 64, 4 <= N <= 64, X bit
+// 0 an M bit. The X tile of every stage is gathered straight into the UMMA MN-major
+// operand layout (the step's permutation fused into the load): by cp.async 16-byte
+// chunks (default), or -- when X bits 0..3 are M bits and the tile bits form <= 5 runs --
+// by one TMA box whose dims are [0] X bits 0..3 (+ re/im), the runs of K bits, the runs
+// of tile M bits, each extended over the outer bits above it (its TMA coordinate).
+struct TmaAbsorbGeom {
+  int ndims;
+  int dim_a[5], dim_c[5], dim_box[5];  // X positions [a, c) of dim d; the box covers [a, a+box)
+  uint64_t outer_x_mask, outer_o_mask;  // outer M bits (tile index) in X and in O
+  uint64_t loopk_x_mask;                // K bits iterated by the stages of a tile
+  uint64_t tile_x_mask, stagek_x_mask;  // tile M bits, stage K bits (gather loader)
+  int tma_ok;                           // the box loader applies (X bits 0..3 in M, <= 5 dims)
+  int64_t n_tiles;
+  int K, N, kstage, mbl, nm, spt;       // stage K bits, log2 M blocks, N_mma, stages/tile
+  int nsr, nsl;                         // ring depths (set at launch from the smem budget)
+  int dbg;
+  int64_t o_m_off[256];                 // O offset of tile-local m
+  int64_t w_k_off[64];                  // W offset of k (k bits in ascending X position)
+  int64_t w_n_off[128];                 // [0, 64): W offset of n; [64, 128): O offset of n
+};
+bool build_tma_absorb(const std::vector<std::pair<int, int>> &kbits,
+                      const std::vector<std::pair<int, int>> &mbits,
+                      const std::vector<std::pair<int, int>> &nbits, int xr, TmaAbsorbGeom &g);
+cudaError_t launch_absorb_tma(const TmaAbsorbGeom &g, const BatchPtrs &p, cudaStream_t stream);
 // Tiled bond-2 bit permutation (the absorb tile machinery with K = N = 0).
 cudaError_t launch_bitperm(const AbsorbGeom &g, const void *in, void *out, int64_t in_bs,
                            int64_t out_bs, int nbatch, cudaStream_t stream);

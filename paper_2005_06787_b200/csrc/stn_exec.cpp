@@ -109,7 +109,7 @@ struct DevBuf {
 // ---------------------------------------------------------------------------
 // plan model
 // ---------------------------------------------------------------------------
-enum class Kern { Generic, Absorb, AbsorbTc, AbsorbDirect, AbsorbMma, SplitK, GemmSimt, GemmTc };
+enum class Kern { Generic, Absorb, AbsorbTc, AbsorbDirect, AbsorbMma, SplitK, GemmSimt, GemmTc, AbsorbTma };
 
 struct Node {
   bool is_leaf = false;
@@ -132,6 +132,7 @@ struct StepPlan {
   bool tc_ok = false;
   stn::DirectGeom dg{};     // tile-free variant (identity low bits)
   bool direct_ok = false;
+  std::shared_ptr<stn::TmaAbsorbGeom> tg;  // TMA-fed tensor-core variant (X bits 0..3 in M)
   // absorb bit geometry (positions in X / W / O), kept for stem-sweep fusion
   bool has_bits = false;
   int xr = 0, wr = 0, orank_ = 0;
@@ -487,6 +488,10 @@ bool build_absorb(StepPlan &sp, const std::vector<int> &ldims, const std::vector
 
   sp.x_is_lhs = x_lhs;
   sp.has_bits = true;
+  {
+    auto tg = std::make_shared<stn::TmaAbsorbGeom>();
+    if (stn::build_tma_absorb(kbits, mbits, nbits, xr, *tg)) sp.tg = tg;
+  }
   sp.xr = xr;
   sp.wr = wr;
   sp.orank_ = orank;
@@ -590,6 +595,13 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     // FAST mode, K x N >= 2^STN_MMA_MIN_BITS: tensor-core direct absorb
     const char *mmin = std::getenv("STN_MMA_MIN_BITS");
     const int mma_min = mmin ? std::atoi(mmin) : 10;
+    // FAST mode, K x N >= 2^STN_TMA_MIN_BITS: TMA-fed tensor-core absorb
+    const char *tmin = std::getenv("STN_TMA_MIN_BITS");
+    const int tma_min = tmin ? std::atoi(tmin) : 99;  // off until it beats the SIMT paths
+    if (!exact && sp.tg && int(sp.kbits.size() + sp.nbits.size()) >= tma_min) {
+      sp.kern = Kern::AbsorbTma;
+      return;
+    }
     if (!exact && sp.direct_ok && stn::mma_absorb_supported(sp.dg) &&
         sp.dg.kb + sp.dg.nb >= mma_min) {
       sp.kern = Kern::AbsorbMma;
@@ -689,6 +701,41 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     sp.gs = {d.D, d.M, d.N, d.K};
     sp.kern = (single && !exact && stn::gemm_tc_supported(sp.gs)) ? Kern::GemmTc : Kern::GemmSimt;
   }
+}
+
+// Diagnostics (STN_PLAN_DUMP): one line per large step with its kernel and bit geometry.
+void dump_step(const StepPlan &sp, int i) {
+  static const char *names[] = {"generic", "absorb", "absorb_tc", "direct", "mma", "splitk",
+                                "gemm_simt", "gemm_tc", "tma"};
+  auto lg = [](int64_t v) { int b = 0; while ((int64_t(1) << b) < v) ++b; return b; };
+  std::string s = "step " + std::to_string(i) + " " + names[int(sp.kern)] + " l2^" +
+                  std::to_string(lg(sp.lsize)) + " r2^" + std::to_string(lg(sp.rsize)) + " o2^" +
+                  std::to_string(lg(sp.osize)) + " D" + std::to_string(sp.d.D) + " M" +
+                  std::to_string(sp.d.M) + " N" + std::to_string(sp.d.N) + " K" +
+                  std::to_string(sp.d.K);
+  if (sp.has_bits) {
+    s += " x_lhs=" + std::to_string(sp.x_is_lhs) + " L=" + std::to_string(sp.dg.L) + " k(x,w):";
+    for (auto &p : sp.kbits) s += " " + std::to_string(p.first) + "," + std::to_string(p.second);
+    s += " n(o,w):";
+    for (auto &p : sp.nbits) s += " " + std::to_string(p.first) + "," + std::to_string(p.second);
+    s += " m(x,o)<16:";
+    for (auto &p : sp.mbits)
+      if (p.first < 16 || p.second < 16)
+        s += " " + std::to_string(p.first) + "," + std::to_string(p.second);
+  }
+  if (sp.kern == Kern::GemmTc || sp.kern == Kern::GemmSimt) {
+    s += " a_id=" + std::to_string(sp.a_id) + " b_id=" + std::to_string(sp.b_id) +
+         " c_id=" + std::to_string(sp.c_id);
+    auto perm = [&](const char *n, const std::vector<int> &p) {
+      s += std::string(" ") + n + "=[";
+      for (int v : p) s += std::to_string(v) + " ";
+      s += "]";
+    };
+    perm("lperm", sp.lperm);
+    perm("rperm", sp.rperm);
+    perm("operm", sp.operm);
+  }
+  fprintf(stderr, "%s\n", s.c_str());
 }
 
 // ---------------------------------------------------------------------------
@@ -1442,6 +1489,8 @@ void create_plan(const stn_plan_desc *desc, int device, int mode, stn_plan *P) {
     require(D == d.D && M == d.M && N == d.N && K == d.K && sp.osize == D * M * N,
             STN_ERR_MALFORMED_NETWORK, "step shape inconsistent at node " + std::to_string(d.node));
     choose_kernel(*P, sp, ld, rd);
+    if (std::getenv("STN_PLAN_DUMP") && !d.is_branch && sp.osize + sp.lsize + sp.rsize >= (1 << 20))
+      dump_step(sp, i);
   }
   // root
   {
@@ -1634,6 +1683,14 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
       const Resolved &w = sp.x_is_lhs ? b : a;
       stn::BatchPtrs p{x.ptr, w.ptr, out, x.bs, w.bs, o.bs, nb};
       cuda_check(stn::launch_absorb_tc(sp.agtc, p, st), "tensor-core absorb kernel");
+      prof.done(STN_KERNEL_ABSORB_TC, io_bytes, flops);
+      break;
+    }
+    case Kern::AbsorbTma: {
+      const Resolved &x = sp.x_is_lhs ? a : b;
+      const Resolved &w = sp.x_is_lhs ? b : a;
+      stn::BatchPtrs p{x.ptr, w.ptr, out, x.bs, w.bs, o.bs, nb};
+      cuda_check(stn::launch_absorb_tma(*sp.tg, p, st), "TMA tensor-core absorb kernel");
       prof.done(STN_KERNEL_ABSORB_TC, io_bytes, flops);
       break;
     }
@@ -1928,7 +1985,7 @@ int stn_plan_get_info(const stn_plan *P, stn_plan_info *info) {
     if (k == Kern::GemmTc) info->steps_tensor_core++;
     else if (k == Kern::GemmSimt) info->steps_generic++;
     else if (k == Kern::Absorb || k == Kern::AbsorbTc || k == Kern::AbsorbDirect ||
-             k == Kern::AbsorbMma)
+             k == Kern::AbsorbMma || k == Kern::AbsorbTma)
       info->steps_absorb++;
     else info->steps_generic++;
   }
