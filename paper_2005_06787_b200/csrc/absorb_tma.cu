@@ -47,7 +47,19 @@ using namespace ptx;
 
 constexpr int kConvWarps = 4, kEpiWarps = 4;
 constexpr int kMaxNSR = 10, kMaxNSL = 4;  // ring depths: raw X stages, lo planes
-constexpr int kLag = 5;  // cp.async groups in flight per loader thread (GATHER)
+constexpr int kMaxLag = 6;  // cp.async groups in flight per loader thread (GATHER), <= nsr - 2
+
+__device__ __forceinline__ void cp_async_wait(int n) {  // wait_group takes an immediate
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+    case 5: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 6;" ::: "memory"); break;
+  }
+}
 
 template <int KSZ, int MB, int NM>
 struct TmaLayout {
@@ -55,7 +67,20 @@ struct TmaLayout {
   static constexpr int LBO = KSZ * 128;              // MN-atom stride (32 m-floats x KSZ rows)
   static constexpr int BROWS = 2 * NM;               // B'' rows: hi then lo
   static constexpr int ACC = MB * 2 * NM;            // TMEM columns of one accumulator buffer
-  static constexpr int TMEM_COLS = 2 * ACC <= 32 ? 32 : (2 * ACC <= 64 ? 64 : (2 * ACC <= 128 ? 128 : (2 * ACC <= 256 ? 256 : 512)));
+  static constexpr int NACC = 4 * ACC <= 512 ? 4 : 2;  // accumulator buffers
+  static constexpr int TMEM_COLS = NACC * ACC <= 32 ? 32 : (NACC * ACC <= 64 ? 64 : (NACC * ACC <= 128 ? 128 : (NACC * ACC <= 256 ? 256 : 512)));
+};
+
+// Position in a ring of mbarrier-guarded slots: slot index and the parity of its phase.
+struct RingPos {
+  int idx = 0;
+  uint32_t phase = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++idx == n) {
+      idx = 0;
+      phase ^= 1u;
+    }
+  }
 };
 
 __device__ __forceinline__ uint64_t pdep64(uint64_t v, uint64_t mask) {
@@ -107,8 +132,8 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
   uint64_t *bars = reinterpret_cast<uint64_t *>(x_k + KSZ);
   uint64_t *full = bars, *empty = full + kMaxNSR;
   uint64_t *lofull = empty + kMaxNSR, *loempty = lofull + kMaxNSL;
-  uint64_t *acc_full = loempty + kMaxNSL, *acc_empty = acc_full + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
+  uint64_t *acc_full = loempty + kMaxNSL, *acc_empty = acc_full + 4;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 4);
 
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int spt = g.spt;  // stages per tile
@@ -142,7 +167,7 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
       mbar_init(&lofull[s], R::LOAD_WARPS);
       mbar_init(&loempty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < Lay::NACC; ++a) {
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], kEpiWarps);
     }
@@ -160,19 +185,20 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int64_t G = gridDim.x;
-  const int64_t n_tiles = g.n_tiles;
+  // each CTA owns a contiguous range of tiles, so outer offsets advance by pdep increments
+  const int64_t t_begin = g.n_tiles * blockIdx.x / gridDim.x;
+  const int64_t t_end = g.n_tiles * (blockIdx.x + 1) / gridDim.x;
 
   if (!GATHER && warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      int gs = 0;
-      for (int64_t t = blockIdx.x; t < n_tiles; t += G) {
-        const uint64_t xt = pdep64(uint64_t(t), g.outer_x_mask);
-        for (int j = 0; j < spt; ++j, ++gs) {
-          const int s = gs % nsr;
-          mbar_wait(&empty[s], ((gs / nsr) & 1) ^ 1);
+      RingPos rs;
+      uint64_t xt = pdep64(uint64_t(t_begin), g.outer_x_mask);
+      for (int64_t t = t_begin; t < t_end; ++t, xt = ((xt | ~g.outer_x_mask) + 1) & g.outer_x_mask) {
+        for (int j = 0; j < spt; ++j, rs.next(nsr)) {
+          const int s = rs.idx;
+          mbar_wait(&empty[s], rs.phase ^ 1);
           const uint64_t full_idx = xt | pdep64(uint64_t(j), g.loopk_x_mask);
           int c[5] = {0, 0, 0, 0, 0};
 #pragma unroll
@@ -192,16 +218,17 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
       const uint32_t raw_base = smem_u32(raw), lo_base = smem_u32(lo);
       constexpr uint32_t IDESC1 = idesc_tf32(2 * NM, true);
       constexpr uint32_t IDESC2 = idesc_tf32(NM, true);
-      int gs = 0, i = 0;
-      for (int64_t t = blockIdx.x; t < n_tiles; t += G, ++i) {
-        const int a = i & 1;
-        mbar_wait(&acc_empty[a], ((i >> 1) & 1) ^ 1);
+      RingPos rs, rl;
+      int i = 0;
+      for (int64_t t = t_begin; t < t_end; ++t, ++i) {
+        const int a = i % Lay::NACC;
+        mbar_wait(&acc_empty[a], ((i / Lay::NACC) & 1) ^ 1);
         tc_fence_after();
         const uint32_t acc_base = tmem + uint32_t(a * Lay::ACC);
-        for (int j = 0; j < spt; ++j, ++gs) {
-          const int s = gs % nsr, l = gs % nsl;
-          mbar_wait(&full[s], (gs / nsr) & 1);
-          mbar_wait(&lofull[l], (gs / nsl) & 1);
+        for (int j = 0; j < spt; ++j, rs.next(nsr), rl.next(nsl)) {
+          const int s = rs.idx, l = rl.idx;
+          mbar_wait(&full[s], rs.phase);
+          mbar_wait(&lofull[l], rl.phase);
           tc_fence_after();
 #pragma unroll
           for (int q = 0; q < KSZ / 8; ++q) {
@@ -231,9 +258,10 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
     constexpr int LT = 32 * R::LOAD_WARPS;
     constexpr int CPT = Lay::STAGE / 16 / LT;  // 16-byte chunks per thread and stage
     // lo = x - trunc_tf32(x) for this thread's chunks (GATHER) or a strided share (TMA)
-    auto convert = [&](int h) {
-      const int s = h % nsr, l = h % nsl;
-      mbar_wait(&loempty[l], ((h / nsl) & 1) ^ 1);
+    RingPos cs, cl;  // slot of the next stage to convert
+    auto convert = [&]() {
+      const int s = cs.idx, l = cl.idx;
+      mbar_wait(&loempty[l], cl.phase ^ 1);
       const float4 *src = reinterpret_cast<const float4 *>(raw + s * Lay::STAGE);
       float4 *dst = reinterpret_cast<float4 *>(lo + l * Lay::STAGE);
       if (!(g.dbg & 4)) {
@@ -251,6 +279,8 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
         if (GATHER) mbar_arrive(&full[s]);
         mbar_arrive(&lofull[l]);
       }
+      cs.next(nsr);
+      cl.next(nsl);
     };
     if constexpr (GATHER) {
       // ---------------- loaders: cp.async gather of the X tile, then lo ----------------
@@ -267,14 +297,18 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
         src_off[u] = x_m2[mm * 8 + plo] + x_k[k];
       }
       const uint32_t raw_base = smem_u32(raw);
+      const int lag = g.lag;
       uint64_t pol;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
       int gs = 0;
-      for (int64_t t = blockIdx.x; t < n_tiles; t += G) {
-        const int64_t xt = int64_t(pdep64(uint64_t(t), g.outer_x_mask));
-        for (int j = 0; j < spt; ++j, ++gs) {
-          const int s = gs % nsr;
-          mbar_wait(&empty[s], ((gs / nsr) & 1) ^ 1);
+      RingPos rs;
+      uint64_t xtu = pdep64(uint64_t(t_begin), g.outer_x_mask);
+      for (int64_t t = t_begin; t < t_end;
+           ++t, xtu = ((xtu | ~g.outer_x_mask) + 1) & g.outer_x_mask) {
+        const int64_t xt = int64_t(xtu);
+        for (int j = 0; j < spt; ++j, ++gs, rs.next(nsr)) {
+          const int s = rs.idx;
+          mbar_wait(&empty[s], rs.phase ^ 1);
           const float2 *base = X + xt + int64_t(pdep64(uint64_t(j), g.loopk_x_mask));
           const uint32_t sdst = raw_base + uint32_t(s * Lay::STAGE);
 #pragma unroll
@@ -284,66 +318,83 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
                          "l"(base + src_off[u]), "l"(pol)
                          : "memory");
           asm volatile("cp.async.commit_group;" ::: "memory");
-          if (gs >= kLag) {
-            asm volatile("cp.async.wait_group %0;" ::"n"(kLag) : "memory");
-            convert(gs - kLag);
+          if (gs >= lag) {
+            cp_async_wait(lag);
+            convert();
           }
         }
       }
       asm volatile("cp.async.wait_group 0;" ::: "memory");
-      for (int h = gs - kLag < 0 ? 0 : gs - kLag; h < gs; ++h) convert(h);
+      for (int h = gs - lag < 0 ? 0 : gs - lag; h < gs; ++h) convert();
     } else {
       // ---------------- converters (TMA variant) ----------------
-      int gs = 0;
-      for (int64_t t = blockIdx.x; t < n_tiles; t += G)
-        for (int j = 0; j < spt; ++j, ++gs) {
-          mbar_wait(&full[gs % nsr], (gs / nsr) & 1);
-          convert(gs);
+      for (int64_t t = t_begin; t < t_end; ++t)
+        for (int j = 0; j < spt; ++j) {
+          mbar_wait(&full[cs.idx], cs.phase);
+          convert();
         }
     }
   } else if (warp >= R::EPI_WARP0) {
     // ---------------- epilogue ----------------
+    // The tile's accumulator is read in batches of up to 4 16-column chunks (all loads of
+    // a batch in flight together); the TMEM buffer is handed back to the MMA thread as
+    // soon as the last batch is in registers, before the shuffles and stores.
+    constexpr int CH = MB * NM / 16, BATCH = CH < 4 ? CH : 4;
     const int q4 = warp & 3;              // TMEM lane quadrant of this warp
     const int row = 32 * q4 + lane;       // real row 2m + s within a 128-row block
     const int sc = row & 1;
     int i = 0;
-    for (int64_t t = blockIdx.x; t < n_tiles; t += G, ++i) {
-      const int a = i & 1;
-      mbar_wait(&acc_full[a], (i >> 1) & 1);
+    uint64_t oo = pdep64(uint64_t(t_begin), g.outer_o_mask);
+    for (int64_t t = t_begin; t < t_end;
+         ++t, ++i, oo = ((oo | ~g.outer_o_mask) + 1) & g.outer_o_mask) {
+      const int a = i % Lay::NACC;
+      mbar_wait(&acc_full[a], (i / Lay::NACC) & 1);
       tc_fence_after();
-      const int64_t o_outer = int64_t(pdep64(uint64_t(t), g.outer_o_mask));
+      const int64_t o_outer = int64_t(oo);
+      const uint32_t tq = tmem + (uint32_t(32 * q4) << 16) + uint32_t(a * Lay::ACC);
 #pragma unroll
-      for (int b = 0; b < MB; ++b) {
-        const int ml = 64 * b + (row >> 1);
-        float2 *orow = O + o_outer + o_m[ml];
-        const uint32_t tb = tmem + (uint32_t(32 * q4) << 16) + uint32_t(a * Lay::ACC + b * 2 * NM);
+      for (int c0 = 0; c0 < CH; c0 += BATCH) {
+        float vals[BATCH][16];
+        {
+          uint32_t vm[BATCH][16], vc[BATCH][16];
 #pragma unroll
-        for (int c0 = 0; c0 < NM; c0 += 16) {
-          uint32_t vm[16], vc[16];
-          tmem_ld16(tb + uint32_t(c0), vm);
-          tmem_ld16(tb + uint32_t(NM + c0), vc);
+          for (int u = 0; u < BATCH; ++u) {
+            const int c = c0 + u, b = c / (NM / 16), cc = (c % (NM / 16)) * 16;
+            tmem_ld16(tq + uint32_t(b * 2 * NM + cc), vm[u]);
+            tmem_ld16(tq + uint32_t(b * 2 * NM + NM + cc), vc[u]);
+          }
           tmem_wait_ld();
-          float vals[16], other[16];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) vals[q] = __uint_as_float(vm[q]) + __uint_as_float(vc[q]);
+          for (int u = 0; u < BATCH; ++u)
 #pragma unroll
-          for (int q = 0; q < 16; ++q) other[q] = __shfl_xor_sync(0xffffffffu, vals[q], 1);
+            for (int q = 0; q < 16; ++q)
+              vals[u][q] = __uint_as_float(vm[u][q]) + __uint_as_float(vc[u][q]);
+        }
+        if (c0 + BATCH >= CH) {  // all of this tile's TMEM is in registers
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[a]);
+        }
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u) {
+          const int c = c0 + u, b = c / (NM / 16), cc = (c % (NM / 16)) * 16;
+          float2 *orow = O + o_outer + o_m[64 * b + (row >> 1)];
+          float other[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) other[q] = __shfl_xor_sync(0xffffffffu, vals[u][q], 1);
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
-            const int nl = 4 * sc + h;  // this lane finishes n = c0/2 + nl
-            const int n = (c0 >> 1) + nl;
-            const float xr_wr = sc ? other[2 * nl] : vals[2 * nl];
-            const float xr_wi = sc ? other[2 * nl + 1] : vals[2 * nl + 1];
-            const float xi_wr = sc ? vals[2 * nl] : other[2 * nl];
-            const float xi_wi = sc ? vals[2 * nl + 1] : other[2 * nl + 1];
+            const int nl = 4 * sc + h;  // this lane finishes n = cc/2 + nl
+            const int n = (cc >> 1) + nl;
+            const float xr_wr = sc ? other[2 * nl] : vals[u][2 * nl];
+            const float xr_wi = sc ? other[2 * nl + 1] : vals[u][2 * nl + 1];
+            const float xi_wr = sc ? vals[u][2 * nl] : other[2 * nl];
+            const float xi_wi = sc ? vals[u][2 * nl + 1] : other[2 * nl + 1];
             if (n < g.N && !(g.dbg & 1))
               __stcs(orow + o_n[n], make_float2(xr_wr - xi_wi, xr_wi + xi_wr));
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&acc_empty[a]);
     }
   }
   tc_fence_before();
@@ -361,16 +412,12 @@ size_t tma_smem_bytes(TmaAbsorbGeom &g) {
   using Lay = TmaLayout<KSZ, MB, NM>;
   const int nslabs = (g.K + 31) / 32;
   const size_t fixed = 1024 + size_t(nslabs) * Lay::BROWS * 128 + 8 * (64 * MB + 64 + 32 * MB + KSZ) +
-                       8 * (2 * kMaxNSR + 2 * kMaxNSL + 4) + 16;
+                       8 * (2 * kMaxNSR + 2 * kMaxNSL + 8) + 16;
   const size_t budget = size_t(227) * 1024;
-  g.nsl = 2;
-  g.nsr = int((budget - fixed) / Lay::STAGE) - g.nsl;
+  const int total = int((budget - fixed) / Lay::STAGE);
+  g.nsl = total >= 11 ? 4 : 3;
+  g.nsr = total - g.nsl;
   if (g.nsr > kMaxNSR) g.nsr = kMaxNSR;
-  if (g.nsr >= 8 && g.nsl < 3) {  // spare room: a third lo plane
-    g.nsl = 3;
-    g.nsr = int((budget - fixed) / Lay::STAGE) - g.nsl;
-    if (g.nsr > kMaxNSR) g.nsr = kMaxNSR;
-  }
   return fixed + size_t(g.nsr + g.nsl) * Lay::STAGE;
 }
 
@@ -397,7 +444,12 @@ cudaError_t launch_tma_impl(const TmaAbsorbGeom &g, const BatchPtrs &p, cudaStre
   auto kern = k_absorb_tma<KSZ, MB, NM, GATHER>;
   TmaAbsorbGeom gl = g;
   const size_t smem = tma_smem_bytes<KSZ, MB, NM>(gl);
-  if (gl.nsr < (GATHER ? kLag + 1 : 2)) return cudaErrorNotSupported;
+  if (gl.nsr < (GATHER ? 4 : 2)) return cudaErrorNotSupported;
+  gl.lag = gl.nsr - 3 < kMaxLag ? gl.nsr - 3 : kMaxLag;
+  static const char *env_lag = std::getenv("STN_TMA_LAG");  // experiments
+  if (env_lag && std::atoi(env_lag) >= 1 && std::atoi(env_lag) <= gl.nsr - 2 &&
+      std::atoi(env_lag) <= kMaxLag)
+    gl.lag = std::atoi(env_lag);
   static const int dbg = std::getenv("STN_TMA_DBG") ? std::atoi(std::getenv("STN_TMA_DBG")) : 0;
   gl.dbg = dbg;  // experiments: 1 no stores, 2 no MMAs, 4 no lo conversion
   if (dbg & 8) {  // experiments (wrong results): box order d0, M runs, K runs
@@ -601,9 +653,10 @@ bool build_tma_absorb(const std::vector<std::pair<int, int>> &kbits,
 
 cudaError_t launch_absorb_tma(const TmaAbsorbGeom &g, const BatchPtrs &p, cudaStream_t stream) {
   const int ksz = 1 << g.kstage, mb = 1 << g.mbl;
-  // default loader: cp.async gather; STN_ABSORB_LOADER=tma selects the TMA box loader
-  static const char *ld = std::getenv("STN_ABSORB_LOADER");
-  const bool use_tma = g.tma_ok && ld && std::strcmp(ld, "tma") == 0;
+  // loader: one TMA box per stage where the geometry allows it (measured faster), else the
+  // cp.async gather; STN_ABSORB_LOADER=gather forces the gather (experiments)
+  const char *ld = std::getenv("STN_ABSORB_LOADER");
+  const bool use_tma = g.tma_ok && !(ld && std::strcmp(ld, "gather") == 0);
 #define STN_TMA(KSZV, MBV, NMV)                                              \
   if (ksz == KSZV && mb == MBV && g.nm == NMV)                               \
     return use_tma ? launch_tma_impl<KSZV, MBV, NMV, false>(g, p, stream)    \

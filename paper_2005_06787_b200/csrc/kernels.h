@@ -178,7 +178,7 @@ struct TmaAbsorbGeom {
   int tma_ok;                           // the box loader applies (X bits 0..3 in M, <= 5 dims)
   int64_t n_tiles;
   int K, N, kstage, mbl, nm, spt;       // stage K bits, log2 M blocks, N_mma, stages/tile
-  int nsr, nsl;                         // ring depths (set at launch from the smem budget)
+  int nsr, nsl, lag;                    // ring depths, loads in flight (set at launch)
   int dbg;
   int64_t o_m_off[256];                 // O offset of tile-local m
   int64_t w_k_off[64];                  // W offset of k (k bits in ascending X position)

@@ -595,12 +595,20 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     // FAST mode, K x N >= 2^STN_MMA_MIN_BITS: tensor-core direct absorb
     const char *mmin = std::getenv("STN_MMA_MIN_BITS");
     const int mma_min = mmin ? std::atoi(mmin) : 10;
-    // FAST mode, K x N >= 2^STN_TMA_MIN_BITS: TMA-fed tensor-core absorb
+    // FAST mode: the gather/TMA-fed tensor-core absorb where the SIMT streams are weak --
+    // no or short identity run of low bits (L <= 2, measured on B200: the tensor-core
+    // kernel streams at 3-4 TB/s, the SIMT kernels at 1.3-3 TB/s there) and 64 x 64
+    // W's -- while long identity runs stay on the SIMT direct kernel (6+ TB/s).
+    // STN_TMA_MIN_BITS=<bits> (experiments) forces it for every K x N >= 2^bits.
     const char *tmin = std::getenv("STN_TMA_MIN_BITS");
-    const int tma_min = tmin ? std::atoi(tmin) : 99;  // off until it beats the SIMT paths
-    if (!exact && sp.tg && int(sp.kbits.size() + sp.nbits.size()) >= tma_min) {
-      sp.kern = Kern::AbsorbTma;
-      return;
+    if (!exact && sp.tg) {
+      const int kn = int(sp.kbits.size() + sp.nbits.size());
+      const bool pick = tmin ? kn >= std::atoi(tmin)
+                             : (!sp.direct_ok || sp.dg.L <= 2 || kn >= 12);
+      if (pick) {
+        sp.kern = Kern::AbsorbTma;
+        return;
+      }
     }
     if (!exact && sp.direct_ok && stn::mma_absorb_supported(sp.dg) &&
         sp.dg.kb + sp.dg.nb >= mma_min) {

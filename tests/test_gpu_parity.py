@@ -268,3 +268,25 @@ def test_tensor_core_absorbs_run_and_meet_tolerance():
     assert len(tc) >= 2, rows
     truth, tol = truth_and_tolerance(name, int(asg[0]), vals[0])
     assert rel_err(got, truth) <= tol
+
+
+@pytest.mark.parametrize("loader", ["tma", "gather"])
+def test_tma_gather_absorb_every_eligible_step(loader, monkeypatch):
+    """Forces the gather/TMA-fed tcgen05 absorb (absorb_tma.cu) onto every cfg2 stem step
+    it can take (K x N >= 64), with either loader; the slice stays within tolerance of
+    the fp64 truth and the kernel really ran (absorb_tc-class steps with K <= 32)."""
+    from paper_2005_06787_b200 import build_branch_cache, run_subtask
+    monkeypatch.setenv("STN_TMA_MIN_BITS", "6")
+    monkeypatch.setenv("STN_ABSORB_LOADER", loader)
+    name = "cfg2_grid5x6_m16"
+    asg, vals, _, _, _ = read_ref(name, "single")
+    plan = load(name, "single", "fast")
+    plan.set_profiling(True)
+    cache = build_branch_cache(plan)
+    plan.reset_profile()
+    got = run_subtask(plan, int(asg[0]), cache).value
+    rows = plan.get_step_profile()
+    tc = [r for r in rows if r["kernel"] == "absorb_tc"]
+    assert len(tc) >= 10, rows
+    truth, tol = truth_and_tolerance(name, int(asg[0]), vals[0])
+    assert rel_err(got, truth) <= tol
