@@ -409,8 +409,16 @@ size_t gemm_tc_workspace_bytes(const GemmShape &s, const BatchPtrs &p) {
   return size_t(2) * 4 * (nbA * size_t(s.M) * 2 * s.K + nbB * size_t(4) * s.N * s.K);
 }
 
+void gemm_tc_a_planes(const GemmShape &s, const BatchPtrs &p, void *workspace, float **hi,
+                      float **lo) {
+  const int64_t nbA = (p.a_bs ? p.nbatch : 1) * s.D;
+  *hi = static_cast<float *>(workspace);
+  *lo = *hi + size_t(s.M) * 2 * s.K * nbA;
+}
+
 cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspace,
-                           size_t workspace_bytes, cudaStream_t stream, cudaEvent_t *gemm_events) {
+                           size_t workspace_bytes, cudaStream_t stream, cudaEvent_t *gemm_events,
+                           bool a_presplit) {
   if (!gemm_tc_supported(s)) return cudaErrorNotSupported;
   const int64_t nbA = (p.a_bs ? p.nbatch : 1) * s.D;
   const int64_t nbB = (p.b_bs ? p.nbatch : 1) * s.D;
@@ -422,7 +430,7 @@ cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspa
   float *alo = ahi + a_plane * nbA;
   float *bhi = alo + a_plane * nbA;
   float *blo = bhi + b_plane * nbB;
-  {
+  if (!a_presplit) {
     const int64_t total = int64_t(a_plane) * nbA;
     int64_t blocks = (total / 4 + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;

@@ -191,6 +191,23 @@ cudaError_t launch_absorb_tma(const TmaAbsorbGeom &g, const BatchPtrs &p, cudaSt
 // Tiled bond-2 bit permutation (the absorb tile machinery with K = N = 0).
 cudaError_t launch_bitperm(const AbsorbGeom &g, const void *in, void *out, int64_t in_bs,
                            int64_t out_bs, int nbatch, cudaStream_t stream);
+// Tiled bond-2 bit permutation (kernels_perm.cu): one CTA per tile of 2^tb complex
+// elements whose bits hold the lowest input and the lowest output bits. Tile-local input
+// index li (tile bits in ascending input position) and output index lo (ascending output
+// position) map to offsets through two 64-entry halves; bases[2t], bases[2t+1] are the
+// input / output offsets of tile t (device table, built at plan creation).
+struct PermTileGeom {
+  int tb;
+  int64_t n_tiles;
+  int64_t in_off[2][64];     // input offset of li bits [0,6) / [6,12)
+  int64_t out_off[2][64];    // output offset of lo bits [0,6) / [6,12)
+  uint16_t li_of_lo[2][64];  // li of lo bits [0,6) / [6,12)
+};
+bool build_perm_tiles(const std::vector<int> &perm, PermTileGeom &g, std::vector<int64_t> &bases);
+// out_lo != nullptr: write the TF32 hi (out) / lo (out_lo) planes of the permuted tensor.
+cudaError_t launch_perm_tiles(const PermTileGeom &g, const int64_t *bases, const void *in,
+                              void *out, int64_t in_bs, int64_t out_bs, int nbatch,
+                              cudaStream_t stream, void *out_lo = nullptr);
 // Split-K reduction (small output, long K; FAST mode). Pow2 geometries, out_size <= 256.
 // The output factorises into A rows (M) x B columns (N); o_mn[o] = m | n << 16.
 struct DotTables {
@@ -220,9 +237,14 @@ cudaError_t launch_sum_ordered(const double *per_slice, uint64_t n_slices, int64
 // N % 128 == 0, K % 32 == 0 (complex elements); returns cudaErrorNotSupported
 // otherwise so the caller can pick another kernel.
 // gemm_events (optional, 2 events) bracket the GEMM kernel alone (no pre-pass).
+// a_presplit: the workspace already holds A's hi / lo planes (a fused permute-split wrote
+// them; see gemm_tc_a_planes), so the A pre-pass is skipped.
 cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspace,
                            size_t workspace_bytes, cudaStream_t stream,
-                           cudaEvent_t *gemm_events = nullptr);
+                           cudaEvent_t *gemm_events = nullptr, bool a_presplit = false);
+// A hi / lo plane pointers inside the workspace (float offsets of the planes).
+void gemm_tc_a_planes(const GemmShape &s, const BatchPtrs &p, void *workspace, float **hi,
+                      float **lo);
 size_t gemm_tc_workspace_bytes(const GemmShape &s, const BatchPtrs &p);
 bool gemm_tc_supported(const GemmShape &s);
 

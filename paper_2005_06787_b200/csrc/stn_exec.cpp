@@ -142,8 +142,12 @@ struct StepPlan {
   bool a_id = true, b_id = true, c_id = true;
   stn::StridedGeom pa{}, pb{}, pc{};
   bool pa_tiled = false, pb_tiled = false, pc_tiled = false;  // bond-2 tiled permutes
+  stn::PermTileGeom pat{}, pbt{}, pct{};                         // high-occupancy tile permutes
+  std::shared_ptr<DevBuf> pa_bases, pb_bases, pc_bases;
   stn::AbsorbGeom pag{}, pbg{}, pcg{};
   stn::GemmShape gs{};
+  bool gemm_swap = false;            // operands exchanged: C^T = B^T A^T
+  std::vector<int> gl, gr, go;       // GEMM operand A / B permutations, product -> output
   int64_t lsize = 0, rsize = 0, osize = 0;
   // split-K dot tables (device)
   std::shared_ptr<DevBuf> dot_buf, dot_mn;
@@ -693,21 +697,65 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
   }
   // dense GEMM path: materialise [D|M|K], [D|K|N], run GEMM, permute [D|M|N]
   if (d.M >= 8 && d.N >= 8 && d.K >= 8 && d.mults >= (uint64_t(1) << 18)) {
-    std::vector<int> prod_dims(d.orank);
-    for (int i = 0; i < d.orank; ++i) prod_dims[sp.operm[i]] = sp.out_dims[i];
-    sp.a_id = is_identity(sp.lperm);
-    sp.b_id = is_identity(sp.rperm);
-    sp.c_id = is_identity(sp.operm);
-    fill_permute(sp.pa, ldims, sp.lperm);
-    fill_permute(sp.pb, rdims, sp.rperm);
-    fill_permute(sp.pc, prod_dims, sp.operm);
-    if (single) {
-      sp.pa_tiled = !sp.a_id && build_bitperm(ldims, sp.lperm, sp.pag);
-      sp.pb_tiled = !sp.b_id && build_bitperm(rdims, sp.rperm, sp.pbg);
-      sp.pc_tiled = !sp.c_id && build_bitperm(prod_dims, sp.operm, sp.pcg);
-    }
     sp.gs = {d.D, d.M, d.N, d.K};
-    sp.kern = (single && !exact && stn::gemm_tc_supported(sp.gs)) ? Kern::GemmTc : Kern::GemmSimt;
+    const bool tc = single && !exact && stn::gemm_tc_supported(sp.gs);
+    sp.kern = tc ? Kern::GemmTc : Kern::GemmSimt;
+    // tcgen05 GEMM: the operand it expands (B -> 2N x 2K real, hi + lo) should be the
+    // small one; with a larger rhs compute C^T = B^T A^T ([D|N|K] x [D|K|M] -> [D|N|M])
+    sp.gemm_swap = false;
+    if (tc && sp.rsize > sp.lsize) {
+      const stn::GemmShape t{d.D, d.N, d.M, d.K};
+      if (stn::gemm_tc_supported(t)) {
+        sp.gemm_swap = true;
+        sp.gs = t;
+      }
+    }
+    const int nd = d.nd, nm = d.nm, nk = d.nk, nn = d.nn;
+    if (!sp.gemm_swap) {
+      sp.gl = sp.lperm;
+      sp.gr = sp.rperm;
+      sp.go = sp.operm;
+    } else {
+      sp.gl.assign(sp.rperm.begin(), sp.rperm.begin() + nd);  // A' = rhs as [D|N|K]
+      sp.gl.insert(sp.gl.end(), sp.rperm.begin() + nd + nk, sp.rperm.end());
+      sp.gl.insert(sp.gl.end(), sp.rperm.begin() + nd, sp.rperm.begin() + nd + nk);
+      sp.gr.assign(sp.lperm.begin(), sp.lperm.begin() + nd);  // B' = lhs as [D|K|M]
+      sp.gr.insert(sp.gr.end(), sp.lperm.begin() + nd + nm, sp.lperm.end());
+      sp.gr.insert(sp.gr.end(), sp.lperm.begin() + nd, sp.lperm.begin() + nd + nm);
+      sp.go.resize(sp.operm.size());  // product axes [D|M|N] -> [D|N|M]
+      for (size_t i = 0; i < sp.operm.size(); ++i) {
+        const int p = sp.operm[i];
+        sp.go[i] = p < nd ? p : (p < nd + nm ? p + nn : p - nm);
+      }
+    }
+    const std::vector<int> &adims = sp.gemm_swap ? rdims : ldims;
+    const std::vector<int> &bdims = sp.gemm_swap ? ldims : rdims;
+    std::vector<int> prod_dims(d.orank);
+    for (int i = 0; i < d.orank; ++i) prod_dims[sp.go[i]] = sp.out_dims[i];
+    sp.a_id = is_identity(sp.gl);
+    sp.b_id = is_identity(sp.gr);
+    sp.c_id = is_identity(sp.go);
+    fill_permute(sp.pa, adims, sp.gl);
+    fill_permute(sp.pb, bdims, sp.gr);
+    fill_permute(sp.pc, prod_dims, sp.go);
+    if (single) {
+      sp.pa_tiled = !sp.a_id && build_bitperm(adims, sp.gl, sp.pag);
+      sp.pb_tiled = !sp.b_id && build_bitperm(bdims, sp.gr, sp.pbg);
+      sp.pc_tiled = !sp.c_id && build_bitperm(prod_dims, sp.go, sp.pcg);
+      auto tiles = [&](bool id, const std::vector<int> &dims, const std::vector<int> &perm,
+                       stn::PermTileGeom &g, std::shared_ptr<DevBuf> &buf) {
+        if (id) return;
+        for (int x : dims)
+          if (x != 2) return;
+        std::vector<int64_t> bases;
+        if (!stn::build_perm_tiles(perm, g, bases)) return;
+        buf = std::make_shared<DevBuf>();
+        buf->upload(bases);
+      };
+      tiles(sp.a_id, adims, sp.gl, sp.pat, sp.pa_bases);
+      tiles(sp.b_id, bdims, sp.gr, sp.pbt, sp.pb_bases);
+      tiles(sp.c_id, prod_dims, sp.go, sp.pct, sp.pc_bases);
+    }
   }
 }
 
@@ -1163,8 +1211,8 @@ void build_program(stn_plan &P, Program &prog, int which /*0 build, 1 cache, 2 n
     const StepPlan &sp = P.steps[prog.ops[k].step];
     if (prog.ops[k].sweep >= 0) continue;
     if (sp.kern != Kern::GemmSimt && sp.kern != Kern::GemmTc) continue;
-    if (!sp.a_id) scr[k][0] = new_item(sp.lsize, int64_t(k), int64_t(k));
-    if (!sp.b_id) scr[k][1] = new_item(sp.rsize, int64_t(k), int64_t(k));
+    if (!sp.a_id) scr[k][0] = new_item(sp.gemm_swap ? sp.rsize : sp.lsize, int64_t(k), int64_t(k));
+    if (!sp.b_id) scr[k][1] = new_item(sp.gemm_swap ? sp.lsize : sp.rsize, int64_t(k), int64_t(k));
     if (!sp.c_id) scr[k][2] = new_item(sp.osize, int64_t(k), int64_t(k));
   }
   // liveness allocation: biggest first, lowest non-conflicting offset
@@ -1728,38 +1776,68 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
     }
     case Kern::GemmSimt:
     case Kern::GemmTc: {
-      const void *ga = a.ptr, *gb = b.ptr;
-      int64_t ga_bs = a.bs, gb_bs = b.bs;
-      if (!sp.a_id) {
+      const Resolved &ra = sp.gemm_swap ? b : a, &rb = sp.gemm_swap ? a : b;
+      const int64_t asize = sp.gemm_swap ? sp.rsize : sp.lsize;
+      const int64_t bsize = sp.gemm_swap ? sp.lsize : sp.rsize;
+      const void *ga = ra.ptr, *gb = rb.ptr;
+      int64_t ga_bs = ra.bs, gb_bs = rb.bs;
+      // tcgen05 GEMM with a permuted A: the tile permute writes A's TF32 hi / lo planes
+      // straight into the GEMM workspace (one pass instead of permute + split)
+      const bool a_fused = sp.kern == Kern::GemmTc && !sp.a_id && sp.pa_bases &&
+                           stn::gemm_tc_supported(sp.gs);
+      if (a_fused) {
+        stn::BatchPtrs pp{nullptr, rb.ptr, nullptr, asize, rb.bs, 0, nb};
+        size_t ws = stn::gemm_tc_workspace_bytes(sp.gs, pp);
+        P.tc_workspace.reserve(std::max<size_t>(ws, 16));
+        float *hi, *lo;
+        stn::gemm_tc_a_planes(sp.gs, pp, P.tc_workspace.ptr, &hi, &lo);
+        cuda_check(stn::launch_perm_tiles(sp.pat, sp.pa_bases->as<int64_t>(), ra.ptr, hi, ra.bs,
+                                          asize, nb, st, lo),
+                   "tile permute + split");
+        prof.done(STN_KERNEL_PERMUTE, (es + 2 * es) * asize * nb, 0);
+        ga = nullptr;
+        ga_bs = asize;
+      } else if (!sp.a_id) {
         void *dst = elem_ptr(P, P.arena.ptr, op.scr_a * nb);
-        if (sp.pa_tiled)
-          cuda_check(stn::launch_bitperm(sp.pag, a.ptr, dst, a.bs, sp.lsize, nb, st), "bitperm");
+        if (sp.pa_bases)
+          cuda_check(stn::launch_perm_tiles(sp.pat, sp.pa_bases->as<int64_t>(), ra.ptr, dst,
+                                            ra.bs, asize, nb, st),
+                     "tile permute");
+        else if (sp.pa_tiled)
+          cuda_check(stn::launch_bitperm(sp.pag, ra.ptr, dst, ra.bs, asize, nb, st), "bitperm");
         else
-          cuda_check(stn::launch_permute<R>(sp.pa, a.ptr, dst, a.bs, sp.lsize, nb, st), "permute");
-        prof.done(STN_KERNEL_PERMUTE, 2 * es * sp.lsize * nb, 0);
+          cuda_check(stn::launch_permute<R>(sp.pa, ra.ptr, dst, ra.bs, asize, nb, st), "permute");
+        prof.done(STN_KERNEL_PERMUTE, 2 * es * asize * nb, 0);
         ga = dst;
-        ga_bs = sp.lsize;
+        ga_bs = asize;
       }
       if (!sp.b_id) {
         void *dst = elem_ptr(P, P.arena.ptr, op.scr_b * nb);
-        if (sp.pb_tiled)
-          cuda_check(stn::launch_bitperm(sp.pbg, b.ptr, dst, b.bs, sp.rsize, nb, st), "bitperm");
+        if (sp.pb_bases)
+          cuda_check(stn::launch_perm_tiles(sp.pbt, sp.pb_bases->as<int64_t>(), rb.ptr, dst,
+                                            rb.bs, bsize, nb, st),
+                     "tile permute");
+        else if (sp.pb_tiled)
+          cuda_check(stn::launch_bitperm(sp.pbg, rb.ptr, dst, rb.bs, bsize, nb, st), "bitperm");
         else
-          cuda_check(stn::launch_permute<R>(sp.pb, b.ptr, dst, b.bs, sp.rsize, nb, st), "permute");
-        prof.done(STN_KERNEL_PERMUTE, 2 * es * sp.rsize * nb, 0);
+          cuda_check(stn::launch_permute<R>(sp.pb, rb.ptr, dst, rb.bs, bsize, nb, st), "permute");
+        prof.done(STN_KERNEL_PERMUTE, 2 * es * bsize * nb, 0);
         gb = dst;
-        gb_bs = sp.rsize;
+        gb_bs = bsize;
       }
       void *gc = sp.c_id ? out : elem_ptr(P, P.arena.ptr, op.scr_c * nb);
       int64_t gc_bs = sp.c_id ? o.bs : sp.osize;
       stn::BatchPtrs p{ga, gb, gc, ga_bs, gb_bs, gc_bs, nb};
-      const double gbytes = es * (sp.lsize * (ga_bs ? nb : 1) + sp.rsize * (gb_bs ? nb : 1) +
+      const double gbytes = es * (asize * (ga_bs ? nb : 1) + bsize * (gb_bs ? nb : 1) +
                                   double(sp.osize) * nb);
       bool done = false;
       if (sp.kern == Kern::GemmTc) {
         size_t ws = stn::gemm_tc_workspace_bytes(sp.gs, p);
         P.tc_workspace.reserve(std::max<size_t>(ws, 16));
-        cudaError_t e = stn::launch_gemm_tc(sp.gs, p, P.tc_workspace.ptr, ws, st);
+        cudaError_t e =
+            stn::launch_gemm_tc(sp.gs, p, P.tc_workspace.ptr, ws, st, nullptr, a_fused);
+        require(!a_fused || e == cudaSuccess, STN_ERR_CUDA,
+                std::string("tcgen05 gemm (pre-split A): ") + cudaGetErrorString(e));
         if (e == cudaSuccess) {
           done = true;
           prof.done(STN_KERNEL_GEMM_TC, gbytes, flops);
@@ -1774,7 +1852,11 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
         prof.done(STN_KERNEL_GEMM_SIMT, gbytes, flops);
       }
       if (!sp.c_id) {
-        if (sp.pc_tiled)
+        if (sp.pc_bases)
+          cuda_check(stn::launch_perm_tiles(sp.pct, sp.pc_bases->as<int64_t>(), gc, out, sp.osize,
+                                            o.bs, nb, st),
+                     "tile permute");
+        else if (sp.pc_tiled)
           cuda_check(stn::launch_bitperm(sp.pcg, gc, out, sp.osize, o.bs, nb, st), "bitperm");
         else
           cuda_check(stn::launch_permute<R>(sp.pc, gc, out, sp.osize, o.bs, nb, st), "permute");
@@ -2311,6 +2393,17 @@ int stn_selftest_bitperm(int32_t log2_elems, const int32_t *perm, int32_t reps, 
     }
     stn::AbsorbGeom g;
     require(build_bitperm(dims, axis_perm, g), STN_ERR_INVALID_ARGUMENT, "no tile geometry");
+    // the executor's permute: the high-occupancy tile permute where it applies
+    stn::PermTileGeom tg;
+    std::vector<int64_t> tbases;
+    DevBuf tb_dev;
+    const bool tiles = std::getenv("STN_BITPERM_LEGACY") == nullptr &&
+                       stn::build_perm_tiles(axis_perm, tg, tbases);
+    if (tiles) tb_dev.upload(tbases);
+    auto launch = [&](const void *src, void *dst, cudaStream_t s) {
+      return tiles ? stn::launch_perm_tiles(tg, tb_dev.as<int64_t>(), src, dst, 0, 0, 1, s)
+                   : stn::launch_bitperm(g, src, dst, 0, 0, 1, s);
+    };
     const size_t n = size_t(1) << r, bytes = n * 8;
     DevBuf in, out, ref;
     in.reserve(bytes);
@@ -2323,7 +2416,7 @@ int stn_selftest_bitperm(int32_t log2_elems, const int32_t *perm, int32_t reps, 
     cudaEvent_t e0, e1;
     cuda_check(cudaEventCreate(&e0), "event");
     cuda_check(cudaEventCreate(&e1), "event");
-    cuda_check(stn::launch_bitperm(g, in.ptr, out.ptr, 0, 0, 1, st), "bitperm");
+    cuda_check(launch(in.ptr, out.ptr, st), "bitperm");
     cuda_check(cudaStreamSynchronize(st), "sync");
     std::vector<uint32_t> got(2 * n);
     cuda_check(cudaMemcpy(got.data(), out.ptr, bytes, cudaMemcpyDeviceToHost), "download");
@@ -2336,8 +2429,7 @@ int stn_selftest_bitperm(int32_t log2_elems, const int32_t *perm, int32_t reps, 
     }
     *correct = ok ? 1 : 0;
     cuda_check(cudaEventRecord(e0, st), "event");
-    for (int i = 0; i < reps; ++i)
-      cuda_check(stn::launch_bitperm(g, in.ptr, out.ptr, 0, 0, 1, st), "bitperm");
+    for (int i = 0; i < reps; ++i) cuda_check(launch(in.ptr, out.ptr, st), "bitperm");
     cuda_check(cudaEventRecord(e1, st), "event");
     cuda_check(cudaEventSynchronize(e1), "sync");
     float ms = 0;

@@ -1,0 +1,4 @@
+rm -rf gpurun_out; mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_kernels.py -x -q -s -k bitperm 2>&1 | grep -E "^bitperm|^\.bitperm|passed|failed"
+timeout 300 python scripts/step_profile.py cfg2 > gpurun_out/r45_prof.txt 2>&1; head -3 gpurun_out/r45_prof.txt; grep -E "^ (746|736|737|738|637) " gpurun_out/r45_prof.txt
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
