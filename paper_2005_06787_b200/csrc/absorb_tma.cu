@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -66,10 +67,18 @@ struct TmaLayout {
   static constexpr int STAGE = MB * KSZ * 512;       // bytes of one raw (or lo) stage
   static constexpr int LBO = KSZ * 128;              // MN-atom stride (32 m-floats x KSZ rows)
   static constexpr int BROWS = 2 * NM;               // B'' rows: hi then lo
-  static constexpr int ACC = MB * 2 * NM;            // TMEM columns of one accumulator buffer
+  static constexpr int ACC = MB * NM;                // TMEM columns of one accumulator buffer
   static constexpr int NACC = 4 * ACC <= 512 ? 4 : 2;  // accumulator buffers
   static constexpr int TMEM_COLS = NACC * ACC <= 32 ? 32 : (NACC * ACC <= 64 ? 64 : (NACC * ACC <= 128 ? 128 : (NACC * ACC <= 256 ? 256 : 512)));
 };
+
+// Experiments (dbg & 32): cycles spent waiting on each barrier kind, CTA 0, printed at exit.
+#define TW(slot, call)                                                 \
+  do {                                                                 \
+    const long long t0_ = (g.dbg & 32) ? clock64() : 0;                \
+    call;                                                              \
+    if (g.dbg & 32) wait_cyc[slot] += clock64() - t0_;                 \
+  } while (0)
 
 // Position in a ring of mbarrier-guarded slots: slot index and the parity of its phase.
 struct RingPos {
@@ -101,13 +110,13 @@ __device__ __forceinline__ uint32_t kmajor_off(int row, int col, int rows) {
 
 template <bool GATHER>
 struct Roles {
-  // GATHER: warp 0 MMA, warps 1-8 loaders (cp.async gather + lo), warps 9-12 epilogue.
-  // TMA:    warp 0 TMA, warp 1 MMA, warps 2-5 converters (lo), warps 6-9 epilogue.
-  static constexpr int THREADS = GATHER ? 416 : 320;
+  // GATHER: warp 0 MMA, warps 1-8 loaders (cp.async gather + lo), warps 9-16 epilogue.
+  // TMA:    warp 0 TMA, warp 1 MMA, warps 2-5 converters (lo), warps 6-13 epilogue.
+  static constexpr int THREADS = GATHER ? 544 : 448;
   static constexpr int MMA_WARP = GATHER ? 0 : 1;
   static constexpr int LOAD_WARP0 = GATHER ? 1 : 2;
   static constexpr int LOAD_WARPS = GATHER ? 8 : 4;
-  static constexpr int EPI_WARP0 = GATHER ? 9 : 6;
+  static constexpr int EPI_WARP0 = GATHER ? 9 : 6;  // 8 epilogue warps: 2 per TMEM quadrant
 };
 
 template <int KSZ, int MB, int NM, bool GATHER>
@@ -137,6 +146,8 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
 
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int spt = g.spt;  // stages per tile
+  long long wait_cyc[7] = {0, 0, 0, 0, 0, 0, 0};
+  const long long t_start = clock64();
 
   // ---- setup: B'' (K-major, rows 2n+t: hi rows then lo rows), offset tables ----
   for (int i = tid; i < nslabs * Lay::BROWS * 32; i += NT) reinterpret_cast<float *>(bmat)[i] = 0.f;
@@ -169,7 +180,7 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
     }
     for (int a = 0; a < Lay::NACC; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], kEpiWarps);
+      mbar_init(&acc_empty[a], 2 * kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (!GATHER) prefetch_tensormap(&map);
@@ -198,7 +209,7 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
       for (int64_t t = t_begin; t < t_end; ++t, xt = ((xt | ~g.outer_x_mask) + 1) & g.outer_x_mask) {
         for (int j = 0; j < spt; ++j, rs.next(nsr)) {
           const int s = rs.idx;
-          mbar_wait(&empty[s], rs.phase ^ 1);
+          TW(0, mbar_wait(&empty[s], rs.phase ^ 1));
           const uint64_t full_idx = xt | pdep64(uint64_t(j), g.loopk_x_mask);
           int c[5] = {0, 0, 0, 0, 0};
 #pragma unroll
@@ -216,35 +227,37 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
     if (lane == 0) {
       const uint32_t b_base = smem_u32(bmat);
       const uint32_t raw_base = smem_u32(raw), lo_base = smem_u32(lo);
-      constexpr uint32_t IDESC1 = idesc_tf32(2 * NM, true);
-      constexpr uint32_t IDESC2 = idesc_tf32(NM, true);
+      constexpr uint32_t IDESC = idesc_tf32(NM, true);
       RingPos rs, rl;
       int i = 0;
       for (int64_t t = t_begin; t < t_end; ++t, ++i) {
         const int a = i % Lay::NACC;
-        mbar_wait(&acc_empty[a], ((i / Lay::NACC) & 1) ^ 1);
+        TW(1, mbar_wait(&acc_empty[a], ((i / Lay::NACC) & 1) ^ 1));
         tc_fence_after();
         const uint32_t acc_base = tmem + uint32_t(a * Lay::ACC);
         for (int j = 0; j < spt; ++j, rs.next(nsr), rl.next(nsl)) {
           const int s = rs.idx, l = rl.idx;
-          mbar_wait(&full[s], rs.phase);
-          mbar_wait(&lofull[l], rl.phase);
+          TW(2, mbar_wait(&full[s], rs.phase));
+          TW(3, mbar_wait(&lofull[l], rl.phase));
           tc_fence_after();
 #pragma unroll
           for (int q = 0; q < KSZ / 8; ++q) {
             const int kg = j * KSZ + q * 8;  // global k of this k-step
             const uint32_t boff = uint32_t((kg >> 5) * Lay::BROWS * 128 + (kg & 31) * 4);
             const uint64_t db = smem_desc(b_base + boff, 16, 1024, 2);
+            const uint64_t dbl = smem_desc(b_base + boff + NM * 128, 16, 1024, 2);
             const uint32_t acc_flag = (j == 0 && q == 0) ? 0u : 1u;
 #pragma unroll
             for (int b = 0; b < MB; ++b) {
               const uint32_t aoff = uint32_t(4 * b * Lay::LBO + q * 1024);
               const uint64_t dr = smem_desc(raw_base + s * Lay::STAGE + aoff, Lay::LBO, 512, 1);
               const uint64_t dl = smem_desc(lo_base + l * Lay::STAGE + aoff, Lay::LBO, 512, 1);
-              const uint32_t d = acc_base + uint32_t(b * 2 * NM);
+              const uint32_t d = acc_base + uint32_t(b * NM);
               if (g.dbg & 2) continue;
-              umma_tf32(d, dr, db, IDESC1, acc_flag);
-              umma_tf32(d + NM, dl, db, IDESC2, 1u);
+              // one fp32 accumulator: hi*hi, then the hi*lo and lo*hi corrections
+              umma_tf32(d, dr, db, IDESC, acc_flag);
+              umma_tf32(d, dr, dbl, IDESC, 1u);
+              umma_tf32(d, dl, db, IDESC, 1u);
             }
           }
           umma_commit(&empty[s]);
@@ -261,7 +274,7 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
     RingPos cs, cl;  // slot of the next stage to convert
     auto convert = [&]() {
       const int s = cs.idx, l = cl.idx;
-      mbar_wait(&loempty[l], cl.phase ^ 1);
+      TW(4, mbar_wait(&loempty[l], cl.phase ^ 1));
       const float4 *src = reinterpret_cast<const float4 *>(raw + s * Lay::STAGE);
       float4 *dst = reinterpret_cast<float4 *>(lo + l * Lay::STAGE);
       if (!(g.dbg & 4)) {
@@ -330,17 +343,19 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
       // ---------------- converters (TMA variant) ----------------
       for (int64_t t = t_begin; t < t_end; ++t)
         for (int j = 0; j < spt; ++j) {
-          mbar_wait(&full[cs.idx], cs.phase);
+          TW(5, mbar_wait(&full[cs.idx], cs.phase));
           convert();
         }
     }
   } else if (warp >= R::EPI_WARP0) {
     // ---------------- epilogue ----------------
-    // The tile's accumulator is read in batches of up to 4 16-column chunks (all loads of
-    // a batch in flight together); the TMEM buffer is handed back to the MMA thread as
-    // soon as the last batch is in registers, before the shuffles and stores.
-    constexpr int CH = MB * NM / 16, BATCH = CH < 4 ? CH : 4;
-    const int q4 = warp & 3;              // TMEM lane quadrant of this warp
+    // Two warps per TMEM lane quadrant take alternate 16-column chunks of the tile's
+    // accumulator (loaded in batches of up to 4, all in flight together); each warp hands
+    // the buffer back as soon as its last batch is in registers, before shuffles and stores.
+    constexpr int CH = MB * NM / 16;
+    constexpr int MINE = (CH + 1) / 2, BATCH = MINE < 4 ? MINE : 4;
+    const int q4 = warp & 3;                       // TMEM lane quadrant of this warp
+    const int half = (warp - R::EPI_WARP0) >> 2;   // which alternate chunks
     const int row = 32 * q4 + lane;       // real row 2m + s within a 128-row block
     const int sc = row & 1;
     int i = 0;
@@ -348,36 +363,45 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
     for (int64_t t = t_begin; t < t_end;
          ++t, ++i, oo = ((oo | ~g.outer_o_mask) + 1) & g.outer_o_mask) {
       const int a = i % Lay::NACC;
-      mbar_wait(&acc_full[a], (i / Lay::NACC) & 1);
+      TW(6, mbar_wait(&acc_full[a], (i / Lay::NACC) & 1));
       tc_fence_after();
       const int64_t o_outer = int64_t(oo);
       const uint32_t tq = tmem + (uint32_t(32 * q4) << 16) + uint32_t(a * Lay::ACC);
+      if (half * 1 >= CH) {  // nothing for this warp (single-chunk tiles)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[a]);
+        continue;
+      }
 #pragma unroll
-      for (int c0 = 0; c0 < CH; c0 += BATCH) {
+      for (int j0 = 0; j0 < MINE; j0 += BATCH) {
         float vals[BATCH][16];
         {
-          uint32_t vm[BATCH][16], vc[BATCH][16];
+          uint32_t vm[BATCH][16];
 #pragma unroll
           for (int u = 0; u < BATCH; ++u) {
-            const int c = c0 + u, b = c / (NM / 16), cc = (c % (NM / 16)) * 16;
-            tmem_ld16(tq + uint32_t(b * 2 * NM + cc), vm[u]);
-            tmem_ld16(tq + uint32_t(b * 2 * NM + NM + cc), vc[u]);
+            const int c = 2 * (j0 + u) + half;
+            if (c < CH) {
+              const int b = c / (NM / 16), cc = (c % (NM / 16)) * 16;
+              tmem_ld16(tq + uint32_t(b * NM + cc), vm[u]);
+            }
           }
           tmem_wait_ld();
 #pragma unroll
           for (int u = 0; u < BATCH; ++u)
 #pragma unroll
-            for (int q = 0; q < 16; ++q)
-              vals[u][q] = __uint_as_float(vm[u][q]) + __uint_as_float(vc[u][q]);
+            for (int q = 0; q < 16; ++q) vals[u][q] = __uint_as_float(vm[u][q]);
         }
-        if (c0 + BATCH >= CH) {  // all of this tile's TMEM is in registers
+        if (j0 + BATCH >= MINE) {  // all of this warp's TMEM share is in registers
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&acc_empty[a]);
         }
 #pragma unroll
         for (int u = 0; u < BATCH; ++u) {
-          const int c = c0 + u, b = c / (NM / 16), cc = (c % (NM / 16)) * 16;
+          const int c = 2 * (j0 + u) + half;
+          if (c >= CH) break;
+          const int b = c / (NM / 16), cc = (c % (NM / 16)) * 16;
           float2 *orow = O + o_outer + o_m[64 * b + (row >> 1)];
           float other[16];
 #pragma unroll
@@ -396,6 +420,13 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
         }
       }
     }
+  }
+  if ((g.dbg & 32) && blockIdx.x == 0 && lane == 0) {
+    const long long tt = clock64() - t_start;
+    printf("cta0 warp %2d: total %lld cyc, waits empty %lld acc_empty %lld full %lld lofull %lld "
+           "loempty %lld conv_full %lld acc_full %lld\n",
+           warp, tt, wait_cyc[0], wait_cyc[1], wait_cyc[2], wait_cyc[3], wait_cyc[4], wait_cyc[5],
+           wait_cyc[6]);
   }
   tc_fence_before();
   __syncthreads();

@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(256, 1) k_cpasync_planes(const char *X, char *
 // issues, waits, re-issues (the data is discarded).
 __global__ void __launch_bounds__(32, 1) k_tma_read(const __grid_constant__ CUtensorMap map,
                                                    int64_t nbox, int bytes, int NS, int d1n,
-                                                   int d2n, int d3n) {
+                                                   int d2n, int d3n, int bx1, int bx2, int bx3) {
   extern __shared__ __align__(1024) char sm[];
   __shared__ uint64_t full[16];
   if (threadIdx.x != 0) return;
@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(32, 1) k_tma_read(const __grid_constant__ CUte
   const int64_t b0 = nbox * blockIdx.x / gridDim.x, b1 = nbox * (blockIdx.x + 1) / gridDim.x;
   auto issue = [&](int64_t b, int s) {
     // box index -> coordinates of dims 1..3 (outer extents d1n, d2n, d3n boxes)
-    int c1 = int(b % d1n), c2 = int((b / d1n) % d2n), c3 = int(b / d1n / d2n);
+    // boxes iterate over dims 3 (fast) and 4; dims 1, 2 lie inside the box
+    int c1 = 0, c2 = 0, c3 = int(b % d3n) * bx3, c4 = int(b / d3n);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])),
                  "r"(bytes)
                  : "memory");
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(32, 1) k_tma_read(const __grid_constant__ CUte
         "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(su32(sm + s * bytes)),
         "l"(reinterpret_cast<uint64_t>(&map)), "r"(su32(&full[s])), "r"(0), "r"(c1), "r"(c2),
-        "r"(c3), "r"(0)
+        "r"(c3), "r"(c4)
         : "memory");
   };
   int g = 0;
@@ -254,11 +255,14 @@ int main() {
     };
     // 477-like: d0 = 32 floats (X bits 0..3), d1 = k bits 16,17 (4, stride 2^16 cx), d2 = k25
     // (2, stride 2^25 cx), d3 = m bits 4..15 (box 4 of 4096, stride 2^4 cx), d4 = m 18..24 etc.
+    // all boxes 16 KiB (dims 0-2 in the box), iterated over dims 3 and 4; X = 1 GiB
     Cfg cfgs[] = {
-        {"tma 5d 477-like, sw32", 1, {32, 4, 2, 4096, 128}, {1u << 19, 1u << 28, 128, 1u << 21}, {32, 4, 2, 4, 1}},
-        {"tma 5d 477-like, no swizzle", 0, {32, 4, 2, 4096, 128}, {1u << 19, 1u << 28, 128, 1u << 21}, {32, 4, 2, 4, 1}},
-        {"tma 5d contiguous rows", 0, {32, 4, 2, 4096, 128}, {128, 512, 1024, 1u << 21}, {32, 4, 2, 4, 1}},
-        {"tma 2d 128B x 128 rows contiguous", 0, {32, 1u << 23, 1, 1, 1}, {128, 1u << 30, 1u << 30, 1u << 30}, {32, 128, 1, 1, 1}},
+        {"planes 2KiB x 8 @512K", 0, {32, 16, 8, 1u << 8, 1u << 8}, {128, 1u << 19, 2048, 1u << 22}, {32, 16, 8, 1, 1}},
+        {"planes 2KiB x (4 @512K x 2 @256M)", 0, {32, 16, 4, 1u << 8, 1u << 7}, {128, 1u << 19, 2048, 1u << 21}, {32, 16, 4, 1, 1}},
+        {"planes 4KiB x 2 @256M", 0, {32, 32, 2, 1u << 17, 2}, {128, 1u << 28, 4096, 1u << 29}, {32, 32, 2, 1, 1}},
+        {"planes 4KiB x 2 @128M", 0, {32, 32, 2, 1u << 15, 4}, {128, 1u << 27, 4096, 1u << 28}, {32, 32, 2, 1, 1}},
+        {"planes 4KiB x 2 @64M", 0, {32, 32, 2, 1u << 14, 8}, {128, 1u << 26, 4096, 1u << 27}, {32, 32, 2, 1, 1}},
+        {"planes 8KiB x 2 @256M", 0, {32, 64, 2, 1u << 16, 2}, {128, 1u << 28, 8192, 1u << 29}, {32, 64, 2, 1, 1}},
     };
     for (auto &c : cfgs) {
       CUtensorMap map;
@@ -273,14 +277,14 @@ int main() {
       }
       const int bytes = int(c.box[0] * c.box[1] * c.box[2] * c.box[3] * c.box[4] * 4);
       // iterate over dims 3 (and 1, 2 beyond the box) with box-sized steps
-      const int d1n = int(c.dims[1] / c.box[1]), d2n = int(c.dims[2] / c.box[2]),
-                d3n = int(c.dims[3] / c.box[3]);
-      const int64_t nbox = int64_t(d1n) * d2n * d3n;
+      const int d1n = 1, d2n = 1, d3n = int(c.dims[3]);
+      const int64_t nbox = int64_t(c.dims[3]) * c.dims[4];
       for (int ns : {4, 8, 12}) {
         if (ns * bytes > 200 * 1024) continue;
         cudaEventRecord(e0);
         for (int rr = 0; rr < 5; ++rr)
-          k_tma_read<<<148, 32, ns * bytes>>>(map, nbox, bytes, ns, d1n, d2n, d3n);
+          k_tma_read<<<148, 32, ns * bytes>>>(map, nbox, bytes, ns, d1n, d2n, d3n, int(c.box[1]),
+                                              int(c.box[2]), int(c.box[3]));
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
