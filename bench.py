@@ -297,7 +297,19 @@ def main():
         achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    # DRAM bytes per launch of the dominant class from the committed ncu launch list
+    # (dram__bytes_read.sum + dram__bytes_write.sum, scripts/traffic_from_ncu.py), next
+    # to the algorithmic bytes per launch that `achieved` is computed from
     roof["traffic"] = None
+    roof["algorithmic_bytes_per_launch"] = d["bytes"] / d["launches"] if d["launches"] else None
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                         "r01_dram_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tcls = json.load(f).get("classes", {}).get(dom)
+        if tcls:
+            roof["traffic"] = tcls["bytes_per_launch"]
+            roof["traffic_source"] = "profiles/r01_dram_traffic.json (ncu, cfg2, 1 slice + cache build)"
     roof["kernel"] = dom
     roof["share_of_step"] = d["ms"] / step_ms_total if step_ms_total else None
     roof["launches_per_step"] = d["launches"] / args.steps

@@ -1,5 +1,5 @@
 // TMA-fed tensor-core absorb (FAST mode): the bond-2 stem step
-//   O[m, n] = sum_k X[m, k] * W[k, n]        (complex64, 8 <= K <= 64, N <= 64)
+//   O[m, n] = sum_k X[m, k] * W[k, n]        (complex64, 4 <= K <= 64, N <= 64)
 // for stems whose four lowest X bits are M bits.
 //
 // The index permutation is fused into the tile loads: one multi-dimensional TMA
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
           TW(3, mbar_wait(&lofull[l], rl.phase));
           tc_fence_after();
 #pragma unroll
-          for (int q = 0; q < KSZ / 8; ++q) {
+          for (int q = 0; q < (KSZ + 7) / 8; ++q) {
             const int kg = j * KSZ + q * 8;  // global k of this k-step
             const uint32_t boff = uint32_t((kg >> 5) * Lay::BROWS * 128 + (kg & 31) * 4);
             const uint64_t db = smem_desc(b_base + boff, 16, 1024, 2);
@@ -250,8 +250,11 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
 #pragma unroll
             for (int b = 0; b < MB; ++b) {
               const uint32_t aoff = uint32_t(4 * b * Lay::LBO + q * 1024);
-              const uint64_t dr = smem_desc(raw_base + s * Lay::STAGE + aoff, Lay::LBO, 512, 1);
-              const uint64_t dl = smem_desc(lo_base + l * Lay::STAGE + aoff, Lay::LBO, 512, 1);
+              // K = 4 stages hold one K atom: SBO = 0 makes the instruction's second atom
+              // repeat the first, against B rows k = 4..7 that are zero
+              constexpr uint32_t SBO = KSZ >= 8 ? 512 : 0;
+              const uint64_t dr = smem_desc(raw_base + s * Lay::STAGE + aoff, Lay::LBO, SBO, 1);
+              const uint64_t dl = smem_desc(lo_base + l * Lay::STAGE + aoff, Lay::LBO, SBO, 1);
               const uint32_t d = acc_base + uint32_t(b * NM);
               if (g.dbg & 2) continue;
               // one fp32 accumulator: hi*hi, then the hi*lo and lo*hi corrections
@@ -564,7 +567,7 @@ bool build_tma_absorb(const std::vector<std::pair<int, int>> &kbits,
                       const std::vector<std::pair<int, int>> &nbits, int xr, TmaAbsorbGeom &g) {
   std::memset(&g, 0, sizeof g);
   const int kb = int(kbits.size()), nb = int(nbits.size());
-  if (kb < 3 || kb > 6 || nb < 2 || nb > 6) return false;
+  if (kb < 2 || kb > 6 || nb < 2 || nb > 6) return false;
   // classes of X positions: 0 = outer M, 1 = tile M, 2 = stage K, 3 = loop K
   std::vector<int> cls(xr, -1), opos(xr, -1);
   for (auto &[xp, op] : mbits) {
@@ -579,6 +582,7 @@ bool build_tma_absorb(const std::vector<std::pair<int, int>> &kbits,
   const int nm = (2 << nb) < 16 ? 16 : (2 << nb);
   int mbl = 5 - kstage;  // log2 MB: 32 k x 64 m per stage
   while (mbl > 0 && (1 << mbl) * 2 * nm > 256) --mbl;
+  if (kstage + mbl < 3) return false;  // stages of >= 4 KiB (one 16-byte chunk per loader)
   const int tm = 6 + mbl;
   // tile M bits: the tm lowest M positions; stage K bits: the kstage lowest K positions
   int got = 0;
@@ -695,6 +699,7 @@ cudaError_t launch_absorb_tma(const TmaAbsorbGeom &g, const BatchPtrs &p, cudaSt
   STN_TMA(32, 1, 16) STN_TMA(32, 1, 32) STN_TMA(32, 1, 64) STN_TMA(32, 1, 128)
   STN_TMA(16, 2, 16) STN_TMA(16, 2, 32) STN_TMA(16, 2, 64) STN_TMA(16, 1, 128)
   STN_TMA(8, 4, 16) STN_TMA(8, 4, 32) STN_TMA(8, 2, 64) STN_TMA(8, 1, 128)
+  STN_TMA(4, 8, 16) STN_TMA(4, 4, 32) STN_TMA(4, 2, 64)
 #undef STN_TMA
   return cudaErrorNotSupported;
 }

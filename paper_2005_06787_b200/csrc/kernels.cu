@@ -117,6 +117,81 @@ __global__ void __launch_bounds__(256)
 // 64x64 output tile per CTA, 16-wide K steps, 4x4 outputs per thread; every
 // output accumulates k in ascending order.
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// "Outer" steps (kernels.h OuterGeom): both operands small, the output large
+// (e.g. the first stem step, a 2^11 x 2^14 -> 2^23 expansion with K = 2). The
+// operand offsets of an output index come from per-byte tables in shared memory
+// instead of a per-axis div/mod walk; the K sum runs in k_generic's order with
+// the same complex MAC, so results are bitwise those of k_generic.
+// ---------------------------------------------------------------------------
+template <class R, bool EXACT>
+__global__ void __launch_bounds__(256)
+    k_outer(const __grid_constant__ OuterGeom g, const BatchPtrs p) {
+  using T = cx_t<R>;
+  __shared__ int32_t ta[4][256], tb[4][256], ka[64], kb[64];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+    ta[i >> 8][i & 255] = g.ta[i >> 8][i & 255];
+    tb[i >> 8][i & 255] = g.tb[i >> 8][i & 255];
+  }
+  for (int i = threadIdx.x; i < g.nk; i += blockDim.x) {
+    ka[i] = g.ka[i];
+    kb[i] = g.kb[i];
+  }
+  __syncthreads();
+  const int b = blockIdx.y;
+  const T *A = static_cast<const T *>(p.a) + int64_t(b) * p.a_bs;
+  const T *B = static_cast<const T *>(p.b) + int64_t(b) * p.b_bs;
+  T *O = static_cast<T *>(p.out) + int64_t(b) * p.out_bs;
+  const int64_t n = int64_t(1) << g.obits;
+  // 8 consecutive outputs per thread: base offsets from the tables once, the three low
+  // output bits from register copies of the first table entries
+  int32_t la[8], lb[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    la[v] = ta[0][v];
+    lb[v] = tb[0][v];
+  }
+  for (int64_t o = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 8; o < n;
+       o += int64_t(gridDim.x) * blockDim.x * 8) {
+    const uint32_t ou = uint32_t(o);
+    const int32_t ao = ta[0][ou & 255] + ta[1][(ou >> 8) & 255] + ta[2][(ou >> 16) & 255] +
+                       ta[3][ou >> 24];
+    const int32_t bo = tb[0][ou & 255] + tb[1][(ou >> 8) & 255] + tb[2][(ou >> 16) & 255] +
+                       tb[3][ou >> 24];
+    T acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      acc[e].x = 0;
+      acc[e].y = 0;
+    }
+    for (int k = 0; k < g.nk; ++k) {
+      const T *ak = A + ao + ka[k];
+      const T *bk = B + bo + kb[k];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) cmac<EXACT>(acc[e], __ldg(ak + la[e]), __ldg(bk + lb[e]));
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) O[o + e] = acc[e];
+  }
+}
+
+}  // namespace
+
+template <class R>
+cudaError_t launch_outer(const OuterGeom &g, const BatchPtrs &p, bool exact, cudaStream_t stream) {
+  const int64_t groups = (int64_t(1) << g.obits) / 8;
+  dim3 grid(unsigned(grid_for(groups, 256, 148 * 16)), unsigned(p.nbatch));
+  if (exact)
+    k_outer<R, true><<<grid, 256, 0, stream>>>(g, p);
+  else
+    k_outer<R, false><<<grid, 256, 0, stream>>>(g, p);
+  return cudaGetLastError();
+}
+template cudaError_t launch_outer<float>(const OuterGeom &, const BatchPtrs &, bool, cudaStream_t);
+template cudaError_t launch_outer<double>(const OuterGeom &, const BatchPtrs &, bool, cudaStream_t);
+
+namespace {
+
 template <class R, bool EXACT>
 __global__ void __launch_bounds__(256)
     k_gemm_simt(const GemmShape s, const BatchPtrs p) {

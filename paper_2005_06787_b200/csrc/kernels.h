@@ -45,6 +45,18 @@ struct BatchPtrs {
   int nbatch;
 };
 
+// Small operands, large output (kernels.cu k_outer): output index bits -> operand
+// offsets through per-byte tables (4 bytes cover <= 32 output bits), K terms in the
+// reference order (bitwise equal to k_generic in both modes).
+struct OuterGeom {
+  int obits;                 // log2 output size (pow2 dims)
+  int nk;                    // K terms (<= 64)
+  int32_t ta[4][256], tb[4][256];
+  int32_t ka[64], kb[64];    // operand offsets of k, row-major over the K axes
+};
+template <class R>
+cudaError_t launch_outer(const OuterGeom &g, const BatchPtrs &p, bool exact, cudaStream_t stream);
+
 // Bond-2 "absorb": one big operand X (the stem side) contracted with a small
 // operand W over K bits, producing N new bits:
 //   O[m, n] = sum_k X[m, k] * W[k, n]
@@ -163,7 +175,7 @@ bool tc_absorb_supported(const AbsorbGeom &g);
 bool mma_absorb_supported(const DirectGeom &g);
 cudaError_t launch_absorb_mma(const DirectGeom &g, const BatchPtrs &p, cudaStream_t stream);
 cudaError_t launch_absorb_tc(const AbsorbGeom &g, const BatchPtrs &p, cudaStream_t stream);
-// Gather-fed tcgen05 absorb (absorb_tma.cu, FAST mode): 8 <= K <= 64, 4 <= N <= 64, X bit
+// Gather-fed tcgen05 absorb (absorb_tma.cu, FAST mode): 4 <= K <= 64, 4 <= N <= 64, X bit
 // 0 an M bit. The X tile of every stage is gathered straight into the UMMA MN-major
 // operand layout (the step's permutation fused into the load): by cp.async 16-byte
 // chunks (default), or -- when X bits 0..3 are M bits and the tile bits form <= 5 runs --
@@ -180,7 +192,7 @@ struct TmaAbsorbGeom {
   int K, N, kstage, mbl, nm, spt;       // stage K bits, log2 M blocks, N_mma, stages/tile
   int nsr, nsl, lag;                    // ring depths, loads in flight (set at launch)
   int dbg;
-  int64_t o_m_off[256];                 // O offset of tile-local m
+  int64_t o_m_off[512];                 // O offset of tile-local m
   int64_t w_k_off[64];                  // W offset of k (k bits in ascending X position)
   int64_t w_n_off[128];                 // [0, 64): W offset of n; [64, 128): O offset of n
 };

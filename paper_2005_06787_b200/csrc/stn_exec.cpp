@@ -109,7 +109,7 @@ struct DevBuf {
 // ---------------------------------------------------------------------------
 // plan model
 // ---------------------------------------------------------------------------
-enum class Kern { Generic, Absorb, AbsorbTc, AbsorbDirect, AbsorbMma, SplitK, GemmSimt, GemmTc, AbsorbTma };
+enum class Kern { Generic, Absorb, AbsorbTc, AbsorbDirect, AbsorbMma, SplitK, GemmSimt, GemmTc, AbsorbTma, Outer };
 
 struct Node {
   bool is_leaf = false;
@@ -126,6 +126,7 @@ struct StepPlan {
   std::vector<int> lperm, rperm, operm, out_dims;
   Kern kern = Kern::Generic;
   stn::StridedGeom geo{};  // generic
+  std::shared_ptr<stn::OuterGeom> og;  // small operands, large output
   // absorb
   stn::AbsorbGeom ag{};
   stn::AbsorbGeom agtc{};  // 128-row tiles for the tensor-core absorb
@@ -586,6 +587,53 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     fill_geom(sp.geo, out_axes, k_axes);
   }
   sp.kern = Kern::Generic;
+  // small operands, large output: table-driven outer kernel (bitwise k_generic)
+  if (sp.lsize <= (int64_t(1) << 16) && sp.rsize <= (int64_t(1) << 16) &&
+      sp.osize >= (int64_t(1) << 20) && sp.osize <= (int64_t(1) << 31) &&
+      sp.geo.k_size <= 64) {
+    bool pow2 = true;
+    for (int i = 0; i < sp.geo.n_out; ++i) pow2 &= (sp.geo.out_dim[i] & (sp.geo.out_dim[i] - 1)) == 0;
+    for (int i = 0; i < sp.geo.n_k; ++i) pow2 &= (sp.geo.k_dim[i] & (sp.geo.k_dim[i] - 1)) == 0;
+    if (pow2) {
+      auto og = std::make_shared<stn::OuterGeom>();
+      memset(og.get(), 0, sizeof(stn::OuterGeom));
+      std::vector<int64_t> abit, bbit;  // per output bit (LSB first)
+      for (int i = sp.geo.n_out - 1; i >= 0; --i)
+        for (int64_t v = 1; v < sp.geo.out_dim[i]; v <<= 1) {
+          abit.push_back(v * sp.geo.out_sa[i]);
+          bbit.push_back(v * sp.geo.out_sb[i]);
+        }
+      og->obits = int(abit.size());
+      for (int c = 0; c < 4; ++c)
+        for (int v = 0; v < 256; ++v) {
+          int64_t a = 0, b = 0;
+          for (int j = 0; j < 8; ++j)
+            if (((v >> j) & 1) && 8 * c + j < og->obits) {
+              a += abit[8 * c + j];
+              b += bbit[8 * c + j];
+            }
+          og->ta[c][v] = int32_t(a);
+          og->tb[c][v] = int32_t(b);
+        }
+      og->nk = int(sp.geo.k_size);
+      for (int64_t k = 0; k < sp.geo.k_size; ++k) {  // row-major over the K axes
+        int64_t rem = k, a = 0, b = 0;
+        for (int i = sp.geo.n_k - 1; i >= 0; --i) {
+          const int64_t idx = rem % sp.geo.k_dim[i];
+          rem /= sp.geo.k_dim[i];
+          a += idx * sp.geo.k_sa[i];
+          b += idx * sp.geo.k_sb[i];
+        }
+        og->ka[k] = int32_t(a);
+        og->kb[k] = int32_t(b);
+      }
+      if (og->obits >= 3) {
+        sp.og = og;
+        sp.kern = Kern::Outer;
+        return;
+      }
+    }
+  }
   const int64_t small = std::min(sp.lsize, sp.rsize);
   const int64_t big = std::max(sp.lsize, sp.rsize);
   // bandwidth-bound absorb: one big operand, a small K x N side
@@ -608,7 +656,8 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     if (!exact && sp.tg) {
       const int kn = int(sp.kbits.size() + sp.nbits.size());
       const bool pick = tmin ? kn >= std::atoi(tmin)
-                             : (!sp.direct_ok || sp.dg.L <= 2 || kn >= 12);
+                             : (big >= (int64_t(1) << 22) &&
+                                (!sp.direct_ok || sp.dg.L <= 2 || kn >= 12));
       if (pick) {
         sp.kern = Kern::AbsorbTma;
         return;
@@ -762,7 +811,7 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
 // Diagnostics (STN_PLAN_DUMP): one line per large step with its kernel and bit geometry.
 void dump_step(const StepPlan &sp, int i) {
   static const char *names[] = {"generic", "absorb", "absorb_tc", "direct", "mma", "splitk",
-                                "gemm_simt", "gemm_tc", "tma"};
+                                "gemm_simt", "gemm_tc", "tma", "outer"};
   auto lg = [](int64_t v) { int b = 0; while ((int64_t(1) << b) < v) ++b; return b; };
   std::string s = "step " + std::to_string(i) + " " + names[int(sp.kern)] + " l2^" +
                   std::to_string(lg(sp.lsize)) + " r2^" + std::to_string(lg(sp.rsize)) + " o2^" +
@@ -1722,6 +1771,12 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
     case Kern::Generic: {
       stn::BatchPtrs p{a.ptr, b.ptr, out, a.bs, b.bs, o.bs, nb};
       cuda_check(stn::launch_generic<R>(sp.geo, p, exact, st), "generic kernel");
+      prof.done(STN_KERNEL_GENERIC, io_bytes, flops);
+      break;
+    }
+    case Kern::Outer: {
+      stn::BatchPtrs p{a.ptr, b.ptr, out, a.bs, b.bs, o.bs, nb};
+      cuda_check(stn::launch_outer<R>(*sp.og, p, exact, st), "outer kernel");
       prof.done(STN_KERNEL_GENERIC, io_bytes, flops);
       break;
     }
