@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <functional>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <numeric>
 #include <set>
@@ -75,6 +76,57 @@ int guarded(F &&f) {
 // ---------------------------------------------------------------------------
 // device buffers
 // ---------------------------------------------------------------------------
+// Process-wide cache of large device blocks (arenas, workspaces): plans created and
+// destroyed back to back (a sampler loop, the bench's end-to-end path) reuse their
+// multi-GiB arenas instead of paying cudaMalloc / cudaFree each time. A block goes
+// back to the cache only after a device synchronisation (cudaFree's own guarantee).
+struct BlockCache {
+  struct Block {
+    int device;
+    size_t bytes;
+    void *ptr;
+  };
+  std::mutex mu;
+  std::vector<Block> blocks;
+  size_t total = 0;
+  static constexpr size_t kMinBytes = 0;
+  static constexpr size_t kMaxTotal = size_t(48) << 30;
+  static BlockCache &get() {
+    static BlockCache *c = new BlockCache;  // never destroyed: no cudaFree at exit
+    return *c;
+  }
+  void *take(size_t n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    for (size_t i = 0; i < blocks.size(); ++i)
+      if (blocks[i].device == dev && blocks[i].bytes >= n && blocks[i].bytes <= 2 * n) {
+        void *p = blocks[i].ptr;
+        total -= blocks[i].bytes;
+        blocks.erase(blocks.begin() + long(i));
+        return p;
+      }
+    return nullptr;
+  }
+  void flush() {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto &bl : blocks) cudaFree(bl.ptr);
+    blocks.clear();
+    total = 0;
+  }
+  bool give(void *p, size_t n) {
+    if (n < kMinBytes) return false;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceSynchronize();
+    std::lock_guard<std::mutex> lk(mu);
+    if (total + n > kMaxTotal) return false;
+    blocks.push_back({dev, n, p});
+    total += n;
+    return true;
+  }
+};
+
 struct DevBuf {
   void *ptr = nullptr;
   size_t bytes = 0;
@@ -83,14 +135,25 @@ struct DevBuf {
   DevBuf &operator=(const DevBuf &) = delete;
   ~DevBuf() { release(); }
   void release() {
-    if (ptr) cudaFree(ptr);
+    if (ptr && !BlockCache::get().give(ptr, bytes)) cudaFree(ptr);
     ptr = nullptr;
     bytes = 0;
   }
   void reserve(size_t n) {
     if (n <= bytes) return;
     release();
-    cuda_check(cudaMalloc(&ptr, n), "cudaMalloc");
+    if (n >= BlockCache::kMinBytes) {
+      if (void *p = BlockCache::get().take(n)) {
+        ptr = p;
+        bytes = n;  // usable size; the block may be larger (returned with this size)
+        return;
+      }
+    }
+    if (cudaMalloc(&ptr, n) != cudaSuccess) {  // out of memory: drop the cached blocks, retry
+      cudaGetLastError();
+      BlockCache::get().flush();
+      cuda_check(cudaMalloc(&ptr, n), "cudaMalloc");
+    }
     bytes = n;
   }
   template <class T>
@@ -1456,6 +1519,7 @@ void upload_sliced_values(stn_plan &P) {
 }
 
 void create_plan(const stn_plan_desc *desc, int device, int mode, stn_plan *P) {
+  const auto t_begin = std::chrono::steady_clock::now();
   require(desc != nullptr, STN_ERR_INVALID_ARGUMENT, "NULL plan descriptor");
   require(desc->precision == STN_SINGLE || desc->precision == STN_DOUBLE,
           STN_ERR_INVALID_ARGUMENT, "bad precision");
@@ -1636,10 +1700,17 @@ void create_plan(const stn_plan_desc *desc, int device, int mode, stn_plan *P) {
       }
     P->cache_elems = off;
   }
+  const auto t_steps = std::chrono::steady_clock::now();
   plan_sweeps(*P);
   build_program(*P, P->build, 0);
   build_program(*P, P->with_cache, 1);
   build_program(*P, P->no_cache, 2);
+  if (std::getenv("STN_PLAN_TIMING")) {
+    const auto t_end = std::chrono::steady_clock::now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    fprintf(stderr, "plan create: steps+leaves %.2f ms, programs %.2f ms\n", ms(t_begin, t_steps),
+            ms(t_steps, t_end));
+  }
 }
 
 // ---------------------------------------------------------------------------
