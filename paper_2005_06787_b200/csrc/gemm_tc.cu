@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.h"
@@ -310,6 +311,161 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ---- 128 x 256 tiles -------------------------------------------------------------
+// Same pipeline with UMMA N = 256: every A byte fetched from L2 now feeds twice the
+// MMA work (the 128 x 128 kernel is bound by L2 -> SM operand traffic: 64 KiB per
+// 810-cycle k-block). The three split-TF32 products go into ONE fp32 TMEM accumulator
+// (256 columns; two buffers for the chunked round-to-nearest flush), two stages of
+// 96 KiB, and 8 epilogue warps (two per TMEM lane quadrant, 128 columns each).
+constexpr int BN2 = 256;
+constexpr int STAGES2 = 2;
+constexpr int B2_TILE_BYTES = BN2 * BK * 4;  // 32 KiB
+constexpr int STAGE2_BYTES = 2 * A_TILE_BYTES + 2 * B2_TILE_BYTES;
+constexpr int THREADS2 = 320;
+constexpr size_t SMEM2_BYTES = size_t(STAGES2) * STAGE2_BYTES + 1024 + 256;
+constexpr uint32_t kIdesc2 = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(BN2 >> 3) << 17) |
+                             (uint32_t(BM >> 4) << 24);
+
+__global__ void __launch_bounds__(THREADS2, 1)
+    k_gemm_tc256(const __grid_constant__ CUtensorMap map_ahi,
+                 const __grid_constant__ CUtensorMap map_alo,
+                 const __grid_constant__ CUtensorMap map_bhi,
+                 const __grid_constant__ CUtensorMap map_blo, const TcArgs args) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *smem = reinterpret_cast<unsigned char *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES2 * STAGE2_BYTES);
+  uint64_t *empty = full + STAGES2;
+  uint64_t *tmem_full = empty + STAGES2;
+  uint64_t *tmem_empty = tmem_full + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n_tile = blockIdx.x % args.n_tiles, m_tile = blockIdx.x / args.n_tiles;
+  const int bz = blockIdx.z;
+  const int slice = bz / args.D, d = bz % args.D;
+  const int za = args.a_batched ? bz : d;
+  const int zb = args.b_batched ? bz : d;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ahi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_alo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], 8);  // one arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < args.k_blocks; ++kb) {
+        const int s = kb % STAGES2;
+        const uint32_t phase = (kb / STAGES2) & 1;
+        mbar_wait(&empty[s], phase ^ 1);
+        unsigned char *st = smem + s * STAGE2_BYTES;
+        mbar_expect_tx(&full[s], STAGE2_BYTES);
+        const int kx = kb * BK;
+        tma_load_3d(st, &map_ahi, &full[s], kx, m_tile * BM, za);
+        tma_load_3d(st + A_TILE_BYTES, &map_alo, &full[s], kx, m_tile * BM, za);
+        tma_load_3d(st + 2 * A_TILE_BYTES, &map_bhi, &full[s], kx, n_tile * BN2, zb);
+        tma_load_3d(st + 2 * A_TILE_BYTES + B2_TILE_BYTES, &map_blo, &full[s], kx, n_tile * BN2,
+                    zb);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int kb = 0; kb < args.k_blocks; ++kb) {
+        const int s = kb % STAGES2;
+        const uint32_t phase = (kb / STAGES2) & 1;
+        const int chunk = kb / CHUNK, buf = chunk & 1;
+        const bool chunk_first = kb % CHUNK == 0;
+        const bool chunk_last = kb % CHUNK == CHUNK - 1 || kb == args.k_blocks - 1;
+        if (chunk_first) {
+          mbar_wait(&tmem_empty[buf], ((chunk >> 1) & 1) ^ 1);
+          tc_fence_after();
+        }
+        mbar_wait(&full[s], phase);
+        tc_fence_after();
+        const uint32_t st = smem_u32(smem + s * STAGE2_BYTES);
+        const uint64_t ahi = smem_desc_sw128(st);
+        const uint64_t alo = smem_desc_sw128(st + A_TILE_BYTES);
+        const uint64_t bhi = smem_desc_sw128(st + 2 * A_TILE_BYTES);
+        const uint64_t blo = smem_desc_sw128(st + 2 * A_TILE_BYTES + B2_TILE_BYTES);
+        const uint32_t tacc = tmem_base + uint32_t(buf * BN2);
+#pragma unroll
+        for (int k = 0; k < BK / UK; ++k) {
+          const uint64_t koff = uint64_t((k * UK * 4) >> 4);
+          const uint32_t acc0 = (!chunk_first || k > 0) ? 1u : 0u;
+          umma_tf32(tacc, ahi + koff, bhi + koff, kIdesc2, acc0);
+          umma_tf32(tacc, ahi + koff, blo + koff, kIdesc2, 1u);
+          umma_tf32(tacc, alo + koff, bhi + koff, kIdesc2, 1u);
+        }
+        umma_commit(&empty[s]);
+        if (chunk_last) umma_commit(&tmem_full[buf]);
+      }
+    }
+  } else {
+    // ---- epilogue: warps 2..9; (warp % 4) = TMEM lane quadrant, half = 128-column half ----
+    const int q4 = warp % 4, half = (warp - 2) / 4;
+    const int lane_base = 32 * q4;
+    const int row = m_tile * BM + lane_base + lane;
+    float acc[128];
+#pragma unroll
+    for (int c = 0; c < 128; ++c) acc[c] = 0.f;
+    const int n_chunks = (args.k_blocks + CHUNK - 1) / CHUNK;
+    for (int chunk = 0; chunk < n_chunks; ++chunk) {
+      const int buf = chunk & 1;
+      mbar_wait(&tmem_full[buf], (chunk >> 1) & 1);
+      tc_fence_after();
+      const uint32_t t0 =
+          tmem_base + (uint32_t(lane_base) << 16) + uint32_t(buf * BN2 + 128 * half);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(t0 + uint32_t(cc * 32), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc[cc * 32 + q] += __uint_as_float(v[q]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[buf]);
+    }
+    float *crow = args.c + int64_t(slice) * args.c_bs + int64_t(d) * args.c_ds +
+                  int64_t(row) * args.two_n + int64_t(n_tile) * BN2 + 128 * half;
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      reinterpret_cast<float4 *>(crow)[q] =
+          make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(512));
+  }
+}
+
 // ---- operand preparation --------------------------------------------------------
 // A (complex M x K per batch) -> hi/lo planes, same M x 2K real layout.
 __global__ void k_split_a(const float *__restrict__ a, int64_t a_bs, int64_t a_ds, int D,
@@ -445,15 +601,22 @@ cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspa
                                                   s.K * s.N, int(s.D), int(s.K), int(s.N), bhi,
                                                   blo);
   }
+  // 128 x 256 tiles where 2N allows (STN_GEMM_BN=128 forces the 128 x 128 kernel)
+  const char *env_bn = std::getenv("STN_GEMM_BN");
+  const bool wide = (2 * s.N) % BN2 == 0 && !(env_bn && std::atoi(env_bn) == 128);
+  const int bn = wide ? BN2 : BN;
   CUtensorMap mah, mal, mbh, mbl;
   if (!make_map(&mah, ahi, 2 * s.K, s.M, nbA, BM) || !make_map(&mal, alo, 2 * s.K, s.M, nbA, BM) ||
-      !make_map(&mbh, bhi, 2 * s.K, 2 * s.N, nbB, BN) ||
-      !make_map(&mbl, blo, 2 * s.K, 2 * s.N, nbB, BN))
+      !make_map(&mbh, bhi, 2 * s.K, 2 * s.N, nbB, bn) ||
+      !make_map(&mbl, blo, 2 * s.K, 2 * s.N, nbB, bn))
     return cudaErrorNotSupported;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e =
         cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_gemm_tc256, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(SMEM2_BYTES));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -466,10 +629,13 @@ cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspa
   args.b_batched = p.b_bs != 0;
   args.k_blocks = int(2 * s.K / BK);
   args.two_n = int(2 * s.N);
-  args.n_tiles = int(2 * s.N / BN);
-  dim3 grid(unsigned((2 * s.N / BN) * (s.M / BM)), 1, unsigned(s.D * p.nbatch));
+  args.n_tiles = int(2 * s.N / bn);
+  dim3 grid(unsigned((2 * s.N / bn) * (s.M / BM)), 1, unsigned(s.D * p.nbatch));
   if (gemm_events) cudaEventRecord(gemm_events[0], stream);
-  k_gemm_tc<<<grid, THREADS, SMEM_BYTES, stream>>>(mah, mal, mbh, mbl, args);
+  if (wide)
+    k_gemm_tc256<<<grid, THREADS2, SMEM2_BYTES, stream>>>(mah, mal, mbh, mbl, args);
+  else
+    k_gemm_tc<<<grid, THREADS, SMEM_BYTES, stream>>>(mah, mal, mbh, mbl, args);
   if (gemm_events) cudaEventRecord(gemm_events[1], stream);
   return cudaGetLastError();
 }
