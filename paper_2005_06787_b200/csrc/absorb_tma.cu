@@ -67,7 +67,12 @@ struct TmaLayout {
   static constexpr int STAGE = MB * KSZ * 512;       // bytes of one raw (or lo) stage
   static constexpr int LBO = KSZ * 128;              // MN-atom stride (32 m-floats x KSZ rows)
   static constexpr int BROWS = 2 * NM;               // B'' rows: hi then lo
-  static constexpr int ACC = MB * NM;                // TMEM columns of one accumulator buffer
+  // DUAL (small N): MMA 1 = raw x [B'hi; B'lo] (N = 2NM) puts hi*hi and hi*lo in two column
+  // halves, MMA 2 adds lo*hi to the second half -- 2 MMAs per k-step instead of 3 (the
+  // single MMA thread is the limit there); the epilogue adds the halves.
+  static constexpr bool DUAL = NM <= 32;
+  static constexpr int BCOLS = DUAL ? 2 * NM : NM;    // TMEM columns of one M block
+  static constexpr int ACC = MB * BCOLS;             // TMEM columns of one accumulator buffer
   static constexpr int NACC = 4 * ACC <= 512 ? 4 : 2;  // accumulator buffers
   static constexpr int TMEM_COLS = NACC * ACC <= 32 ? 32 : (NACC * ACC <= 64 ? 64 : (NACC * ACC <= 128 ? 128 : (NACC * ACC <= 256 ? 256 : 512)));
 };
@@ -228,6 +233,7 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
       const uint32_t b_base = smem_u32(bmat);
       const uint32_t raw_base = smem_u32(raw), lo_base = smem_u32(lo);
       constexpr uint32_t IDESC = idesc_tf32(NM, true);
+      constexpr uint32_t IDESC2 = idesc_tf32(2 * NM, true);
       RingPos rs, rl;
       int i = 0;
       for (int64_t t = t_begin; t < t_end; ++t, ++i) {
@@ -255,12 +261,17 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
               constexpr uint32_t SBO = KSZ >= 8 ? 512 : 0;
               const uint64_t dr = smem_desc(raw_base + s * Lay::STAGE + aoff, Lay::LBO, SBO, 1);
               const uint64_t dl = smem_desc(lo_base + l * Lay::STAGE + aoff, Lay::LBO, SBO, 1);
-              const uint32_t d = acc_base + uint32_t(b * NM);
+              const uint32_t d = acc_base + uint32_t(b * Lay::BCOLS);
               if (g.dbg & 2) continue;
-              // one fp32 accumulator: hi*hi, then the hi*lo and lo*hi corrections
-              umma_tf32(d, dr, db, IDESC, acc_flag);
-              umma_tf32(d, dr, dbl, IDESC, 1u);
-              umma_tf32(d, dl, db, IDESC, 1u);
+              if constexpr (Lay::DUAL) {
+                umma_tf32(d, dr, db, IDESC2, acc_flag);
+                umma_tf32(d + NM, dl, db, IDESC, 1u);
+              } else {
+                // one fp32 accumulator: hi*hi, then the hi*lo and lo*hi corrections
+                umma_tf32(d, dr, db, IDESC, acc_flag);
+                umma_tf32(d, dr, dbl, IDESC, 1u);
+                umma_tf32(d, dl, db, IDESC, 1u);
+              }
             }
           }
           umma_commit(&empty[s]);
@@ -380,20 +391,24 @@ __global__ void __launch_bounds__(Roles<GATHER>::THREADS, 1)
       for (int j0 = 0; j0 < MINE; j0 += BATCH) {
         float vals[BATCH][16];
         {
-          uint32_t vm[BATCH][16];
+          uint32_t vm[BATCH][16], vc[Lay::DUAL ? BATCH : 1][16];
 #pragma unroll
           for (int u = 0; u < BATCH; ++u) {
             const int c = 2 * (j0 + u) + half;
             if (c < CH) {
               const int b = c / (NM / 16), cc = (c % (NM / 16)) * 16;
-              tmem_ld16(tq + uint32_t(b * NM + cc), vm[u]);
+              tmem_ld16(tq + uint32_t(b * Lay::BCOLS + cc), vm[u]);
+              if constexpr (Lay::DUAL) tmem_ld16(tq + uint32_t(b * Lay::BCOLS + NM + cc), vc[u]);
             }
           }
           tmem_wait_ld();
 #pragma unroll
           for (int u = 0; u < BATCH; ++u)
 #pragma unroll
-            for (int q = 0; q < 16; ++q) vals[u][q] = __uint_as_float(vm[u][q]);
+            for (int q = 0; q < 16; ++q) {
+              vals[u][q] = __uint_as_float(vm[u][q]);
+              if constexpr (Lay::DUAL) vals[u][q] += __uint_as_float(vc[u][q]);
+            }
         }
         if (j0 + BATCH >= MINE) {  // all of this warp's TMEM share is in registers
           tc_fence_before();
