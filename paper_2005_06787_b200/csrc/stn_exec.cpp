@@ -115,7 +115,9 @@ struct BlockCache {
     total = 0;
   }
   bool give(void *p, size_t n) {
-    if (n < kMinBytes) return false;
+    static const bool off = std::getenv("STN_BLOCK_CACHE") &&
+                            std::string(std::getenv("STN_BLOCK_CACHE")) == "0";
+    if (off || n < kMinBytes) return false;
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceSynchronize();
