@@ -31,6 +31,17 @@ __device__ __forceinline__ uint64_t pdep_mask(uint64_t v, uint64_t mask) {
   return r;
 }
 
+// Blackwell packed FP32 FMA (FFMA2) on 64-bit register pairs: acc += x * w, lane-wise.
+__device__ __forceinline__ void ffma2(unsigned long long &acc, const unsigned long long x,
+                                      const unsigned long long w) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(x), "l"(w));
+}
+__device__ __forceinline__ float2 unpack2(const unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+
 // KC / NC: K and N chunks held in registers (compile time, <= 16). FULLK:
 // K == KC, so the K inputs of an m pair are loaded once and reused for every
 // N chunk; otherwise every (N chunk, K chunk) reloads (an L1/L2 hit).
@@ -39,8 +50,12 @@ __global__ void __launch_bounds__(kDirThreads)
     k_absorb_direct(const __grid_constant__ DirectGeom g, const BatchPtrs p) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const int K = FULLK ? KC : (1 << g.kb), N = 1 << g.nb;
-  float2 *wsm = reinterpret_cast<float2 *>(dsm);                 // [N][K]
-  int64_t *xko = reinterpret_cast<int64_t *>(wsm + K * N);       // [K] X offset / 2 of k
+  // EXACT: W as [N][K] float2. FAST (FFMA2 form): [N][K] float4 (wr, wr, wi, -wi), so
+  // that with x = (xr, xi) as loaded, U += x * (wr, wr) and V += x * (wi, -wi) give
+  // re = U.x + V.y and im = U.y + V.x without repacking any operand.
+  float2 *wsm = reinterpret_cast<float2 *>(dsm);
+  float4 *wq = reinterpret_cast<float4 *>(dsm);
+  int64_t *xko = reinterpret_cast<int64_t *>(EXACT ? (void *)(wsm + K * N) : (void *)(wq + K * N));
   int64_t *ono = xko + K;                                         // [N] O offset of n
   const int b = blockIdx.y;
   const float2 *X = static_cast<const float2 *>(p.a) + int64_t(b) * p.a_bs;
@@ -53,7 +68,12 @@ __global__ void __launch_bounds__(kDirThreads)
       if ((k >> j) & 1) off += g.w_k_stride[j];
     for (int j = 0; j < g.nb; ++j)
       if ((n >> j) & 1) off += g.w_n_stride[j];
-    wsm[i] = Wg[off];
+    const float2 w = Wg[off];
+    if constexpr (EXACT) {
+      wsm[i] = w;
+    } else {
+      wq[i] = make_float4(w.x, w.x, w.y, -w.y);
+    }
   }
   for (int k = threadIdx.x; k < K; k += kDirThreads) {
     int64_t off = 0;
@@ -80,10 +100,49 @@ __global__ void __launch_bounds__(kDirThreads)
     const float4 *xs = reinterpret_cast<const float4 *>(X + px + lo);
     float2 *os = O + po + lo;
     float4 xv[KC];
-    if constexpr (FULLK) {
+    if constexpr (FULLK && EXACT) {
 #pragma unroll
       for (int k = 0; k < KC; ++k) xv[k] = __ldcs(xs + xko[k]);
     }
+    if constexpr (!EXACT) {
+      const ulonglong2 *xq = reinterpret_cast<const ulonglong2 *>(xs);
+      const ulonglong2 *wq2 = reinterpret_cast<const ulonglong2 *>(wq);
+      ulonglong2 xp[KC];  // (x m0, x m1) as 64-bit (re, im) pairs
+      if constexpr (FULLK) {
+#pragma unroll
+        for (int k = 0; k < KC; ++k) xp[k] = __ldcs(xq + xko[k]);
+      }
+      for (int n0 = 0; n0 < N; n0 += NC) {
+        unsigned long long u0[NC], v0[NC], u1[NC], v1[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) u0[c] = v0[c] = u1[c] = v1[c] = 0ull;
+        for (int k0 = 0; k0 < K; k0 += KC) {
+          if constexpr (!FULLK) {
+#pragma unroll
+            for (int k = 0; k < KC; ++k) xp[k] = xq[xko[k0 + k]];
+          }
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const ulonglong2 *qr = wq2 + (n0 + c) * K + k0;
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+              const ulonglong2 q = qr[k];  // ((wr, wr), (wi, -wi))
+              ffma2(u0[c], xp[k].x, q.x);
+              ffma2(v0[c], xp[k].x, q.y);
+              ffma2(u1[c], xp[k].y, q.x);
+              ffma2(v1[c], xp[k].y, q.y);
+            }
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const float2 U0 = unpack2(u0[c]), V0 = unpack2(v0[c]);
+          const float2 U1 = unpack2(u1[c]), V1 = unpack2(v1[c]);
+          __stcs(reinterpret_cast<float4 *>(os + ono[n0 + c]),
+                 make_float4(U0.x + V0.y, U0.y + V0.x, U1.x + V1.y, U1.y + V1.x));
+        }
+      }
+    } else
     for (int n0 = 0; n0 < N; n0 += NC) {
       float2 a0[NC], a1[NC];
 #pragma unroll
@@ -124,8 +183,10 @@ cudaError_t launch_direct_exact(const DirectGeom &g, const BatchPtrs &p, cudaStr
   const int64_t threads = (int64_t(1) << (g.L - 1)) *
                           (((int64_t(1) << g.mh_bits) + kDirR - 1) / kDirR);
   dim3 grid(unsigned((threads + kDirThreads - 1) / kDirThreads), unsigned(p.nbatch));
-  const size_t smem = (size_t(8) << (g.kb + g.nb)) + 8 * ((size_t(1) << g.kb) + (size_t(1) << g.nb));
-  const int kc = g.kb >= 4 ? 16 : (1 << g.kb), nc = g.nb >= 4 ? 16 : (1 << g.nb);
+  const size_t smem = (size_t(EXACT ? 8 : 24) << (g.kb + g.nb)) +
+                      8 * ((size_t(1) << g.kb) + (size_t(1) << g.nb));
+  // FAST keeps two accumulator pairs per (m, n): at most 8 n per register tile
+  const int kc = g.kb >= 4 ? 16 : (1 << g.kb), nc = g.nb >= (EXACT ? 4 : 3) ? (EXACT ? 16 : 8) : (1 << g.nb);
   const bool full = g.kb <= 4;
 #define STN_DIR(KV, NV, FULL)                                                          \
   if (kc == KV && nc == NV && full == FULL) {                                          \
