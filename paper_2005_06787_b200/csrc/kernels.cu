@@ -392,28 +392,57 @@ __global__ void __launch_bounds__(256)
       kb += idx * g.k_sb[i];
     }
   };
+  int64_t *rows = kb_tab + kc;  // [M] A row offsets + ka0, then [N] B column offsets + kb0
   for (int kk = threadIdx.x; kk < kc; kk += blockDim.x) koff(kk, ka_tab[kk], kb_tab[kk]);
-  int64_t ka0, kb0;
-  koff(k0, ka0, kb0);
+  {
+    int64_t ka0, kb0;
+    koff(k0, ka0, kb0);
+    for (int r = threadIdx.x; r < t.M + t.N; r += blockDim.x)
+      rows[r] = r < t.M ? t.a_row[r] + ka0 : t.b_col[r - t.M] + kb0;
+  }
   __syncthreads();
-  // stage A[:, chunk] and B[:, chunk]: consecutive threads take consecutive k
-  for (int idx = threadIdx.x; idx < (t.M + t.N) * kc; idx += blockDim.x) {
-    const int row = idx / kc, kk = idx % kc;
-    T v;
-    v.x = v.y = 0;
-    if (kk < len)
-      v = row < t.M ? A[t.a_row[row] + ka0 + ka_tab[kk]] : B[t.b_col[row - t.M] + kb0 + kb_tab[kk]];
-    sA[row * (kc + 1) + kk] = v;  // sB follows sA contiguously
+  // stage A[:, chunk] and B[:, chunk]: consecutive threads take consecutive k;
+  // kBatch independent loads in flight per thread before any shared store
+  constexpr int kBatch = 8;
+  const int kc_log = __ffs(kc) - 1;
+  const int total = (t.M + t.N) << kc_log;
+  for (int base = 0; base < total; base += kBatch * 256) {
+    T v[kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int idx = base + j * 256 + int(threadIdx.x);
+      const int row = idx >> kc_log, kk = idx & (kc - 1);
+      v[j].x = v[j].y = 0;
+      if (idx < total && kk < len) {
+        const T *src = row < t.M ? A : B;
+        v[j] = src[rows[row] + (row < t.M ? ka_tab[kk] : kb_tab[kk])];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int idx = base + j * 256 + int(threadIdx.x);
+      if (idx < total) sA[(idx >> kc_log) * (kc + 1) + (idx & (kc - 1))] = v[j];  // sB follows sA
+    }
   }
   __syncthreads();
   for (int o = threadIdx.x; o < g.out_size; o += blockDim.x) {
     const int mn = t.o_mn[o];
     const T *ra = sA + (mn & 0xFFFF) * (kc + 1);
     const T *rb = sB + (mn >> 16) * (kc + 1);
-    T acc;
-    acc.x = acc.y = 0;
-    for (int kk = 0; kk < len; ++kk) cmac<false>(acc, ra[kk], rb[kk]);
-    partial[o] = acc;
+    // four independent accumulators (k mod 4), summed in a fixed order
+    T acc[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j].x = acc[j].y = 0;
+    int kk = 0;
+    for (; kk + 4 <= len; kk += 4) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cmac<false>(acc[j], ra[kk + j], rb[kk + j]);
+    }
+    for (; kk < len; ++kk) cmac<false>(acc[0], ra[kk], rb[kk]);
+    T r;
+    r.x = (acc[0].x + acc[1].x) + (acc[2].x + acc[3].x);
+    r.y = (acc[0].y + acc[1].y) + (acc[2].y + acc[3].y);
+    partial[o] = r;
   }
 }
 
@@ -450,7 +479,8 @@ __global__ void __launch_bounds__(256)
 // k per chunk: A and B rows of the chunk fit in 48 KiB of shared memory
 int splitk_kc(const DotTables &t, size_t esize) {
   int kc = 256;
-  while (kc > 8 && size_t(t.M + t.N) * (kc + 1) * esize > 48 * 1024) kc /= 2;
+  while (kc > 8 && size_t(t.M + t.N) * (kc + 1) * esize + 8 * size_t(t.M + t.N) > 44 * 1024)
+    kc /= 2;
   return kc;
 }
 
@@ -464,7 +494,8 @@ cudaError_t launch_splitk(const StridedGeom &g, const BatchPtrs &p, const DotTab
                           void *workspace, cudaStream_t stream) {
   const int kc = splitk_kc(t, sizeof(cx_t<R>));
   const int nchunks = splitk_chunks(g, t, sizeof(cx_t<R>));
-  const size_t smem = size_t(t.M + t.N) * (kc + 1) * sizeof(cx_t<R>) + 16 * size_t(kc);
+  const size_t smem = size_t(t.M + t.N) * (kc + 1) * sizeof(cx_t<R>) + 16 * size_t(kc) +
+                      8 * size_t(t.M + t.N);
   k_splitk_partial<R><<<dim3(nchunks, p.nbatch), 256, smem, stream>>>(g, p, t, kc, nchunks,
                                                                       workspace);
   k_splitk_sum<R><<<unsigned(g.out_size * p.nbatch), 256, 0, stream>>>(

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+timeout 300 python scripts/step_profile.py cfg2 > gpurun_out/r66_prof.txt 2>&1; echo prof=$?; head -12 gpurun_out/r66_prof.txt; grep " 750 " gpurun_out/r66_prof.txt
+STN_PLAN_TIMING=1 timeout 300 python scripts/e2e_breakdown.py 2>&1 | tail -8
