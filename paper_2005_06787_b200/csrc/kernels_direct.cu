@@ -111,6 +111,14 @@ __global__ void __launch_bounds__(kDirThreads)
       if constexpr (FULLK) {
 #pragma unroll
         for (int k = 0; k < KC; ++k) xp[k] = __ldcs(xq + xko[k]);
+        // pull the next m_hi's X into L2 while this one computes
+        if (r + 1 < kDirR && hi0 + r + 1 < n_hi) {
+          const uint64_t pxn = ((px | ~g.hi_x_mask) + 1) & g.hi_x_mask;
+          const float2 *xn = X + pxn + lo;
+#pragma unroll
+          for (int k = 0; k < KC; ++k)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(xn + 2 * xko[k]));
+        }
       }
       for (int n0 = 0; n0 < N; n0 += NC) {
         unsigned long long u0[NC], v0[NC], u1[NC], v1[NC];
