@@ -19,7 +19,8 @@ using namespace dev;
 // cover 512 contiguous bytes per k / per n; no tiles, no barriers in the loop.
 // ---------------------------------------------------------------------------
 constexpr int kDirThreads = 256;
-constexpr int kDirR = 8;  // m_hi values per thread
+constexpr int kDirR = 8;   // m_hi values per thread
+constexpr int kDirPf = 2;  // L2 prefetch distance (m_hi values) in FAST mode
 
 __device__ __forceinline__ uint64_t pdep_mask(uint64_t v, uint64_t mask) {
   uint64_t r = 0;
@@ -111,13 +112,16 @@ __global__ void __launch_bounds__(kDirThreads)
       if constexpr (FULLK) {
 #pragma unroll
         for (int k = 0; k < KC; ++k) xp[k] = __ldcs(xq + xko[k]);
-        // pull the next m_hi's X into L2 while this one computes
-        if (r + 1 < kDirR && hi0 + r + 1 < n_hi) {
-          const uint64_t pxn = ((px | ~g.hi_x_mask) + 1) & g.hi_x_mask;
-          const float2 *xn = X + pxn + lo;
+        // pull the X inputs kDirPf m_hi ahead into L2 while this one computes
+        uint64_t pxn = px;
+        for (int d = 1; d <= kDirPf; ++d) {
+          pxn = ((pxn | ~g.hi_x_mask) + 1) & g.hi_x_mask;
+          if ((r == 0 || d == kDirPf) && r + d < kDirR && hi0 + r + d < n_hi) {
+            const float2 *xn = X + pxn + lo;
 #pragma unroll
-          for (int k = 0; k < KC; ++k)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(xn + 2 * xko[k]));
+            for (int k = 0; k < KC; ++k)
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(xn + 2 * xko[k]));
+          }
         }
       }
       for (int n0 = 0; n0 < N; n0 += NC) {
