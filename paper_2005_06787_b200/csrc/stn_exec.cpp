@@ -1522,6 +1522,7 @@ void upload_sliced_values(stn_plan &P) {
 
 void create_plan(const stn_plan_desc *desc, int device, int mode, stn_plan *P) {
   const auto t_begin = std::chrono::steady_clock::now();
+  double choose_ms[16] = {0};  // per kernel kind (STN_PLAN_TIMING)
   require(desc != nullptr, STN_ERR_INVALID_ARGUMENT, "NULL plan descriptor");
   require(desc->precision == STN_SINGLE || desc->precision == STN_DOUBLE,
           STN_ERR_INVALID_ARGUMENT, "bad precision");
@@ -1531,10 +1532,16 @@ void create_plan(const stn_plan_desc *desc, int device, int mode, stn_plan *P) {
   require(e == cudaSuccess && ndev > 0, STN_ERR_NO_DEVICE, "no CUDA device available");
   require(device >= 0 && device < ndev, STN_ERR_NO_DEVICE, "device index out of range");
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
-  cudaDeviceProp prop;
-  cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
-  require(prop.major == 10, STN_ERR_NO_DEVICE,
-          std::string("executor is built for sm_100a; device is ") + prop.name);
+  // (attribute queries: cudaGetDeviceProperties costs milliseconds per call)
+  int cc_major = 0, cc_minor = 0;
+  cuda_check(cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, device),
+             "cudaDeviceGetAttribute");
+  cuda_check(cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, device),
+             "cudaDeviceGetAttribute");
+  require(cc_major == 10, STN_ERR_NO_DEVICE,
+          "executor is built for sm_100a; device is sm_" + std::to_string(cc_major) +
+              std::to_string(cc_minor));
+  const auto t_dev = std::chrono::steady_clock::now();
   P->device = device;
   P->mode = mode;
   P->precision = desc->precision;
@@ -1659,7 +1666,10 @@ void create_plan(const stn_plan_desc *desc, int device, int mode, stn_plan *P) {
     for (int q = 0; q < d.nn; ++q) N *= rd[sp.rperm[d.nd + d.nk + q]];
     require(D == d.D && M == d.M && N == d.N && K == d.K && sp.osize == D * M * N,
             STN_ERR_MALFORMED_NETWORK, "step shape inconsistent at node " + std::to_string(d.node));
+    const auto t_ck = std::chrono::steady_clock::now();
     choose_kernel(*P, sp, ld, rd);
+    choose_ms[int(sp.kern)] +=
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_ck).count();
     if (std::getenv("STN_PLAN_DUMP") && !d.is_branch && sp.osize + sp.lsize + sp.rsize >= (1 << 20))
       dump_step(sp, i);
   }
@@ -1686,8 +1696,10 @@ void create_plan(const stn_plan_desc *desc, int device, int mode, stn_plan *P) {
     }
   }
   P->consts_elems = std::max<int64_t>(coff, 1);
+  const auto t_up0 = std::chrono::steady_clock::now();
   upload_consts(*P);
   upload_sliced_values(*P);
+  const auto t_up1 = std::chrono::steady_clock::now();
   // branch outputs that survive the cache build (runtime.hpp:473-487)
   {
     std::vector<char> needed(desc->n_nodes, 0);
@@ -1712,6 +1724,12 @@ void create_plan(const stn_plan_desc *desc, int device, int mode, stn_plan *P) {
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
     fprintf(stderr, "plan create: steps+leaves %.2f ms, programs %.2f ms\n", ms(t_begin, t_steps),
             ms(t_steps, t_end));
+    fprintf(stderr, "  device query %.2f ms, leaf/const uploads %.2f ms\n", ms(t_begin, t_dev),
+            ms(t_up0, t_up1));
+    fprintf(stderr, "  choose_kernel ms by kind:");
+    for (int k = 0; k < 16; ++k)
+      if (choose_ms[k] > 0.05) fprintf(stderr, " %d:%.2f", k, choose_ms[k]);
+    fprintf(stderr, "\n");
   }
 }
 
