@@ -9,6 +9,7 @@
 //            bitwise identical to the reference CPU executor.
 //   fast   - the same order with fused multiply-adds.
 #include <cstdint>
+#include <type_traits>
 #include <cstdlib>
 #include <cuda_runtime.h>
 
@@ -508,10 +509,82 @@ size_t splitk_workspace_bytes(const StridedGeom &g, const DotTables &t, int nbat
   return size_t(splitk_chunks(g, t, esize)) * g.out_size * nbatch * esize;
 }
 
+// Skinny GEMM (FAST, N <= 8, K * N <= 4096): C[m][:] = A[m][:] . B for very tall A
+// (e.g. 2^20 x 512 x 8). The 64 x 64 tile kernel wastes 7/8 of its math on N = 8; here
+// B^T sits in shared memory ([n][k]: lanes read consecutive k, no bank conflicts) and
+// each warp streams kSkRows rows of A with 16-byte loads along k, every B load serving
+// all its rows; the 32 lane partials of each output are summed with xor shuffles.
+constexpr int kSkRows = 4, kSkN = 8;
+__global__ void __launch_bounds__(256)
+    k_gemm_skinny(const GemmShape s, const BatchPtrs p) {
+  extern __shared__ __align__(16) float2 bt[];  // [kSkN][K]
+  const int64_t batch = blockIdx.z;  // = slice * D + d
+  const int64_t slice = batch / s.D, d = batch % s.D;
+  const float2 *A = static_cast<const float2 *>(p.a) + slice * p.a_bs + d * s.M * s.K;
+  const float2 *B = static_cast<const float2 *>(p.b) + slice * p.b_bs + d * s.K * s.N;
+  float2 *C = static_cast<float2 *>(p.out) + slice * p.out_bs + d * s.M * s.N;
+  const int K = int(s.K), N = int(s.N);
+  for (int e = threadIdx.x; e < kSkN * K; e += 256) {
+    const int n = e / K, k = e % K;
+    bt[e] = n < N ? B[int64_t(k) * N + n] : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t m0 = (int64_t(blockIdx.x) * 8 + warp) * kSkRows;
+  if (m0 >= s.M) return;
+  float2 acc[kSkRows][kSkN];
+#pragma unroll
+  for (int r = 0; r < kSkRows; ++r)
+#pragma unroll
+    for (int n = 0; n < kSkN; ++n) acc[r][n] = make_float2(0.f, 0.f);
+  for (int k = 2 * lane; k < K; k += 64) {
+    float4 x[kSkRows];
+#pragma unroll
+    for (int r = 0; r < kSkRows; ++r)
+      x[r] = m0 + r < s.M ? __ldcs(reinterpret_cast<const float4 *>(A + (m0 + r) * K + k))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int n = 0; n < kSkN; ++n) {
+      const float4 w = *reinterpret_cast<const float4 *>(bt + n * K + k);
+#pragma unroll
+      for (int r = 0; r < kSkRows; ++r) {
+        cmac<false>(acc[r][n], make_float2(x[r].x, x[r].y), make_float2(w.x, w.y));
+        cmac<false>(acc[r][n], make_float2(x[r].z, x[r].w), make_float2(w.z, w.w));
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kSkRows; ++r)
+#pragma unroll
+    for (int n = 0; n < kSkN; ++n)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc[r][n].x += __shfl_xor_sync(0xffffffffu, acc[r][n].x, o);
+        acc[r][n].y += __shfl_xor_sync(0xffffffffu, acc[r][n].y, o);
+      }
+#pragma unroll
+  for (int r = 0; r < kSkRows; ++r) {
+    float2 v = acc[r][0];
+#pragma unroll
+    for (int n = 1; n < kSkN; ++n)
+      if (lane == n) v = acc[r][n];
+    if (lane < N && m0 + r < s.M) C[(m0 + r) * N + lane] = v;
+  }
+}
+
 template <class R>
 cudaError_t launch_gemm_simt(const GemmShape &s, const BatchPtrs &p, bool exact,
                              cudaStream_t stream) {
   if (s.M == 0 || s.N == 0 || p.nbatch == 0) return cudaSuccess;
+  if constexpr (std::is_same<R, float>::value) {
+    if (!exact && s.N <= kSkN && s.K % 2 == 0 && s.K >= 64 && s.K * kSkN <= 4096 &&
+        s.M >= 4096) {
+      const int64_t rows_per_cta = 8 * kSkRows;
+      dim3 grid(unsigned((s.M + rows_per_cta - 1) / rows_per_cta), 1, unsigned(s.D * p.nbatch));
+      k_gemm_skinny<<<grid, 256, size_t(kSkN) * s.K * sizeof(float2), stream>>>(s, p);
+      return cudaGetLastError();
+    }
+  }
   const int64_t tiles = ((s.M + 63) / 64) * ((s.N + 63) / 64);
   dim3 grid(unsigned(tiles), 1, unsigned(s.D * p.nbatch));
   if (exact)
