@@ -516,14 +516,21 @@ size_t splitk_workspace_bytes(const StridedGeom &g, const DotTables &t, int nbat
 // all its rows; the 32 lane partials of each output are summed with xor shuffles.
 constexpr int kSkRows = 4, kSkN = 8;
 __global__ void __launch_bounds__(256)
-    k_gemm_skinny(const GemmShape s, const BatchPtrs p) {
-  extern __shared__ __align__(16) float2 bt[];  // [kSkN][K]
+    k_gemm_skinny(const GemmShape s, const BatchPtrs p, const int64_t *gtab, int mbits) {
+  extern __shared__ __align__(16) float2 bt[];  // [kSkN][K], then (gather) [K] k offsets
   const int64_t batch = blockIdx.z;  // = slice * D + d
   const int64_t slice = batch / s.D, d = batch % s.D;
   const float2 *A = static_cast<const float2 *>(p.a) + slice * p.a_bs + d * s.M * s.K;
   const float2 *B = static_cast<const float2 *>(p.b) + slice * p.b_bs + d * s.K * s.N;
   float2 *C = static_cast<float2 *>(p.out) + slice * p.out_bs + d * s.M * s.N;
   const int K = int(s.K), N = int(s.N);
+  // gather form (gtab): A is the step's operand in its own layout; element (m, k) sits
+  // at mo(m) + ko(k), ko = gtab[0..K), mo = sum of the bit strides gtab[K + j]
+  int64_t *ko = reinterpret_cast<int64_t *>(bt + kSkN * K);
+  if (gtab) {
+    A = static_cast<const float2 *>(p.a) + slice * p.a_bs;
+    for (int k = threadIdx.x; k < K; k += 256) ko[k] = gtab[k];
+  }
   for (int e = threadIdx.x; e < kSkN * K; e += 256) {
     const int n = e / K, k = e % K;
     bt[e] = n < N ? B[int64_t(k) * N + n] : make_float2(0.f, 0.f);
@@ -537,11 +544,23 @@ __global__ void __launch_bounds__(256)
   for (int r = 0; r < kSkRows; ++r)
 #pragma unroll
     for (int n = 0; n < kSkN; ++n) acc[r][n] = make_float2(0.f, 0.f);
+  int64_t row[kSkRows];
+#pragma unroll
+  for (int r = 0; r < kSkRows; ++r) {
+    row[r] = (m0 + r) * K;
+    if (gtab) {
+      int64_t o = 0;
+      for (int j = 0; j < mbits; ++j)
+        if (((m0 + r) >> j) & 1) o += gtab[K + j];
+      row[r] = o;
+    }
+  }
   for (int k = 2 * lane; k < K; k += 64) {
+    const int64_t kof = gtab ? ko[k] : k;
     float4 x[kSkRows];
 #pragma unroll
     for (int r = 0; r < kSkRows; ++r)
-      x[r] = m0 + r < s.M ? __ldcs(reinterpret_cast<const float4 *>(A + (m0 + r) * K + k))
+      x[r] = m0 + r < s.M ? __ldcs(reinterpret_cast<const float4 *>(A + row[r] + kof))
                           : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int n = 0; n < kSkN; ++n) {
@@ -572,6 +591,21 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+bool gemm_skinny_supported(const GemmShape &s) {
+  return s.D == 1 && s.N <= kSkN && s.K % 2 == 0 && s.K >= 64 && s.K * kSkN <= 4096 &&
+         s.M >= 4096;
+}
+
+cudaError_t launch_gemm_skinny_gather(const GemmShape &s, const BatchPtrs &p, const int64_t *gtab,
+                                      int mbits, cudaStream_t stream) {
+  if (!gemm_skinny_supported(s)) return cudaErrorNotSupported;
+  const int64_t rows_per_cta = 8 * kSkRows;
+  dim3 grid(unsigned((s.M + rows_per_cta - 1) / rows_per_cta), 1, unsigned(p.nbatch));
+  k_gemm_skinny<<<grid, 256, size_t(kSkN) * s.K * sizeof(float2) + 8 * size_t(s.K), stream>>>(
+      s, p, gtab, mbits);
+  return cudaGetLastError();
+}
+
 template <class R>
 cudaError_t launch_gemm_simt(const GemmShape &s, const BatchPtrs &p, bool exact,
                              cudaStream_t stream) {
@@ -581,7 +615,7 @@ cudaError_t launch_gemm_simt(const GemmShape &s, const BatchPtrs &p, bool exact,
         s.M >= 4096) {
       const int64_t rows_per_cta = 8 * kSkRows;
       dim3 grid(unsigned((s.M + rows_per_cta - 1) / rows_per_cta), 1, unsigned(s.D * p.nbatch));
-      k_gemm_skinny<<<grid, 256, size_t(kSkN) * s.K * sizeof(float2), stream>>>(s, p);
+      k_gemm_skinny<<<grid, 256, size_t(kSkN) * s.K * sizeof(float2), stream>>>(s, p, nullptr, 0);
       return cudaGetLastError();
     }
   }

@@ -233,6 +233,11 @@ cudaError_t launch_splitk(const StridedGeom &g, const BatchPtrs &p, const DotTab
                           void *workspace, cudaStream_t stream);
 size_t splitk_workspace_bytes(const StridedGeom &g, const DotTables &t, int nbatch,
                               size_t esize);
+// Skinny GEMM reading A straight from the step operand's own layout (FAST, float):
+// gtab = [K] offsets of k, then [mbits] offsets of the M index bits.
+bool gemm_skinny_supported(const GemmShape &s);
+cudaError_t launch_gemm_skinny_gather(const GemmShape &s, const BatchPtrs &p, const int64_t *gtab,
+                                      int mbits, cudaStream_t stream);
 template <class R>
 cudaError_t launch_gemm_simt(const GemmShape &s, const BatchPtrs &p, bool exact,
                              cudaStream_t stream);

@@ -210,6 +210,8 @@ struct StepPlan {
   bool pa_tiled = false, pb_tiled = false, pc_tiled = false;  // bond-2 tiled permutes
   stn::PermTileGeom pat{}, pbt{}, pct{};                         // high-occupancy tile permutes
   std::shared_ptr<DevBuf> pa_bases, pb_bases, pc_bases;
+  std::shared_ptr<DevBuf> skinny_tab;  // gathered skinny GEMM: k offsets, M bit strides
+  int skinny_mbits = 0;
   stn::AbsorbGeom pag{}, pbg{}, pcg{};
   stn::GemmShape gs{};
   bool gemm_swap = false;            // operands exchanged: C^T = B^T A^T
@@ -869,6 +871,29 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
       tiles(sp.a_id, adims, sp.gl, sp.pat, sp.pa_bases);
       tiles(sp.b_id, bdims, sp.gr, sp.pbt, sp.pb_bases);
       tiles(sp.c_id, prod_dims, sp.go, sp.pct, sp.pc_bases);
+      // FAST skinny GEMM (N <= 8): read A through offset tables instead of permuting it
+      bool all2 = true;
+      for (int x : adims) all2 &= x == 2;
+      const int nmb = __builtin_ctzll(uint64_t(sp.gs.M)), nkb = __builtin_ctzll(uint64_t(sp.gs.K));
+      if (!exact && sp.kern == Kern::GemmSimt && !sp.gemm_swap && !sp.a_id && all2 &&
+          stn::gemm_skinny_supported(sp.gs) && int(adims.size()) == nmb + nkb &&
+          (int64_t(1) << nmb) == sp.gs.M && (int64_t(1) << nkb) == sp.gs.K) {
+        const int r = int(adims.size());
+        std::vector<int64_t> tab(size_t(sp.gs.K + nmb));
+        for (int64_t k = 0; k < sp.gs.K; ++k) {
+          int64_t off = 0;
+          for (int j = 0; j < nkb; ++j)
+            if ((k >> j) & 1) off += int64_t(1) << (r - 1 - sp.gl[r - 1 - j]);
+          tab[size_t(k)] = off;
+        }
+        for (int j = 0; j < nmb; ++j)
+          tab[size_t(sp.gs.K + j)] = int64_t(1) << (r - 1 - sp.gl[r - 1 - nkb - j]);
+        if (tab[1] == 1) {  // k pairs contiguous: 16-byte loads
+          sp.skinny_tab = std::make_shared<DevBuf>();
+          sp.skinny_tab->upload(tab);
+          sp.skinny_mbits = nmb;
+        }
+      }
     }
   }
 }
@@ -1943,6 +1968,8 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
         prof.done(STN_KERNEL_PERMUTE, (es + 2 * es) * asize * nb, 0);
         ga = nullptr;
         ga_bs = asize;
+      } else if (sp.skinny_tab) {
+        // gathered by the skinny GEMM itself
       } else if (!sp.a_id) {
         void *dst = elem_ptr(P, P.arena.ptr, op.scr_a * nb);
         if (sp.pa_bases)
@@ -1992,6 +2019,13 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
                   std::string("tcgen05 gemm: ") + cudaGetErrorString(e));
           cudaGetLastError();
         }
+      }
+      if (!done && sp.skinny_tab) {
+        cuda_check(stn::launch_gemm_skinny_gather(sp.gs, p, sp.skinny_tab->as<int64_t>(),
+                                                  sp.skinny_mbits, st),
+                   "skinny gemm");
+        prof.done(STN_KERNEL_GEMM_SIMT, gbytes, flops);
+        done = true;
       }
       if (!done) {
         cuda_check(stn::launch_gemm_simt<R>(sp.gs, p, exact, st), "gemm kernel");
