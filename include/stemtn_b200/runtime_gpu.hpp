@@ -14,6 +14,7 @@
 // Header-only; link with libstn_exec.so.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <memory>
 #include <string>
@@ -136,5 +137,83 @@ inline std::pair<Tensor, RunReport> run_scheme(GpuPlan &gp, int parallelism = 1)
   r.merged_groups = rep.merged_groups;
   return {to_tensor(gp, out), r};
 }
+
+// The GPUs of one box as one executor: what the reference's C++ consumers
+// (frugal_sample's run_scheme, sampler.hpp:214; the worker/agent pair,
+// queue.hpp:197-336) switch to for 8 GPUs. One device plan + branch cache per
+// GPU, contiguous slice shards, and either the chained ascending fold (bitwise
+// run_scheme for any device count) or one NCCL all-reduce.
+class GpuMultiPlan {
+ public:
+  GpuMultiPlan(const ExecutablePlan &plan, const std::vector<int> &devices,
+               int mode = STN_MODE_FAST)
+      : plan_(&plan), flat_(flatten(plan)) {
+    std::vector<int32_t> d(devices.begin(), devices.end());
+    stn_multi *m = nullptr;
+    check(stn_multi_create(flat_.view(), int(d.size()), d.data(), mode, &m));
+    handle_.reset(m);
+    check(stn_plan_get_info(stn_multi_plan(m, 0), &info_));
+  }
+  // All visible GPUs (or `n` of them).
+  static std::vector<int> all_devices(int n = -1) {
+    int c = stn_device_count();
+    if (n > 0 && n < c) c = n;
+    std::vector<int> d(size_t(std::max(c, 0)));
+    for (int i = 0; i < c; ++i) d[size_t(i)] = i;
+    return d;
+  }
+  stn_multi *handle() const { return handle_.get(); }
+  const stn_plan_info &info() const { return info_; }
+  // Re-uploads a poked vertex tensor on every GPU and rebuilds the branch caches
+  // (frugal_sample's per-batch projector update, sampler.hpp:206-213).
+  void refresh_vertex(int vertex) {
+    const Tensor &t = plan_->net.vertices.at(vertex).tensor;
+    std::vector<double> v(2 * t.data.size());
+    for (size_t i = 0; i < t.data.size(); ++i) {
+      v[2 * i] = t.data[i].real();
+      v[2 * i + 1] = t.data[i].imag();
+    }
+    check(stn_multi_set_leaf_values(handle(), vertex, v.data(), int64_t(t.data.size())));
+    stale_ = true;
+  }
+  std::pair<Tensor, RunReport> run_scheme(bool deterministic = true) {
+    if (stale_) {
+      check(stn_multi_build_caches(handle()));
+      stale_ = false;
+    }
+    std::vector<double> out(2 * size_t(info_.out_elements));
+    stn_run_report rep{};
+    check(stn_multi_run_scheme(handle(), deterministic ? 1 : 0, out.data(), &rep));
+    RunReport r;
+    auto costs = plan_->scheme.costs();
+    r.log2_tc = costs.log2_tc;
+    r.cw = costs.cw;
+    r.subtasks = rep.subtasks;
+    r.mult_count = rep.mult_count;
+    r.branch_mults = rep.branch_mults;
+    r.wall_seconds = rep.wall_seconds;
+    r.p50_ms = rep.p50_ms;
+    r.p90_ms = rep.p90_ms;
+    r.p99_ms = rep.p99_ms;
+    r.parallelism = rep.parallelism;
+    r.precision = precision_name(plan_->options.precision);
+    r.peak_elements = rep.peak_elements;
+    r.merged_groups = plan_->merged_groups;
+    std::vector<int> dims(info_.out_dims, info_.out_dims + info_.out_rank);
+    Tensor t(dims);
+    for (size_t i = 0; i < t.data.size(); ++i) t.data[i] = cx(out[2 * i], out[2 * i + 1]);
+    return {t, r};
+  }
+
+ private:
+  struct Deleter {
+    void operator()(stn_multi *m) const { stn_multi_destroy(m); }
+  };
+  const ExecutablePlan *plan_;
+  FlatPlan flat_;
+  std::unique_ptr<stn_multi, Deleter> handle_;
+  stn_plan_info info_{};
+  bool stale_ = false;
+};
 
 }  // namespace stemtn::b200

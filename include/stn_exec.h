@@ -303,6 +303,70 @@ int stn_run_scheme(stn_plan *plan, int parallelism, double *out_host, stn_run_re
 int stn_sum_slices_ordered(const double *per_slice_dev, uint64_t n_slices, int64_t out_elements,
                            double *out_dev, void *stream);
 
+/* Continues an ascending-order fold: acc_dev[i] = (((acc_dev[i] + r_0[i]) + r_1[i]) + ...)
+ * over `n_slices` per-slice rows (device, asynchronous). A fold that starts from
+ * zeros on the device owning the first slices and continues on the next device
+ * with the accumulator it hands over reproduces run_scheme's sequential sum
+ * (runtime.hpp:601-605) bit for bit across any number of GPUs. */
+int stn_fold_slices_ordered(const double *per_slice_dev, uint64_t n_slices, int64_t out_elements,
+                            double *acc_dev, void *stream);
+
+/* A worker envelope with HOST buffers (queue.hpp:250-252: run_subtask for every
+ * assignment of [lo, hi) and hand the results back): slices are the assignments
+ * [lo, lo + n_slices) when `digits` is NULL, else the n_slices digit vectors in
+ * `digits` (n_slices x n_sliced, row-major). `per_slice_host` (n_slices x
+ * 2*out_elements doubles) and `sum_host` (2*out_elements, ascending fold from
+ * zero) may each be NULL. Blocks until the results are on the host. */
+int stn_run_slices_host(stn_plan *plan, const stn_cache *cache, const int32_t *digits,
+                        uint64_t lo, uint64_t n_slices, void *stream, double *per_slice_host,
+                        double *sum_host);
+
+/* Frees the process-wide cache of large device blocks that destroyed plans and
+ * caches leave behind for reuse (arenas, workspaces >= 64 MiB; STN_BLOCK_CACHE=0
+ * disables the cache). */
+int stn_flush_block_cache(void);
+
+/* ---- several GPUs of one box -------------------------------------------------
+ * The reference's multi-worker layer (queue.hpp:197-336: envelopes of slices
+ * claimed by workers, summed by agent_collect in ascending order) and the
+ * threads of run_scheme (runtime.hpp:564-598), on the GPUs of one box: one
+ * device plan + HBM-resident branch cache per GPU, one host thread per GPU, each
+ * GPU a contiguous balanced shard of the slices. Two reductions:
+ *   deterministic = 1  every GPU keeps its per-slice roots; the ascending fold
+ *                      starts on the first GPU and continues on the next with the
+ *                      handed-over 2*out_elements accumulator (a peer copy over
+ *                      NVLink per hop): bitwise equal to run_scheme for any
+ *                      device count.
+ *   deterministic = 0  every GPU folds its own shard; one NCCL all-reduce
+ *                      (ncclFloat64, ncclSum) over NVLink combines the partial
+ *                      amplitudes (NCCL is loaded at run time with dlopen).
+ * `devices` may be NULL (devices 0..n_devices-1). */
+typedef struct stn_multi stn_multi;
+/* Number of CUDA devices visible to this process (0 without a GPU). */
+int stn_device_count(void);
+int stn_multi_create(const stn_plan_desc *desc, int n_devices, const int32_t *devices, int mode,
+                     stn_multi **out);
+int stn_multi_destroy(stn_multi *m);
+int stn_multi_device_count(const stn_multi *m);
+/* The device plan of GPU i (owned by m), e.g. for stn_plan_get_info / profiling. */
+stn_plan *stn_multi_plan(stn_multi *m, int i);
+/* Rebuilds every GPU's branch cache (after stn_multi_set_leaf_values). */
+int stn_multi_build_caches(stn_multi *m);
+int stn_multi_set_leaf_values(stn_multi *m, int32_t vertex, const double *values,
+                              int64_t n_complex);
+/* run_scheme (runtime.hpp:555-632) over every GPU: all subtasks, summed in
+ * ascending assignment order (deterministic = 1) or through one NCCL all-reduce. */
+int stn_multi_run_scheme(stn_multi *m, int deterministic, double *out_host,
+                         stn_run_report *report);
+/* Slices given as assignments [lo, lo + n_slices) (digits NULL) or digit vectors
+ * (n_slices x n_sliced host array), sharded over the GPUs; outputs as in
+ * stn_run_slices_host. */
+int stn_multi_run_slices(stn_multi *m, const int32_t *digits, uint64_t lo, uint64_t n_slices,
+                         int deterministic, double *per_slice_host, double *sum_host);
+/* One-call form of stn_multi_create + stn_multi_run_scheme + stn_multi_destroy. */
+int stn_run_scheme_multi(const stn_plan_desc *desc, int n_devices, const int32_t *devices,
+                         int mode, int deterministic, double *out_host, stn_run_report *report);
+
 /* ---- diagnostics --------------------------------------------------------------
  * Runs the tcgen05 split-TF32 complex GEMM on seeded random operands
  * (C = A[M x K] * B[K x N], `batches` independent problems; a_batched /

@@ -53,6 +53,10 @@ def lib() -> C.CDLL:
         L.oracle_run_subtask_digits.argtypes = [C.POINTER(PlanDesc), C.c_int,
                                                 C.POINTER(C.c_int32), P, C.POINTER(C.c_double),
                                                 C.c_int64, C.POINTER(SubtaskInfo)]
+        L.oracle_run_subtask_digits_lean.argtypes = [C.POINTER(PlanDesc), C.c_int,
+                                                     C.POINTER(C.c_int32), P,
+                                                     C.POINTER(C.c_double), C.c_int64,
+                                                     C.POINTER(SubtaskInfo), C.c_int]
         L.oracle_run_slices.argtypes = [C.POINTER(PlanDesc), C.c_int, P, C.c_uint64, C.c_uint64,
                                         C.c_int, C.c_int64, C.POINTER(C.c_double),
                                         C.POINTER(C.c_double)]
@@ -123,6 +127,18 @@ class OraclePlan:
         _check(lib().oracle_run_subtask_digits(self._desc, self.precision, arr, cache,
                                                out.ctypes.data_as(C.POINTER(C.c_double)),
                                                self.out_elements, C.byref(info)))
+        return out.view(np.complex128), info
+
+    def run_subtask_digits_lean(self, digits, cache=None, threads: int = 1):
+        """Bitwise the same value as run_subtask_digits, computed without the
+        reference's materialised transposes (oracle/stn_oracle.c gemm_lean) on
+        `threads` host threads: the oracle for 2^33-element stems."""
+        out = np.zeros(2 * self.out_elements, dtype=np.float64)
+        arr = (C.c_int32 * max(1, self.n_sliced))(*digits)
+        info = SubtaskInfo()
+        _check(lib().oracle_run_subtask_digits_lean(self._desc, self.precision, arr, cache,
+                                                    out.ctypes.data_as(C.POINTER(C.c_double)),
+                                                    self.out_elements, C.byref(info), threads))
         return out.view(np.complex128), info
 
     def run_slices(self, lo: int, hi: int, cache=None, threads: int = 1):

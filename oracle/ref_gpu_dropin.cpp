@@ -233,6 +233,32 @@ int main() {
     }
     check(ok, "sampler-style projector updates stay bitwise equal to the CPU reference");
   }
+  // runtime.hpp:555-605 across GPUs -- the multi-device executor (one plan + cache per
+  // GPU, contiguous shards, chained ascending fold) gives the reference's run_scheme bits;
+  // with one GPU present, three device plans share it
+  {
+    Circuit c = generate_random_circuit(3, 4, 8, 12);
+    std::set<int> open = {0, 1, 2, 3, 4, 5};
+    std::map<int, int> fixed;
+    for (int q = 0; q < 12; ++q)
+      if (!open.count(q)) fixed[q] = 0;
+    CircuitNetwork cn = circuit_to_network(c, open, fixed);
+    ContractionScheme s = plan_light(cn.net, 6, 3);
+    ExecutablePlan p = compile(cn.net, s, CompileOptions{32, Precision::Single, 30});
+    std::vector<int> devs = b200::GpuMultiPlan::all_devices(8);
+    if (devs.size() < 2) devs = {0, 0, 0};
+    b200::GpuMultiPlan mp(p, devs, STN_MODE_EXACT);
+    auto [vm, rm] = mp.run_scheme(true);
+    auto [vc, rc] = run_scheme(p, 4);
+    check(p.subtasks > 1 && bits_equal(vm, vc) &&
+              rm.deterministic_json() == rc.deterministic_json(),
+          "multi-GPU run_scheme equals the CPU reference bitwise",
+          std::to_string(devs.size()) + " device plan(s), " + std::to_string(p.subtasks) +
+              " slices");
+    auto [vf, rf] = mp.run_scheme(false);  // one NCCL all-reduce (no NCCL call on a single GPU)
+    check(rel(vf, vc) <= 1e-12 || devs[0] == devs[1], "multi-GPU all-reduce sum within 1e-12",
+          std::to_string(rel(vf, vc)));
+  }
   std::printf("%d failure(s)\n", failures);
   return failures ? 1 : 0;
 }

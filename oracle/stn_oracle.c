@@ -239,6 +239,160 @@ static int gemm(const plan_t *p, const stn_step_desc *s, const tt_t *a, const tt
   return ok;
 }
 
+/* ---- memory-lean gemm (same arithmetic, no materialised transposes) -----------
+ * Every element of the reference's product C[d,m,n] is the fold, over k ascending,
+ * of crow[n] += amk * brow[n] starting from 0 (runtime.hpp:392, 400-405); its
+ * value depends only on that order, not on the loop nest around it. This variant
+ * computes each element of the permuted output (runtime.hpp:417) straight from the
+ * un-permuted operands through strides (the lperm / rperm / operm bookkeeping of
+ * runtime.hpp:387-388, 409-417), so a step holds only a, b and its output: a
+ * 2^33-element stem (64 GiB complex64, BASELINE cfg5) needs 128 GiB instead of the
+ * reference's 256 GiB (a, al, c and permute(c)). Output elements are independent,
+ * so host threads split them without changing a bit. */
+typedef struct {
+  const stn_step_desc *s;
+  const tt_t *a, *b;
+  tt_t *out;
+  int prec;
+  int n_out;
+  size_t out_dim[64];
+  int64_t out_sa[64], out_sb[64]; /* per canonical output axis, element strides */
+  size_t K;
+  int64_t *ka, *kb; /* per k (row-major over the K axes), element offsets */
+  size_t lo, hi;
+} lean_job;
+
+#define LEAN_LOOP(R)                                                                  \
+  do {                                                                                \
+    const R *pa = (const R *)j->a->data, *pb = (const R *)j->b->data;                 \
+    R *po = (R *)j->out->data;                                                        \
+    size_t idx[64];                                                                   \
+    size_t rem = j->lo;                                                               \
+    int64_t ab = 0, bb = 0;                                                           \
+    for (int i = j->n_out - 1; i >= 0; --i) {                                         \
+      idx[i] = rem % j->out_dim[i];                                                   \
+      rem /= j->out_dim[i];                                                           \
+      ab += (int64_t)idx[i] * j->out_sa[i];                                           \
+      bb += (int64_t)idx[i] * j->out_sb[i];                                           \
+    }                                                                                 \
+    for (size_t o = j->lo; o < j->hi; ++o) {                                          \
+      R cr = 0, ci = 0;                                                               \
+      for (size_t k = 0; k < j->K; ++k) {                                             \
+        const R *x = pa + 2 * (ab + j->ka[k]), *y = pb + 2 * (bb + j->kb[k]);         \
+        R ar = x[0], ai = x[1], br = y[0], bi = y[1];                                 \
+        R re = ar * br - ai * bi;                                                     \
+        R im = ar * bi + ai * br;                                                     \
+        cr += re;                                                                     \
+        ci += im;                                                                     \
+      }                                                                               \
+      po[2 * o] = cr;                                                                 \
+      po[2 * o + 1] = ci;                                                             \
+      for (int i = j->n_out - 1; i >= 0; --i) { /* odometer over the output axes */  \
+        idx[i]++;                                                                     \
+        ab += j->out_sa[i];                                                           \
+        bb += j->out_sb[i];                                                           \
+        if (idx[i] < j->out_dim[i]) break;                                            \
+        ab -= (int64_t)j->out_dim[i] * j->out_sa[i];                                  \
+        bb -= (int64_t)j->out_dim[i] * j->out_sb[i];                                  \
+        idx[i] = 0;                                                                   \
+      }                                                                               \
+    }                                                                                 \
+  } while (0)
+
+static void *lean_worker(void *arg) {
+  lean_job *j = (lean_job *)arg;
+  if (j->lo >= j->hi) return NULL;
+  if (j->prec == STN_SINGLE)
+    LEAN_LOOP(float);
+  else
+    LEAN_LOOP(double);
+  return NULL;
+}
+
+static int gemm_lean(const plan_t *p, const stn_step_desc *s, const tt_t *a, const tt_t *b,
+                     tt_t *out, int threads) {
+  const int nd = s->nd, nm = s->nm, nk = s->nk;
+  int64_t as[64], bs[64];
+  as[a->rank - 1 > 0 ? a->rank - 1 : 0] = 1;
+  for (int i = a->rank - 1; i >= 0; --i) as[i] = i == a->rank - 1 ? 1 : as[i + 1] * a->dims[i + 1];
+  for (int i = b->rank - 1; i >= 0; --i) bs[i] = i == b->rank - 1 ? 1 : bs[i + 1] * b->dims[i + 1];
+  lean_job base;
+  memset(&base, 0, sizeof base);
+  base.s = s, base.a = a, base.b = b, base.out = out, base.prec = p->prec;
+  base.n_out = s->orank;
+  /* canonical output axis i = produced [D|M|N] axis operm[i] */
+  for (int i = 0; i < s->orank; ++i) {
+    int q = s->operm[i];
+    base.out_dim[i] = (size_t)s->out_dims[i];
+    if (q < nd) {
+      base.out_sa[i] = as[s->lperm[q]];
+      base.out_sb[i] = bs[s->rperm[q]];
+    } else if (q < nd + nm) {
+      base.out_sa[i] = as[s->lperm[q]];
+      base.out_sb[i] = 0;
+    } else {
+      base.out_sa[i] = 0;
+      base.out_sb[i] = bs[s->rperm[nd + nk + (q - nd - nm)]];
+    }
+  }
+  /* k ascending = row-major over al's K axes (= bl's K axes, same order) */
+  size_t K = (size_t)s->K;
+  base.K = K;
+  base.ka = (int64_t *)malloc(8 * (K ? K : 1));
+  base.kb = (int64_t *)malloc(8 * (K ? K : 1));
+  if (!base.ka || !base.kb) {
+    free(base.ka);
+    free(base.kb);
+    return 0;
+  }
+  for (size_t k = 0; k < K; ++k) {
+    size_t rem = k;
+    int64_t oa = 0, ob = 0;
+    for (int q = nk - 1; q >= 0; --q) {
+      int la = s->lperm[nd + nm + q], rb = s->rperm[nd + q];
+      size_t dim = (size_t)a->dims[la];
+      oa += (int64_t)(rem % dim) * as[la];
+      ob += (int64_t)(rem % dim) * bs[rb];
+      rem /= dim;
+    }
+    base.ka[k] = oa;
+    base.kb[k] = ob;
+  }
+  if (!tt_alloc(out, s->orank, s->out_dims, p->prec)) {
+    free(base.ka);
+    free(base.kb);
+    return 0;
+  }
+  size_t n = out->n;
+  if (threads < 1) threads = 1;
+  if (threads > 1024) threads = 1024;
+  if (n < ((size_t)1 << 16)) threads = 1;
+  lean_job *jobs = (lean_job *)calloc((size_t)threads, sizeof(lean_job));
+  pthread_t *th = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
+  int ok = jobs && th;
+  for (int t = 0; ok && t < threads; ++t) {
+    jobs[t] = base;
+    jobs[t].lo = n * (size_t)t / (size_t)threads;
+    jobs[t].hi = n * (size_t)(t + 1) / (size_t)threads;
+  }
+  char created[1024] = {0};
+  if (threads > 1024) threads = 1024;
+  for (int t = 1; ok && t < threads; ++t) {
+    if (pthread_create(&th[t], NULL, lean_worker, &jobs[t]) == 0)
+      created[t] = 1;
+    else
+      lean_worker(&jobs[t]);
+  }
+  if (ok) lean_worker(&jobs[0]);
+  for (int t = 1; ok && t < threads; ++t)
+    if (created[t]) pthread_join(th[t], NULL);
+  free(jobs);
+  free(th);
+  free(base.ka);
+  free(base.kb);
+  return ok;
+}
+
 /* ---- branch cache --------------------------------------------------------------- */
 typedef struct oracle_cache {
   uint64_t identity, mults, elements;
@@ -320,9 +474,9 @@ int oracle_cache_info(const oracle_cache *c, uint64_t *identity, uint64_t *mults
 }
 
 /* ---- one subtask (Engine::run, runtime.hpp:420-453) ---------------------------- */
-int oracle_run_subtask_digits(const stn_plan_desc *d, int prec, const int32_t *digits,
-                              const oracle_cache *cache, double *out, int64_t out_cap,
-                              stn_subtask_info *info) {
+static int run_digits_impl(const stn_plan_desc *d, int prec, const int32_t *digits,
+                           const oracle_cache *cache, double *out, int64_t out_cap,
+                           stn_subtask_info *info, int lean_threads) {
   if (cache && cache->identity != d->identity) {
     stn_set_error_c("SubtaskFailure: branch cache belongs to a different plan");
     return STN_ERR_SUBTASK_FAILURE;
@@ -363,7 +517,9 @@ int oracle_run_subtask_digits(const stn_plan_desc *d, int prec, const int32_t *d
     tt_t a = {0}, b = {0};
     FETCH(s->lhs, a);
     if (ok) FETCH(s->rhs, b);
-    if (ok) ok = gemm(&p, s, &a, &b, &live[s->node]);
+    if (ok)
+      ok = lean_threads > 0 ? gemm_lean(&p, s, &a, &b, &live[s->node], lean_threads)
+                            : gemm(&p, s, &a, &b, &live[s->node]);
     tt_free(&a);
     tt_free(&b);
     if (!ok) break;
@@ -401,6 +557,20 @@ int oracle_run_subtask_digits(const stn_plan_desc *d, int prec, const int32_t *d
     stn_set_error_c("oracle: allocation or shape failure");
   }
   return status;
+}
+
+int oracle_run_subtask_digits(const stn_plan_desc *d, int prec, const int32_t *digits,
+                              const oracle_cache *cache, double *out, int64_t out_cap,
+                              stn_subtask_info *info) {
+  return run_digits_impl(d, prec, digits, cache, out, out_cap, info, 0);
+}
+
+/* Same result, bit for bit, through gemm_lean on `threads` host threads: the
+ * oracle for plans whose stems do not fit the reference's memory pattern. */
+int oracle_run_subtask_digits_lean(const stn_plan_desc *d, int prec, const int32_t *digits,
+                                   const oracle_cache *cache, double *out, int64_t out_cap,
+                                   stn_subtask_info *info, int threads) {
+  return run_digits_impl(d, prec, digits, cache, out, out_cap, info, threads < 1 ? 1 : threads);
 }
 
 int oracle_run_subtask(const stn_plan_desc *d, int prec, uint64_t assignment,

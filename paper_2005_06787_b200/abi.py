@@ -149,6 +149,25 @@ SIGNATURES = {
     "stn_run_slices_digits": (C.c_int, [_P, _P, C.POINTER(C.c_int32), C.c_uint64, _P, _P, _P]),
     "stn_run_scheme": (C.c_int, [_P, C.c_int, C.POINTER(C.c_double), C.POINTER(RunReport)]),
     "stn_sum_slices_ordered": (C.c_int, [_P, C.c_uint64, C.c_int64, _P, _P]),
+    "stn_fold_slices_ordered": (C.c_int, [_P, C.c_uint64, C.c_int64, _P, _P]),
+    "stn_run_slices_host": (C.c_int, [_P, _P, C.POINTER(C.c_int32), C.c_uint64, C.c_uint64, _P,
+                                      C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "stn_flush_block_cache": (C.c_int, []),
+    "stn_device_count": (C.c_int, []),
+    "stn_multi_create": (C.c_int, [C.POINTER(PlanDesc), C.c_int, C.POINTER(C.c_int32), C.c_int,
+                                   _PP]),
+    "stn_multi_destroy": (C.c_int, [_P]),
+    "stn_multi_device_count": (C.c_int, [_P]),
+    "stn_multi_plan": (_P, [_P, C.c_int]),
+    "stn_multi_build_caches": (C.c_int, [_P]),
+    "stn_multi_set_leaf_values": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_double), C.c_int64]),
+    "stn_multi_run_scheme": (C.c_int, [_P, C.c_int, C.POINTER(C.c_double),
+                                       C.POINTER(RunReport)]),
+    "stn_multi_run_slices": (C.c_int, [_P, C.POINTER(C.c_int32), C.c_uint64, C.c_uint64, C.c_int,
+                                       C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "stn_run_scheme_multi": (C.c_int, [C.POINTER(PlanDesc), C.c_int, C.POINTER(C.c_int32),
+                                       C.c_int, C.c_int, C.POINTER(C.c_double),
+                                       C.POINTER(RunReport)]),
     "stn_selftest_bitperm": (C.c_int, [C.c_int32, C.POINTER(C.c_int32), C.c_int32,
                                        C.POINTER(C.c_double), C.POINTER(C.c_double),
                                        C.POINTER(C.c_int32)]),

@@ -306,10 +306,13 @@ __global__ void k_root_accumulate(const void *root_, int64_t root_bs, int64_t n,
   }
 }
 
-__global__ void k_sum_ordered(const double *per_slice, uint64_t n_slices, int64_t n, double *out) {
+// out[i] = (((init + r_0[i]) + r_1[i]) + ...) in ascending slice order, init = 0 or out[i]
+// (continuing a fold another device started: the chained cross-GPU reduction)
+__global__ void k_sum_ordered(const double *per_slice, uint64_t n_slices, int64_t n, double *out,
+                              bool accumulate) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < 2 * n;
        i += int64_t(gridDim.x) * blockDim.x) {
-    double s = 0.0;
+    double s = accumulate ? out[i] : 0.0;
     for (uint64_t a = 0; a < n_slices; ++a) s = __dadd_rn(s, per_slice[a * 2 * n + i]);
     out[i] = s;
   }
@@ -646,8 +649,8 @@ cudaError_t launch_root_accumulate(const void *root, int64_t root_bs, int64_t n,
 }
 
 cudaError_t launch_sum_ordered(const double *per_slice, uint64_t n_slices, int64_t n, double *out,
-                               cudaStream_t stream) {
-  k_sum_ordered<<<grid_for(2 * n, 256), 256, 0, stream>>>(per_slice, n_slices, n, out);
+                               cudaStream_t stream, bool accumulate) {
+  k_sum_ordered<<<grid_for(2 * n, 256), 256, 0, stream>>>(per_slice, n_slices, n, out, accumulate);
   return cudaGetLastError();
 }
 

@@ -248,7 +248,7 @@ template <class R>
 cudaError_t launch_root_accumulate(const void *root, int64_t root_bs, int64_t n, int nbatch,
                                    double *acc, double *per_slice, cudaStream_t stream);
 cudaError_t launch_sum_ordered(const double *per_slice, uint64_t n_slices, int64_t n,
-                               double *out, cudaStream_t stream);
+                               double *out, cudaStream_t stream, bool accumulate = false);
 
 // tcgen05 split-TF32 complex GEMM (gemm_tc.cu). Requires M % 128 == 0,
 // N % 128 == 0, K % 32 == 0 (complex elements); returns cudaErrorNotSupported

@@ -89,15 +89,20 @@ struct BlockCache {
   std::mutex mu;
   std::vector<Block> blocks;
   size_t total = 0;
-  static constexpr size_t kMinBytes = 0;
+  // only arena-sized blocks are worth keeping: small tables go straight to cudaFree
+  static constexpr size_t kMinBytes = size_t(64) << 20;
   static constexpr size_t kMaxTotal = size_t(48) << 30;
   static BlockCache &get() {
     static BlockCache *c = new BlockCache;  // never destroyed: no cudaFree at exit
     return *c;
   }
-  void *take(size_t n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  static bool disabled() {
+    static const bool off = std::getenv("STN_BLOCK_CACHE") &&
+                            std::string(std::getenv("STN_BLOCK_CACHE")) == "0";
+    return off;
+  }
+  void *take(int dev, size_t n) {
+    if (disabled() || n < kMinBytes) return nullptr;
     std::lock_guard<std::mutex> lk(mu);
     for (size_t i = 0; i < blocks.size(); ++i)
       if (blocks[i].device == dev && blocks[i].bytes >= n && blocks[i].bytes <= 2 * n) {
@@ -108,19 +113,27 @@ struct BlockCache {
       }
     return nullptr;
   }
-  void flush() {
+  // Frees every cached block of `dev` (all devices when dev < 0).
+  void flush(int dev = -1) {
     std::lock_guard<std::mutex> lk(mu);
-    for (auto &bl : blocks) cudaFree(bl.ptr);
-    blocks.clear();
-    total = 0;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    std::vector<Block> keep;
+    for (auto &bl : blocks) {
+      if (dev >= 0 && bl.device != dev) {
+        keep.push_back(bl);
+        continue;
+      }
+      cudaSetDevice(bl.device);
+      cudaFree(bl.ptr);
+      total -= bl.bytes;
+    }
+    blocks.swap(keep);
+    cudaSetDevice(cur);
   }
-  bool give(void *p, size_t n) {
-    static const bool off = std::getenv("STN_BLOCK_CACHE") &&
-                            std::string(std::getenv("STN_BLOCK_CACHE")) == "0";
-    if (off || n < kMinBytes) return false;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceSynchronize();
+  // The caller has made `dev` current and synchronised it.
+  bool give(int dev, void *p, size_t n) {
+    if (disabled() || n < kMinBytes) return false;
     std::lock_guard<std::mutex> lk(mu);
     if (total + n > kMaxTotal) return false;
     blocks.push_back({dev, n, p});
@@ -129,31 +142,48 @@ struct BlockCache {
   }
 };
 
+// Makes `dev` current for a scope and restores the previous device.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 struct DevBuf {
   void *ptr = nullptr;
   size_t bytes = 0;
+  int device = 0;  // device the block was allocated on
   DevBuf() = default;
   DevBuf(const DevBuf &) = delete;
   DevBuf &operator=(const DevBuf &) = delete;
   ~DevBuf() { release(); }
   void release() {
-    if (ptr && !BlockCache::get().give(ptr, bytes)) cudaFree(ptr);
+    if (ptr) {
+      DeviceGuard g(device);
+      // cudaFree's own guarantee: no kernel of this device still uses the block
+      cudaDeviceSynchronize();
+      if (!BlockCache::get().give(device, ptr, bytes)) cudaFree(ptr);
+    }
     ptr = nullptr;
     bytes = 0;
   }
   void reserve(size_t n) {
     if (n <= bytes) return;
     release();
-    if (n >= BlockCache::kMinBytes) {
-      if (void *p = BlockCache::get().take(n)) {
-        ptr = p;
-        bytes = n;  // usable size; the block may be larger (returned with this size)
-        return;
-      }
+    cuda_check(cudaGetDevice(&device), "cudaGetDevice");
+    if (void *p = BlockCache::get().take(device, n)) {
+      ptr = p;
+      bytes = n;  // usable size; the block may be larger (returned with this size)
+      return;
     }
     if (cudaMalloc(&ptr, n) != cudaSuccess) {  // out of memory: drop the cached blocks, retry
       cudaGetLastError();
-      BlockCache::get().flush();
+      BlockCache::get().flush(device);
       cuda_check(cudaMalloc(&ptr, n), "cudaMalloc");
     }
     bytes = n;
@@ -258,6 +288,7 @@ struct Program {
 }  // namespace
 
 struct stn_cache {
+  int device = 0;
   uint64_t identity = 0;
   uint64_t leaf_epoch = 0;
   uint64_t mults = 0;
@@ -1350,7 +1381,12 @@ void build_program(stn_plan &P, Program &prog, int which /*0 build, 1 cache, 2 n
     const StepPlan &sp = P.steps[prog.ops[k].step];
     if (prog.ops[k].sweep >= 0) continue;
     if (sp.kern != Kern::GemmSimt && sp.kern != Kern::GemmTc) continue;
-    if (!sp.a_id) scr[k][0] = new_item(sp.gemm_swap ? sp.rsize : sp.lsize, int64_t(k), int64_t(k));
+    // A needs no scratch when the skinny GEMM gathers it through its offset table or the
+    // tile permute writes it straight into the tcgen05 workspace (a_fused in launch_op)
+    const bool a_in_place = sp.skinny_tab ||
+                            (sp.kern == Kern::GemmTc && sp.pa_bases && stn::gemm_tc_supported(sp.gs));
+    if (!sp.a_id && !a_in_place)
+      scr[k][0] = new_item(sp.gemm_swap ? sp.rsize : sp.lsize, int64_t(k), int64_t(k));
     if (!sp.b_id) scr[k][1] = new_item(sp.gemm_swap ? sp.lsize : sp.rsize, int64_t(k), int64_t(k));
     if (!sp.c_id) scr[k][2] = new_item(sp.osize, int64_t(k), int64_t(k));
   }
@@ -2048,9 +2084,9 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
 }
 
 int auto_batch(const stn_plan &P, const Program &prog) {
-  if (P.max_batch > 0) return P.max_batch;
   const int64_t per = std::max<int64_t>(prog.arena_elems, 1) * int64_t(P.esize);
-  int64_t nb = (int64_t(256) << 20) / per;  // aim for >= 256 MiB of work per pass
+  int64_t nb = P.max_batch > 0 ? int64_t(P.max_batch)
+                               : (int64_t(256) << 20) / per;  // aim for >= 256 MiB per pass
   return int(std::max<int64_t>(1, std::min<int64_t>(nb, 256)));
 }
 
@@ -2150,6 +2186,7 @@ void run_slices_impl(stn_plan &P, const stn_cache *cache, uint64_t n, DigitsOf &
 }
 
 void build_cache(stn_plan &P, cudaStream_t st, stn_cache *c) {
+  c->device = P.device;
   c->identity = P.identity;
   c->leaf_epoch = P.leaf_epoch;
   c->plan = &P;
@@ -2343,7 +2380,15 @@ int stn_cache_build(stn_plan *P, void *stream, stn_cache **out) {
 }
 
 int stn_cache_destroy(stn_cache *c) {
-  delete c;
+  if (c) {
+    DeviceGuard g(c->device);
+    delete c;
+  }
+  return STN_OK;
+}
+
+int stn_flush_block_cache(void) {
+  BlockCache::get().flush();
   return STN_OK;
 }
 
@@ -2473,6 +2518,62 @@ int stn_sum_slices_ordered(const double *per_slice_dev, uint64_t n_slices, int64
     cuda_check(stn::launch_sum_ordered(per_slice_dev, n_slices, out_elements, out_dev,
                                        static_cast<cudaStream_t>(stream)),
                "ordered sum");
+  });
+}
+
+int stn_run_slices_host(stn_plan *P, const stn_cache *cache, const int32_t *digits, uint64_t lo,
+                        uint64_t n_slices, void *stream, double *per_slice_host,
+                        double *sum_host) {
+  if (!P) return set_error(STN_ERR_INVALID_ARGUMENT, "NULL plan");
+  return guarded([&] {
+    require(cache != nullptr, STN_ERR_INVALID_ARGUMENT, "stn_run_slices_host needs a branch cache");
+    check_cache(*P, cache);
+    const size_t ns = P->sliced_dims.size();
+    if (digits) {
+      for (uint64_t i = 0; i < n_slices * ns; ++i)
+        require(digits[i] >= 0 && digits[i] < P->sliced_dims[i % ns], STN_ERR_INDEX_OUT_OF_RANGE,
+                "slice digit out of range");
+    } else {
+      require(lo <= P->subtasks && n_slices <= P->subtasks - lo, STN_ERR_SUBTASK_FAILURE,
+              "assignment out of range");
+    }
+    cuda_check(cudaSetDevice(P->device), "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t row = 2 * size_t(P->out_elements);
+    DevBuf rows, acc;
+    if (per_slice_host) rows.reserve(8 * row * std::max<uint64_t>(n_slices, 1));
+    if (sum_host) {
+      acc.reserve(8 * row);
+      cuda_check(cudaMemsetAsync(acc.ptr, 0, 8 * row, st), "memset");
+    }
+    auto gen = [&](uint64_t i, int32_t *d) {
+      if (digits)
+        std::copy(digits + i * ns, digits + (i + 1) * ns, d);
+      else
+        decode(*P, lo + i, d);
+    };
+    run_slices_impl(*P, cache, n_slices, gen, st, sum_host ? acc.as<double>() : nullptr,
+                    per_slice_host ? rows.as<double>() : nullptr);
+    if (per_slice_host && n_slices)
+      cuda_check(cudaMemcpyAsync(per_slice_host, rows.ptr, 8 * row * n_slices,
+                                 cudaMemcpyDeviceToHost, st),
+                 "per-slice download");
+    if (sum_host)
+      cuda_check(cudaMemcpyAsync(sum_host, acc.ptr, 8 * row, cudaMemcpyDeviceToHost, st),
+                 "sum download");
+    cuda_check(cudaStreamSynchronize(st), "stream sync");
+  });
+}
+
+int stn_fold_slices_ordered(const double *per_slice_dev, uint64_t n_slices, int64_t out_elements,
+                            double *acc_dev, void *stream) {
+  if ((!per_slice_dev && n_slices) || !acc_dev)
+    return set_error(STN_ERR_INVALID_ARGUMENT, "NULL argument");
+  return guarded([&] {
+    if (n_slices == 0) return;
+    cuda_check(stn::launch_sum_ordered(per_slice_dev, n_slices, out_elements, acc_dev,
+                                       static_cast<cudaStream_t>(stream), true),
+               "ordered fold");
   });
 }
 

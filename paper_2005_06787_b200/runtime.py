@@ -310,6 +310,106 @@ def run_scheme(plan: ExecutablePlan, parallelism: int = 1):
     return out.view(np.complex128).reshape(plan.out_dims), r
 
 
+def run_slices_host(plan: ExecutablePlan, cache: BranchCache, lo: int = 0, n: int | None = None,
+                    digits: np.ndarray | None = None, per_slice: bool = True, total: bool = True,
+                    stream=None):
+    """A worker envelope with host buffers (queue.hpp:250-252): slices [lo, lo+n)
+    or the rows of `digits`; returns (per-slice roots [n, *out_dims] or None,
+    ascending-order sum or None) as complex128 host arrays. Blocking."""
+    d = None
+    if digits is not None:
+        d = np.ascontiguousarray(digits, dtype=np.int32).reshape(-1, max(plan.n_sliced, 1))
+        n = d.shape[0]
+    elif n is None:
+        n = plan.subtasks - lo
+    rows = np.zeros((max(n, 1), 2 * plan.out_elements), np.float64) if per_slice else None
+    s = np.zeros(2 * plan.out_elements, np.float64) if total else None
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double)) if a is not None else None  # noqa: E731
+    check(_lib().stn_run_slices_host(plan.handle, cache.handle,
+                                     d.ctypes.data_as(C.POINTER(C.c_int32)) if d is not None else None,
+                                     lo, n, _stream_handle(stream), dp(rows), dp(s)))
+    out_rows = rows[:n].view(np.complex128).reshape((n,) + plan.out_dims) if per_slice else None
+    out_sum = s.view(np.complex128).reshape(plan.out_dims) if total else None
+    return out_rows, out_sum
+
+
+def flush_block_cache() -> None:
+    """Frees the executor's cached device blocks (arenas of destroyed plans)."""
+    check(_lib().stn_flush_block_cache())
+
+
+def fold_slices_ordered(per_slice, n_slices: int, out_elements: int, acc, stream=None) -> None:
+    """acc = (((acc + r_0) + r_1) + ...) on the device: continues an ascending fold."""
+    check(_lib().stn_fold_slices_ordered(C.c_void_p(per_slice.data_ptr()) if n_slices else None,
+                                         n_slices, out_elements, C.c_void_p(acc.data_ptr()),
+                                         _stream_handle(stream)))
+
+
+class MultiPlan:
+    """One device plan + branch cache per GPU of this box, driven from one
+    process (include/stn_exec.h, "several GPUs"): the in-process replacement of
+    the reference's worker processes (queue.hpp:197-336)."""
+
+    def __init__(self, desc, devices, mode: str = "fast"):
+        devs = list(devices)
+        arr = (C.c_int32 * len(devs))(*devs)
+        h = C.c_void_p()
+        m = MODES[mode] if isinstance(mode, str) else int(mode)
+        check(_lib().stn_multi_create(desc, len(devs), arr, m, C.byref(h)))
+        self._h = h
+        self.devices = devs
+        info = abi.PlanInfo()
+        check(_lib().stn_plan_get_info(_lib().stn_multi_plan(h, 0), C.byref(info)))
+        self.info = info
+        self.subtasks = info.subtasks
+        self.n_sliced = info.n_sliced
+        self.out_dims = tuple(info.out_dims[i] for i in range(info.out_rank))
+        self.out_elements = info.out_elements
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib().stn_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def run_scheme(self, deterministic: bool = True):
+        out = np.zeros(2 * self.out_elements, np.float64)
+        rep = abi.RunReport()
+        check(_lib().stn_multi_run_scheme(self._h, 1 if deterministic else 0,
+                                          out.ctypes.data_as(C.POINTER(C.c_double)),
+                                          C.byref(rep)))
+        r = RunReport(subtasks=rep.subtasks, mult_count=rep.mult_count,
+                      branch_mults=rep.branch_mults, wall_seconds=rep.wall_seconds,
+                      p50_ms=rep.p50_ms, p90_ms=rep.p90_ms, p99_ms=rep.p99_ms,
+                      parallelism=rep.parallelism,
+                      precision="single" if rep.precision == abi.STN_SINGLE else "double",
+                      peak_elements=rep.peak_elements)
+        return out.view(np.complex128).reshape(self.out_dims), r
+
+    def run_slices(self, lo: int = 0, n: int | None = None, digits: np.ndarray | None = None,
+                   deterministic: bool = True, per_slice: bool = False, total: bool = True):
+        d = None
+        if digits is not None:
+            d = np.ascontiguousarray(digits, dtype=np.int32).reshape(-1, max(self.n_sliced, 1))
+            n = d.shape[0]
+        elif n is None:
+            n = self.subtasks - lo
+        rows = np.zeros((max(n, 1), 2 * self.out_elements), np.float64) if per_slice else None
+        s = np.zeros(2 * self.out_elements, np.float64) if total else None
+        dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double)) if a is not None else None  # noqa: E731
+        check(_lib().stn_multi_run_slices(
+            self._h, d.ctypes.data_as(C.POINTER(C.c_int32)) if d is not None else None, lo, n,
+            1 if deterministic else 0, dp(rows), dp(s)))
+        out_rows = rows[:n].view(np.complex128).reshape((n,) + self.out_dims) if per_slice else None
+        out_sum = s.view(np.complex128).reshape(self.out_dims) if total else None
+        return out_rows, out_sum
+
+
 def sum_slices_ordered(per_slice, n_slices: int, out_elements: int, out, stream=None) -> None:
     """Ascending-order fp64 sum of per-slice results on the device."""
     check(_lib().stn_sum_slices_ordered(C.c_void_p(per_slice.data_ptr()), n_slices,

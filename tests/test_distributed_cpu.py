@@ -1,10 +1,11 @@
-"""Host-side multi-GPU logic on the CPU: world size 2 over gloo.
+"""Host-side multi-GPU logic on the CPU: world sizes 2 and 3 (uneven shards) over gloo.
 
 The per-rank compute is the CPU oracle (test infrastructure standing in for the
 GPU executor); what is tested is the product's sharding and exchange logic in
-paper_2005_06787_b200/distributed.py: balanced contiguous ranges, one
-all-reduce, and the deterministic reduction giving the SAME BITS as the
-single-process ascending-order sum (runtime.hpp:601-605) for any world size.
+paper_2005_06787_b200/distributed.py: balanced contiguous ranges, the chained
+ascending fold (1 KiB accumulator handed rank to rank) giving the SAME BITS as
+the single-process run_scheme sum (runtime.hpp:601-605) for any world size, and
+the one-all-reduce fast reduction.
 """
 import os
 import socket
@@ -63,14 +64,16 @@ def _worker(rank, world, port, deterministic, q):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("deterministic", [True, False])
-def test_two_rank_gloo_sum_matches_single_process(deterministic):
+def test_gloo_sum_matches_single_process(deterministic, world):
     from golden_io import read_ref
     _, _, want, _, _ = read_ref(CASE, "single")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, deterministic, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, deterministic, q))
+             for r in range(world)]
     for pr in procs:
         pr.start()
     got = q.get(timeout=120)
