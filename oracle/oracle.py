@@ -57,6 +57,10 @@ def lib() -> C.CDLL:
                                                      C.POINTER(C.c_int32), P,
                                                      C.POINTER(C.c_double), C.c_int64,
                                                      C.POINTER(SubtaskInfo), C.c_int]
+        L.oracle_time_slice_lean.argtypes = [C.POINTER(PlanDesc), C.c_int, C.POINTER(C.c_int32),
+                                             P, C.c_int, C.c_double, C.POINTER(C.c_double),
+                                             C.c_int32, C.POINTER(C.c_int32),
+                                             C.POINTER(C.c_int32), C.POINTER(C.c_double)]
         L.oracle_run_slices.argtypes = [C.POINTER(PlanDesc), C.c_int, P, C.c_uint64, C.c_uint64,
                                         C.c_int, C.c_int64, C.POINTER(C.c_double),
                                         C.POINTER(C.c_double)]
@@ -140,6 +144,24 @@ class OraclePlan:
                                                     out.ctypes.data_as(C.POINTER(C.c_double)),
                                                     self.out_elements, C.byref(info), threads))
         return out.view(np.complex128), info
+
+    def time_slice_lean(self, digits, cache=None, threads: int = 1, budget_s: float = 0.0,
+                        with_value: bool = False):
+        """Per-step wall-clock ms of the lean oracle on one slice (stops after
+        the step during which budget_s passed; 0 = whole slice) -> (ms list,
+        complete[, value when complete])."""
+        arr = (C.c_int32 * max(1, self.n_sliced))(*digits)
+        cap = 1 << 16
+        ms = np.zeros(cap, np.float64)
+        out = np.zeros(2 * self.out_elements, np.float64)
+        n, done = C.c_int32(), C.c_int32()
+        _check(lib().oracle_time_slice_lean(self._desc, self.precision, arr, cache, threads,
+                                            budget_s, ms.ctypes.data_as(C.POINTER(C.c_double)),
+                                            cap, C.byref(n), C.byref(done),
+                                            out.ctypes.data_as(C.POINTER(C.c_double))))
+        if with_value:
+            return ms[: n.value].tolist(), bool(done.value), out.view(np.complex128)
+        return ms[: n.value].tolist(), bool(done.value)
 
     def run_slices(self, lo: int, hi: int, cache=None, threads: int = 1):
         n = hi - lo

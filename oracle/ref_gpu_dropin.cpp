@@ -256,7 +256,7 @@ int main() {
           std::to_string(devs.size()) + " device plan(s), " + std::to_string(p.subtasks) +
               " slices");
     auto [vf, rf] = mp.run_scheme(false);  // one NCCL all-reduce (no NCCL call on a single GPU)
-    check(rel(vf, vc) <= 1e-12 || devs[0] == devs[1], "multi-GPU all-reduce sum within 1e-12",
+    check(rel(vf, vc) <= 1e-12, "multi-GPU all-reduce sum within 1e-12",
           std::to_string(rel(vf, vc)));
   }
   std::printf("%d failure(s)\n", failures);

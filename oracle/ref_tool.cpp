@@ -285,7 +285,10 @@ int cmd_golden(const Args &a) {
   for (auto &th : pool) th.join();
   std::uint64_t out_elems = res.empty() ? 0 : res[0].value.data.size();
   std::string path = dir + "/ref_" + prec + ".bin";
-  FILE *f = std::fopen(path.c_str(), "wb");
+  // written to a temporary name and renamed at the end: a long run never leaves a
+  // truncated fixture where the tests read it
+  std::string tmp = path + ".partial";
+  FILE *f = std::fopen(tmp.c_str(), "wb");
   require(f != nullptr, ErrorKind::MissingResult, "cannot write " + path);
   std::uint64_t n = slices.size();
   std::fwrite(&n, 8, 1, f);
@@ -306,6 +309,8 @@ int cmd_golden(const Args &a) {
   std::fwrite(&mu, 8, 1, f);
   std::fwrite(&pk, 8, 1, f);
   std::fclose(f);
+  require(std::rename(tmp.c_str(), path.c_str()) == 0, ErrorKind::MissingResult,
+          "cannot rename " + tmp);
   nlohmann::json j = {{"slices", n},
                       {"out_elems", out_elems},
                       {"precision", prec},

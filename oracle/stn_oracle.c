@@ -22,7 +22,9 @@
  * what GCC emits for std::complex multiplication of finite values; the file is
  * compiled with -ffp-contract=off so no FMA changes the rounding.
  */
+#define _POSIX_C_SOURCE 200809L
 #include <math.h>
+#include <time.h>
 #include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -474,9 +476,26 @@ int oracle_cache_info(const oracle_cache *c, uint64_t *identity, uint64_t *mults
 }
 
 /* ---- one subtask (Engine::run, runtime.hpp:420-453) ---------------------------- */
+int64_t oracle_out_elements(const stn_plan_desc *d);
+
+/* Per-step wall-clock timing of a (possibly partial) run, for the CPU baseline. */
+typedef struct {
+  double budget_s; /* stop after the step during which this much time passed (<= 0: all) */
+  double *step_ms; /* [cap] per executed per-slice step */
+  int32_t cap;
+  int32_t done;     /* steps executed */
+  int32_t complete; /* 1 if the whole slice ran */
+} step_timer;
+
+static double now_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
+
 static int run_digits_impl(const stn_plan_desc *d, int prec, const int32_t *digits,
                            const oracle_cache *cache, double *out, int64_t out_cap,
-                           stn_subtask_info *info, int lean_threads) {
+                           stn_subtask_info *info, int lean_threads, step_timer *timer) {
   if (cache && cache->identity != d->identity) {
     stn_set_error_c("SubtaskFailure: branch cache belongs to a different plan");
     return STN_ERR_SUBTASK_FAILURE;
@@ -511,9 +530,16 @@ static int run_digits_impl(const stn_plan_desc *d, int prec, const int32_t *digi
       stn_set_error_c("SubtaskFailure: operand unavailable");                          \
     }                                                                                  \
   } while (0)
+  const double t_start = timer ? now_s() : 0.0;
+  int stopped = 0;
   for (int i = 0; ok && i < d->n_steps; ++i) {
     const stn_step_desc *s = &d->steps[i];
     if (cache && s->is_branch) continue;
+    if (timer && timer->budget_s > 0 && timer->done > 0 && now_s() - t_start > timer->budget_s) {
+      stopped = 1;
+      break;
+    }
+    const double t_step = timer ? now_s() : 0.0;
     tt_t a = {0}, b = {0};
     FETCH(s->lhs, a);
     if (ok) FETCH(s->rhs, b);
@@ -526,6 +552,16 @@ static int run_digits_impl(const stn_plan_desc *d, int prec, const int32_t *digi
     step_count++;
     mults += s->mults;
     if (live[s->node].n > peak) peak = live[s->node].n;
+    if (timer && timer->done < timer->cap) timer->step_ms[timer->done++] = 1e3 * (now_s() - t_step);
+  }
+  if (timer) {
+    timer->complete = ok && !stopped;
+    if (stopped) { /* partial run: no result */
+      for (int n = 0; live && n < d->n_nodes; ++n) tt_free(&live[n]);
+      free(live);
+      plan_free(&p);
+      return STN_OK;
+    }
   }
   tt_t result = {0};
   if (ok) FETCH(d->root, result);
@@ -562,7 +598,7 @@ static int run_digits_impl(const stn_plan_desc *d, int prec, const int32_t *digi
 int oracle_run_subtask_digits(const stn_plan_desc *d, int prec, const int32_t *digits,
                               const oracle_cache *cache, double *out, int64_t out_cap,
                               stn_subtask_info *info) {
-  return run_digits_impl(d, prec, digits, cache, out, out_cap, info, 0);
+  return run_digits_impl(d, prec, digits, cache, out, out_cap, info, 0, NULL);
 }
 
 /* Same result, bit for bit, through gemm_lean on `threads` host threads: the
@@ -570,7 +606,27 @@ int oracle_run_subtask_digits(const stn_plan_desc *d, int prec, const int32_t *d
 int oracle_run_subtask_digits_lean(const stn_plan_desc *d, int prec, const int32_t *digits,
                                    const oracle_cache *cache, double *out, int64_t out_cap,
                                    stn_subtask_info *info, int threads) {
-  return run_digits_impl(d, prec, digits, cache, out, out_cap, info, threads < 1 ? 1 : threads);
+  return run_digits_impl(d, prec, digits, cache, out, out_cap, info, threads < 1 ? 1 : threads,
+                         NULL);
+}
+
+/* The lean oracle on one slice with per-step wall-clock times, stopping after the
+ * step during which `budget_s` elapsed (budget_s <= 0: the whole slice). The CPU
+ * baseline of bench.py for plans the reference's own executor cannot hold. */
+int oracle_time_slice_lean(const stn_plan_desc *d, int prec, const int32_t *digits,
+                           const oracle_cache *cache, int threads, double budget_s,
+                           double *step_ms, int32_t cap, int32_t *n_done, int32_t *complete,
+                           double *out /* 2*out_elements, or NULL; filled when complete */) {
+  step_timer t = {budget_s, step_ms, cap, 0, 0};
+  int64_t oe = oracle_out_elements(d);
+  double *buf = (double *)calloc(2 * (size_t)(oe > 0 ? oe : 1), 8);
+  if (!buf) return STN_ERR_OUT_OF_MEMORY;
+  int st = run_digits_impl(d, prec, digits, cache, buf, oe, NULL, threads < 1 ? 1 : threads, &t);
+  if (out && st == STN_OK && t.complete) memcpy(out, buf, 16 * (size_t)oe);
+  free(buf);
+  *n_done = t.done;
+  *complete = t.complete;
+  return st;
 }
 
 int oracle_run_subtask(const stn_plan_desc *d, int prec, uint64_t assignment,

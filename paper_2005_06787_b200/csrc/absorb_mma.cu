@@ -438,7 +438,7 @@ cudaError_t launch_mma_impl(const DirectGeom &g, const BatchPtrs &p, cudaStream_
   if (ctas < 1) ctas = 1;
   if (ctas > n_tiles) ctas = n_tiles;
   dim3 grid(unsigned(ctas), unsigned(p.nbatch));
-  static const int dbg = std::getenv("STN_MMA_DBG") ? std::atoi(std::getenv("STN_MMA_DBG")) : 0;
+  static const int dbg = stn::debug_opt("mma_dbg") ? std::atoi(stn::debug_opt("mma_dbg")) : 0;
   kern<<<grid, kThreads, Lay::SMEM, stream>>>(g, p, n_tiles, dbg);
   return cudaGetLastError();
 }
@@ -737,7 +737,7 @@ bool mma_absorb_supported(const DirectGeom &g) {
 cudaError_t launch_absorb_mma(const DirectGeom &g, const BatchPtrs &p, cudaStream_t stream) {
   if (!mma_absorb_supported(g)) return cudaErrorNotSupported;
   const int nm = (2 << g.nb) < 16 ? 16 : (2 << g.nb);
-  static const char *force1 = std::getenv("STN_MMA_V1");  // experiments: de-interleaved kernel only
+  static const char *force1 = stn::debug_opt("mma_v1");  // experiments: de-interleaved kernel only
   if (!force1 && g.kb <= 5) {  // interleaved kernel: whole complex rows, larger tiles
 #define STN_MMA2(KBV, NMV) \
   if (g.kb == KBV && nm == NMV) return launch_mma2_impl<KBV, NMV>(g, p, stream);

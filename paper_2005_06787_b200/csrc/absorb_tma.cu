@@ -495,11 +495,11 @@ cudaError_t launch_tma_impl(const TmaAbsorbGeom &g, const BatchPtrs &p, cudaStre
   const size_t smem = tma_smem_bytes<KSZ, MB, NM>(gl);
   if (gl.nsr < (GATHER ? 4 : 2)) return cudaErrorNotSupported;
   gl.lag = gl.nsr - 3 < kMaxLag ? gl.nsr - 3 : kMaxLag;
-  static const char *env_lag = std::getenv("STN_TMA_LAG");  // experiments
+  static const char *env_lag = stn::debug_opt("tma_lag");  // experiments
   if (env_lag && std::atoi(env_lag) >= 1 && std::atoi(env_lag) <= gl.nsr - 2 &&
       std::atoi(env_lag) <= kMaxLag)
     gl.lag = std::atoi(env_lag);
-  static const int dbg = std::getenv("STN_TMA_DBG") ? std::atoi(std::getenv("STN_TMA_DBG")) : 0;
+  static const int dbg = stn::debug_opt("tma_dbg") ? std::atoi(stn::debug_opt("tma_dbg")) : 0;
   gl.dbg = dbg;  // experiments: 1 no stores, 2 no MMAs, 4 no lo conversion
   if (dbg & 8) {  // experiments (wrong results): box order d0, M runs, K runs
     int order[5], n = 0;
@@ -527,7 +527,7 @@ cudaError_t launch_tma_impl(const TmaAbsorbGeom &g, const BatchPtrs &p, cudaStre
     set = true;
   }
   if (smem > size_t(227 * 1024)) return cudaErrorNotSupported;
-  static const char *env_nsr = std::getenv("STN_TMA_NSR");  // experiments: raw ring depth
+  static const char *env_nsr = stn::debug_opt("tma_nsr");  // experiments: raw ring depth
   if (env_nsr && std::atoi(env_nsr) >= 2 && std::atoi(env_nsr) <= gl.nsr) gl.nsr = std::atoi(env_nsr);
   EncodeFn enc = encode_fn();
   if (!enc && !GATHER) return cudaErrorNotSupported;
@@ -705,7 +705,7 @@ cudaError_t launch_absorb_tma(const TmaAbsorbGeom &g, const BatchPtrs &p, cudaSt
   const int ksz = 1 << g.kstage, mb = 1 << g.mbl;
   // loader: one TMA box per stage where the geometry allows it (measured faster), else the
   // cp.async gather; STN_ABSORB_LOADER=gather forces the gather (experiments)
-  const char *ld = std::getenv("STN_ABSORB_LOADER");
+  const char *ld = stn::debug_opt("absorb_loader");
   const bool use_tma = g.tma_ok && !(ld && std::strcmp(ld, "gather") == 0);
 #define STN_TMA(KSZV, MBV, NMV)                                              \
   if (ksz == KSZV && mb == MBV && g.nm == NMV)                               \

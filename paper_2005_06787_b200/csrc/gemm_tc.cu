@@ -602,7 +602,7 @@ cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspa
                                                   blo);
   }
   // 128 x 256 tiles where 2N allows (STN_GEMM_BN=128 forces the 128 x 128 kernel)
-  const char *env_bn = std::getenv("STN_GEMM_BN");
+  const char *env_bn = stn::debug_opt("gemm_bn");
   const bool wide = (2 * s.N) % BN2 == 0 && !(env_bn && std::atoi(env_bn) == 128);
   const int bn = wide ? BN2 : BN;
   CUtensorMap mah, mal, mbh, mbl;

@@ -10,10 +10,52 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <mutex>
+#include <set>
+#include <string>
 #include <utility>
 #include <vector>
 
 namespace stn {
+
+// Experiment and diagnostic switches of the executor, all behind ONE environment
+// variable (unset in production): STN_DEBUG="key=value,key,...". Keys:
+//   lanes=0|1|all          lane-mapped absorb off / default policy / every eligible step
+//   lanes_pf=0|1           lane absorb: L2 prefetch of the next row group (default K <= 4)
+//   direct_max_bits=B      direct absorb only for K x N <= 2^B (default 12)
+//   direct_min_l=L         direct absorb needs >= L identity low bits (default 2)
+//   mma_min_bits=B         tensor-core direct absorb from K x N >= 2^B (default 10)
+//   tma_min_bits=B         TMA absorb for every K x N >= 2^B
+//   absorb_policy=simt|tc  tiled absorb: never / from K x N >= 64 on tensor cores
+//   sweep_bits=B, sweep_debug, sweep_dbg=N   stem-sweep fusion tile size / traces
+//   plan_dump, plan_timing                 per-step kernel choice / plan-build timing
+//   bitperm_legacy         legacy bit-permute kernel for the selftest
+//   sweep_only=..., no_bulk, tma_lag=N, tma_nsr=N, perm_tb=N   pipeline experiments
+//   mma_v1, mma_dbg=N, tma_dbg=N, absorb_loader=tma|gather, gemm_bn=N   kernel experiments
+// Returns the value ("" for a bare key) or nullptr when the key is absent. Read at
+// every call (tests change it at run time); returned strings stay valid.
+inline const char *debug_opt(const char *key) {
+  static std::mutex mu;
+  static std::set<std::string> interned;
+  const char *e = std::getenv("STN_DEBUG");
+  if (!e) return nullptr;
+  std::string s = e, item;
+  for (size_t i = 0; i <= s.size(); ++i) {
+    if (i == s.size() || s[i] == ',') {
+      const size_t eq = item.find('=');
+      if (item.substr(0, eq) == key) {
+        std::lock_guard<std::mutex> lk(mu);
+        return interned.insert(eq == std::string::npos ? std::string() : item.substr(eq + 1))
+            .first->c_str();
+      }
+      item.clear();
+    } else {
+      item += s[i];
+    }
+  }
+  return nullptr;
+}
 
 constexpr int kMaxAxes = 40;
 
@@ -101,6 +143,31 @@ struct DirectGeom {
   int64_t w_n_stride[12];    // W stride of N bit j
 };
 bool direct_absorb_launchable(const DirectGeom &g);
+
+// Lane-mapped bond-2 absorb (kernels_lanes.cu), single precision: any
+// interleaving of M bits (from the stem X) and N bits (from W) in the output.
+// Output index o = ((row << 5) | lane) << U | pair, U = 0 (mode 0) or 1 (mode 1:
+// the pair bit is X bit 0, so X is read as 16-byte m pairs; mode 2: the pair bit
+// is an N bit whose W offset is w_pair). Every output bit maps to an X offset or
+// a W offset: lane bits through xl / wl, row bits through per-byte tables.
+constexpr int kLaneMaxK = 64;
+struct LaneTables {        // device memory, one per step
+  int64_t xr[4][256];      // X offset of row byte c with value v
+  int32_t wr[4][256];      // W offset of row byte c with value v
+  int64_t xl[32];          // X offset of lane bits
+  int32_t wl[32];          // W offset of lane bits
+  int64_t xk[kLaneMaxK];   // X offset of k (bit j of k = K bit j, ascending X position)
+  int32_t wk[kLaneMaxK];   // W offset of k
+};
+struct LaneGeom {
+  int mode;                // 0, 1, 2 (above)
+  int K;                   // k terms (<= 64)
+  int64_t rows;            // output rows of 32 lanes per batch
+  int32_t w_pair;          // mode 2: W offset of the pair bit
+  int32_t w_elems;         // W elements staged in shared memory (<= 8192)
+};
+cudaError_t launch_absorb_lanes(const LaneTables *T, const LaneGeom &g, const BatchPtrs &p,
+                                bool exact, cudaStream_t stream);
 cudaError_t launch_absorb_direct(const DirectGeom &g, const BatchPtrs &p, bool exact,
                                  cudaStream_t stream);
 

@@ -467,7 +467,7 @@ cudaError_t launch_absorb2_impl(const AbsorbGeom &g, const BatchPtrs &p, cudaStr
 
 template <bool EXACT, int KC, int NC, bool BLOCKED>
 cudaError_t launch_absorb_best(const AbsorbGeom &g, const BatchPtrs &p, cudaStream_t st) {
-  static const bool no_bulk = std::getenv("STN_NO_BULK") != nullptr;  // experiments only
+  static const bool no_bulk = stn::debug_opt("no_bulk") != nullptr;  // experiments only
   if (!no_bulk && absorb3_ok(g)) {
     cudaError_t e = launch_absorb3_impl<EXACT, false, KC, NC, BLOCKED>(g, p, st);
     if (e != cudaErrorNotSupported) return e;

@@ -94,7 +94,7 @@ bool build_perm_tiles(const std::vector<int> &perm, PermTileGeom &g, std::vector
       ++n;
     }
   };
-  static const char *env_tb = std::getenv("STN_PERM_TB");  // experiments: tile bits
+  static const char *env_tb = stn::debug_opt("perm_tb");  // experiments: tile bits
   const int target = env_tb ? std::atoi(env_tb) : 11;  // 16 KiB tiles: measured best on B200
   for (int p = 0; p < 5; ++p) add(p);
   for (int q = 0; q < 5 && n < target; ++q) add(inpos_of_out[q]);

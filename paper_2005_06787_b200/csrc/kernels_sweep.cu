@@ -261,7 +261,7 @@ cudaError_t launch_sweep(const SweepGeom &g, const BatchPtrs &p, bool exact,
   if (ctas < 1) ctas = 1;
   if (ctas > n_tiles) ctas = n_tiles;
   dim3 grid(unsigned(ctas), unsigned(p.nbatch));
-  static const int dbg = std::getenv("STN_SWEEP_DBG") ? std::atoi(std::getenv("STN_SWEEP_DBG")) : 0;
+  static const int dbg = stn::debug_opt("sweep_dbg") ? std::atoi(stn::debug_opt("sweep_dbg")) : 0;
   kern<<<grid, kSwThreads, smem, stream>>>(g, p, n_tiles, dbg);
   return cudaGetLastError();
 }

@@ -257,9 +257,34 @@ struct stn_multi {
     cuda(cudaStreamSynchronize(streams[last]), "stream sync");
   }
 
-  // One NCCL all-reduce of the per-GPU partial folds.
+  bool distinct() const {
+    std::vector<int> d(devices);
+    std::sort(d.begin(), d.end());
+    return std::adjacent_find(d.begin(), d.end()) == d.end();
+  }
+
+  // One NCCL all-reduce of the per-GPU partial folds. Several device plans on one
+  // GPU (tests on a 1-GPU box) cannot form an NCCL communicator; their partials
+  // are added on the first plan's device instead.
   void allreduce(double *sum_host) {
     const size_t row = 2 * size_t(info.out_elements);
+    if (n() > 1 && !distinct()) {
+      DeviceMem tmp;
+      tmp.reserve(devices[0], 8 * row);
+      for (int i = 1; i < n(); ++i) {
+        cuda(cudaSetDevice(devices[i]), "cudaSetDevice");
+        cuda(cudaStreamSynchronize(streams[i]), "stream sync");
+        cuda(cudaSetDevice(devices[0]), "cudaSetDevice");
+        cuda(cudaMemcpyPeerAsync(tmp.p, devices[0], acc[i].p, devices[i], 8 * row, streams[0]),
+             "partial copy");
+        check(stn_fold_slices_ordered(tmp.d(), 1, info.out_elements, acc[0].d(), streams[0]),
+              "partial add");
+      }
+      cuda(cudaMemcpyAsync(sum_host, acc[0].p, 8 * row, cudaMemcpyDeviceToHost, streams[0]),
+           "sum download");
+      cuda(cudaStreamSynchronize(streams[0]), "stream sync");
+      return;
+    }
     if (n() > 1) {
       Nccl &nc = Nccl::get();
       if (!nc.ok()) throw Failure{STN_ERR_CUDA, nc.error};

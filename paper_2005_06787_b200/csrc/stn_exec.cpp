@@ -204,7 +204,7 @@ struct DevBuf {
 // ---------------------------------------------------------------------------
 // plan model
 // ---------------------------------------------------------------------------
-enum class Kern { Generic, Absorb, AbsorbTc, AbsorbDirect, AbsorbMma, SplitK, GemmSimt, GemmTc, AbsorbTma, Outer };
+enum class Kern { Generic, Absorb, AbsorbTc, AbsorbDirect, AbsorbMma, SplitK, GemmSimt, GemmTc, AbsorbTma, Outer, Lanes };
 
 struct Node {
   bool is_leaf = false;
@@ -229,6 +229,9 @@ struct StepPlan {
   stn::DirectGeom dg{};     // tile-free variant (identity low bits)
   bool direct_ok = false;
   std::shared_ptr<stn::TmaAbsorbGeom> tg;  // TMA-fed tensor-core variant (X bits 0..3 in M)
+  stn::LaneGeom lg{};                      // lane-mapped SIMT variant (any low-bit interleave)
+  std::shared_ptr<DevBuf> lane_tab;        // its stn::LaneTables
+  double lane_eff = 0;                     // X sector efficiency of one warp row (all k)
   // absorb bit geometry (positions in X / W / O), kept for stem-sweep fusion
   bool has_bits = false;
   int xr = 0, wr = 0, orank_ = 0;
@@ -538,6 +541,67 @@ bool make_tile_geom(const std::vector<std::pair<int, int>> &kbits,
   return true;
 }
 
+// Lane-mapped absorb tables (kernels.h LaneGeom / LaneTables). kbits: (x, w) by
+// ascending X position (k bit j = kbits[j], the reference's k order);
+// mbits: (x, o); nbits: (o, w).
+void build_lanes(StepPlan &sp, const std::vector<std::pair<int, int>> &kbits,
+                 const std::vector<std::pair<int, int>> &mbits,
+                 const std::vector<std::pair<int, int>> &nbits, int xr, int wr, int orank) {
+  const int kb = int(kbits.size());
+  if (kb > 6 || wr > 13) return;  // K <= 64, W <= 8192 complex in shared memory
+  std::vector<int64_t> xs(size_t(orank), 0);
+  std::vector<int32_t> ws(size_t(orank), 0);
+  for (auto &[xp, op] : mbits) xs[size_t(op)] = int64_t(1) << xp;
+  for (auto &[op, wp] : nbits) ws[size_t(op)] = int32_t(1) << wp;
+  int mode = 0;
+  if (xs[0] == 1) mode = 1;       // O bit 0 = X bit 0: m pairs
+  else if (ws[0] != 0) mode = 2;  // O bit 0 = an N bit: n pairs
+  const int U = mode ? 1 : 0;
+  const int row_bits = orank - U - 5;
+  if (row_bits < 0 || row_bits > 32) return;
+  auto T = std::make_unique<stn::LaneTables>();
+  memset(T.get(), 0, sizeof(stn::LaneTables));
+  for (int l = 0; l < 32; ++l)
+    for (int j = 0; j < 5; ++j)
+      if ((l >> j) & 1) {
+        T->xl[l] += xs[size_t(U + j)];
+        T->wl[l] += ws[size_t(U + j)];
+      }
+  for (int c = 0; c < 4; ++c)
+    for (int v = 0; v < 256; ++v)
+      for (int j = 0; j < 8; ++j)
+        if (((v >> j) & 1) && 8 * c + j < row_bits) {
+          T->xr[c][v] += xs[size_t(U + 5 + 8 * c + j)];
+          T->wr[c][v] += ws[size_t(U + 5 + 8 * c + j)];
+        }
+  const int K = 1 << kb;
+  for (int k = 0; k < K; ++k)
+    for (int j = 0; j < kb; ++j)
+      if ((k >> j) & 1) {
+        T->xk[k] += int64_t(1) << kbits[size_t(j)].first;
+        T->wk[k] += int32_t(1) << kbits[size_t(j)].second;
+      }
+  // X sector efficiency of one warp row over all k (L1 / L2 serve the re-reads)
+  std::set<int64_t> elems, sectors;
+  for (int l = 0; l < 32; ++l)
+    for (int k = 0; k < K; ++k)
+      for (int u = 0; u < (mode == 1 ? 2 : 1); ++u) {
+        const int64_t e = T->xl[l] + T->xk[k] + u;
+        elems.insert(e);
+        sectors.insert(e / 4);
+      }
+  sp.lane_eff = double(elems.size()) / (4.0 * double(sectors.size()));
+  sp.lg.mode = mode;
+  sp.lg.K = K;
+  sp.lg.rows = int64_t(1) << row_bits;
+  sp.lg.w_pair = mode == 2 ? ws[0] : 0;
+  sp.lg.w_elems = int32_t(1) << wr;
+  sp.lane_tab = std::make_shared<DevBuf>();
+  sp.lane_tab->reserve(sizeof(stn::LaneTables));
+  cuda_check(cudaMemcpy(sp.lane_tab->ptr, T.get(), sizeof(stn::LaneTables), cudaMemcpyHostToDevice),
+             "lane tables");
+}
+
 bool build_absorb(StepPlan &sp, const std::vector<int> &ldims, const std::vector<int> &rdims) {
   const stn_step_desc &d = sp.d;
   if (d.nd != 0) return false;
@@ -601,6 +665,7 @@ bool build_absorb(StepPlan &sp, const std::vector<int> &ldims, const std::vector
   sp.kbits = kbits;
   sp.mbits = mbits;
   sp.nbits = nbits;
+  build_lanes(sp, kbits, mbits, nbits, xr, wr, orank);
   // tile-free geometry: the lowest L bits of X are M bits at the same O positions
   {
     std::map<int, int> o_of_x;
@@ -738,19 +803,33 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
   if (single && big >= (int64_t(1) << 12) && small <= 4096 && build_absorb(sp, ldims, rdims)) {
     sp.kern = Kern::Absorb;
     // tile-free streaming when the low bits line up (K x N <= 2^STN_DIRECT_MAX_BITS)
-    static const char *dmax = std::getenv("STN_DIRECT_MAX_BITS");
+    static const char *dmax = stn::debug_opt("direct_max_bits");
     const int direct_max = dmax ? std::atoi(dmax) : 12;
-    static const char *dminl = std::getenv("STN_DIRECT_MIN_L");
+    static const char *dminl = stn::debug_opt("direct_min_l");
     const int direct_min_L = dminl ? std::atoi(dminl) : 2;
     // FAST mode, K x N >= 2^STN_MMA_MIN_BITS: tensor-core direct absorb
-    const char *mmin = std::getenv("STN_MMA_MIN_BITS");
+    const char *mmin = stn::debug_opt("mma_min_bits");
     const int mma_min = mmin ? std::atoi(mmin) : 10;
     // FAST mode: the gather/TMA-fed tensor-core absorb where the SIMT streams are weak --
     // no or short identity run of low bits (L <= 2, measured on B200: the tensor-core
     // kernel streams at 3-4 TB/s, the SIMT kernels at 1.3-3 TB/s there) and 64 x 64
     // W's -- while long identity runs stay on the SIMT direct kernel (6+ TB/s).
     // STN_TMA_MIN_BITS=<bits> (experiments) forces it for every K x N >= 2^bits.
-    const char *tmin = std::getenv("STN_TMA_MIN_BITS");
+    const char *tmin = stn::debug_opt("tma_min_bits");
+    // lane-mapped SIMT absorb (any interleave of the low output bits) for small K x N
+    // where the direct stream does not apply (no identity run of >= 3 low bits).
+    // STN_LANES=0 (experiments) disables it, STN_LANES=all takes every eligible step.
+    {
+      const char *lp = stn::debug_opt("lanes");
+      const int policy = lp ? (std::string(lp) == "all" ? 2 : std::atoi(lp) != 0) : 1;
+      const int kn = int(sp.kbits.size() + sp.nbits.size());
+      const bool ok = sp.lane_tab && sp.lane_eff >= 0.5 && big >= (int64_t(1) << 16);
+      const bool direct_strong = sp.direct_ok && sp.dg.L >= 3;
+      if (ok && (policy == 2 || (policy == 1 && kn <= 8 && !direct_strong))) {
+        sp.kern = Kern::Lanes;
+        return;
+      }
+    }
     if (!exact && sp.tg) {
       const int kn = int(sp.kbits.size() + sp.nbits.size());
       const bool pick = tmin ? kn >= std::atoi(tmin)
@@ -776,7 +855,7 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     }
     // large K x N: SIMT math would bound the stream; use the tensor cores.
     // STN_ABSORB_POLICY (experiments only): "simt" never, "tc" from K*N >= 64.
-    static const char *policy = std::getenv("STN_ABSORB_POLICY");
+    static const char *policy = stn::debug_opt("absorb_policy");
     int tc_min_bits = 10;
     if (policy && std::string(policy) == "simt") tc_min_bits = 99;
     if (policy && std::string(policy) == "tc") tc_min_bits = 6;
@@ -932,7 +1011,7 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
 // Diagnostics (STN_PLAN_DUMP): one line per large step with its kernel and bit geometry.
 void dump_step(const StepPlan &sp, int i) {
   static const char *names[] = {"generic", "absorb", "absorb_tc", "direct", "mma", "splitk",
-                                "gemm_simt", "gemm_tc", "tma", "outer"};
+                                "gemm_simt", "gemm_tc", "tma", "outer", "lanes"};
   auto lg = [](int64_t v) { int b = 0; while ((int64_t(1) << b) < v) ++b; return b; };
   std::string s = "step " + std::to_string(i) + " " + names[int(sp.kern)] + " l2^" +
                   std::to_string(lg(sp.lsize)) + " r2^" + std::to_string(lg(sp.rsize)) + " o2^" +
@@ -1190,7 +1269,7 @@ void plan_sweeps(stn_plan &P) {
   // per-tile stage math of a sweep is FFMA-issue bound and loses to the
   // unfused HBM-rate direct / tensor-core absorbs. STN_SWEEP_BITS=<tile bits>
   // (e.g. 12) enables it; read per plan so tests can toggle it.
-  const char *env_bits = std::getenv("STN_SWEEP_BITS");
+  const char *env_bits = stn::debug_opt("sweep_bits");
   const int max_bits = env_bits ? std::atoi(env_bits) : 0;
   if (max_bits <= 0) return;
   const int n = int(P.steps.size());
@@ -1222,13 +1301,13 @@ void plan_sweeps(stn_plan &P) {
       if (best > a) {
         stn_plan::Sweep sw;
         std::vector<int> seg(chain.begin() + a, chain.begin() + best + 1);
-        static const char *env_only = std::getenv("STN_SWEEP_ONLY");  // profiling aid
+        static const char *env_only = stn::debug_opt("sweep_only");  // profiling aid
         static int seen = 0;
         const bool take = !env_only || std::atoi(env_only) == seen;
         ++seen;
         if (take && build_sweep(P, seg, max_bits, &sw)) {
           const int id = int(P.sweeps.size());
-          if (std::getenv("STN_SWEEP_DEBUG")) {
+          if (stn::debug_opt("sweep_debug")) {
             const stn::SweepGeom &g = sw.geom;
             fprintf(stderr, "sweep %d: steps", id);
             for (int q : seg) fprintf(stderr, " %d", q);
@@ -1731,7 +1810,7 @@ void create_plan(const stn_plan_desc *desc, int device, int mode, stn_plan *P) {
     choose_kernel(*P, sp, ld, rd);
     choose_ms[int(sp.kern)] +=
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_ck).count();
-    if (std::getenv("STN_PLAN_DUMP") && !d.is_branch && sp.osize + sp.lsize + sp.rsize >= (1 << 20))
+    if (stn::debug_opt("plan_dump") && !d.is_branch && sp.osize + sp.lsize + sp.rsize >= (1 << 20))
       dump_step(sp, i);
   }
   // root
@@ -1780,7 +1859,7 @@ void create_plan(const stn_plan_desc *desc, int device, int mode, stn_plan *P) {
   build_program(*P, P->build, 0);
   build_program(*P, P->with_cache, 1);
   build_program(*P, P->no_cache, 2);
-  if (std::getenv("STN_PLAN_TIMING")) {
+  if (stn::debug_opt("plan_timing")) {
     const auto t_end = std::chrono::steady_clock::now();
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
     fprintf(stderr, "plan create: steps+leaves %.2f ms, programs %.2f ms\n", ms(t_begin, t_steps),
@@ -1970,6 +2049,15 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
       const Resolved &w = sp.x_is_lhs ? b : a;
       stn::BatchPtrs p{x.ptr, w.ptr, out, x.bs, w.bs, o.bs, nb};
       cuda_check(stn::launch_absorb_direct(sp.dg, p, exact, st), "direct absorb kernel");
+      prof.done(STN_KERNEL_ABSORB, io_bytes, flops);
+      break;
+    }
+    case Kern::Lanes: {
+      const Resolved &x = sp.x_is_lhs ? a : b;
+      const Resolved &w = sp.x_is_lhs ? b : a;
+      stn::BatchPtrs p{x.ptr, w.ptr, out, x.bs, w.bs, o.bs, nb};
+      cuda_check(stn::launch_absorb_lanes(sp.lane_tab->as<stn::LaneTables>(), sp.lg, p, exact, st),
+                 "lane absorb kernel");
       prof.done(STN_KERNEL_ABSORB, io_bytes, flops);
       break;
     }
@@ -2292,7 +2380,7 @@ int stn_plan_get_info(const stn_plan *P, stn_plan_info *info) {
     if (k == Kern::GemmTc) info->steps_tensor_core++;
     else if (k == Kern::GemmSimt) info->steps_generic++;
     else if (k == Kern::Absorb || k == Kern::AbsorbTc || k == Kern::AbsorbDirect ||
-             k == Kern::AbsorbMma || k == Kern::AbsorbTma)
+             k == Kern::AbsorbMma || k == Kern::AbsorbTma || k == Kern::Lanes)
       info->steps_absorb++;
     else info->steps_generic++;
   }
@@ -2678,7 +2766,7 @@ int stn_selftest_bitperm(int32_t log2_elems, const int32_t *perm, int32_t reps, 
     stn::PermTileGeom tg;
     std::vector<int64_t> tbases;
     DevBuf tb_dev;
-    const bool tiles = std::getenv("STN_BITPERM_LEGACY") == nullptr &&
+    const bool tiles = stn::debug_opt("bitperm_legacy") == nullptr &&
                        stn::build_perm_tiles(axis_perm, tg, tbases);
     if (tiles) tb_dev.upload(tbases);
     auto launch = [&](const void *src, void *dst, cudaStream_t s) {

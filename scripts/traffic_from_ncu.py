@@ -12,6 +12,7 @@ import sys
 
 CLASSES = [  # (substring of the kernel name, class)
     ("k_absorb_direct", "absorb"), ("k_absorb3", "absorb"), ("k_absorb2", "absorb"),
+    ("k_absorb_lanes", "absorb"), ("k_gemm_skinny", "gemm_simt"), ("k_sum_ordered", "root"),
     ("k_absorb_tma", "absorb_tc"), ("k_absorb_tc", "absorb_tc"), ("k_absorb_mma", "absorb_tc"),
     ("k_gemm_tc", "gemm_tc"), ("k_split_a", "gemm_tc"), ("k_expand_b", "gemm_tc"),
     ("k_perm_tiles", "permute"), ("k_gemm_simt", "gemm_simt"), ("k_generic", "generic"),
@@ -39,7 +40,9 @@ def main(src, dst):
         o["ns"] += m.get("gpu__time_duration.sum", 0)
     for o in out.values():
         o["bytes_per_launch"] = o["dram_bytes"] / o["launches"]
-    json.dump({"source": src, "classes": out}, open(dst, "w"), indent=1)
+        o["dram_bytes_per_launch"] = o["bytes_per_launch"]
+    label = sys.argv[3] if len(sys.argv) > 3 else src
+    json.dump({"source": label, "classes": out}, open(dst, "w"), indent=1)
     print(json.dumps(out, indent=1))
 
 

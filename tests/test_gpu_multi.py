@@ -39,9 +39,9 @@ def test_multi_run_scheme_bitwise_reference(precision, n_plans):
     got, rep = mp.run_scheme(deterministic=True)
     assert np.array_equal(bits(got.ravel()), bits(want))
     assert rep.subtasks == mp.subtasks == 32
-    if len(set(devices)) == len(devices):  # NCCL needs distinct GPUs
-        fast, _ = mp.run_scheme(deterministic=False)
-        assert np.abs(fast.ravel() - want).max() <= 1e-12 * np.abs(want).max()
+    # one NCCL all-reduce over distinct GPUs (partials added on one GPU otherwise)
+    fast, _ = mp.run_scheme(deterministic=False)
+    assert np.abs(fast.ravel() - want).max() <= 1e-12 * np.abs(want).max()
     mp.close()
 
 
