@@ -32,6 +32,8 @@ namespace stn {
 //   plan_dump, plan_timing                 per-step kernel choice / plan-build timing
 //   bitperm_legacy         legacy bit-permute kernel for the selftest
 //   sweep_only=..., no_bulk, tma_lag=N, tma_nsr=N, perm_tb=N   pipeline experiments
+//   tcf=0                  GEMM steps on the pre-split kernels of gemm_tc.cu
+//   tcf_bn=64|128|256      fused-split GEMM tile width
 //   mma_v1, mma_dbg=N, tma_dbg=N, absorb_loader=tma|gather, gemm_bn=N   kernel experiments
 // Returns the value ("" for a bare key) or nullptr when the key is absent. Read at
 // every call (tests change it at run time); returned strings stay valid.
@@ -331,5 +333,15 @@ void gemm_tc_a_planes(const GemmShape &s, const BatchPtrs &p, void *workspace, f
                       float **lo);
 size_t gemm_tc_workspace_bytes(const GemmShape &s, const BatchPtrs &p);
 bool gemm_tc_supported(const GemmShape &s);
+
+// tcgen05 split-TF32 complex GEMM with the split fused into shared memory
+// (gemm_tcf.cu): A (the [D|M|K] operand, read in place) and the raw B'' plane are
+// TMA-loaded as fp32 tiles, lo = x - trunc_tf32(x) is formed in shared memory.
+// Requires M % 128 == 0, N % 32 == 0, K % 32 == 0; A batch stride 0 or D*M*K.
+// Workspace: the raw B'' plane(s).
+bool gemm_tcf_supported(const GemmShape &s);
+size_t gemm_tcf_workspace_bytes(const GemmShape &s, const BatchPtrs &p);
+cudaError_t launch_gemm_tcf(const GemmShape &s, const BatchPtrs &p, void *workspace,
+                            size_t workspace_bytes, cudaStream_t stream);
 
 }  // namespace stn

@@ -248,6 +248,7 @@ struct StepPlan {
   stn::AbsorbGeom pag{}, pbg{}, pcg{};
   stn::GemmShape gs{};
   bool gemm_swap = false;            // operands exchanged: C^T = B^T A^T
+  bool tcf = false;                  // fused-split tcgen05 GEMM (gemm_tcf.cu)
   std::vector<int> gl, gr, go;       // GEMM operand A / B permutations, product -> output
   int64_t lsize = 0, rsize = 0, osize = 0;
   // split-K dot tables (device)
@@ -816,19 +817,21 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     // W's -- while long identity runs stay on the SIMT direct kernel (6+ TB/s).
     // STN_TMA_MIN_BITS=<bits> (experiments) forces it for every K x N >= 2^bits.
     const char *tmin = stn::debug_opt("tma_min_bits");
-    // lane-mapped SIMT absorb (any interleave of the low output bits) for small K x N
-    // where the direct stream does not apply (no identity run of >= 3 low bits).
-    // STN_LANES=0 (experiments) disables it, STN_LANES=all takes every eligible step.
-    {
-      const char *lp = stn::debug_opt("lanes");
-      const int policy = lp ? (std::string(lp) == "all" ? 2 : std::atoi(lp) != 0) : 1;
-      const int kn = int(sp.kbits.size() + sp.nbits.size());
-      const bool ok = sp.lane_tab && sp.lane_eff >= 0.5 && big >= (int64_t(1) << 16);
-      const bool direct_strong = sp.direct_ok && sp.dg.L >= 3;
-      if (ok && (policy == 2 || (policy == 1 && kn <= 8 && !direct_strong))) {
-        sp.kern = Kern::Lanes;
-        return;
-      }
+    // lane-mapped SIMT absorb (any interleave of the low output bits): where neither
+    // the direct stream (identity run of >= 3 low bits) nor the TMA-fed tensor-core
+    // absorb takes the step, it replaces the tiled SIMT absorb (measured on B200:
+    // cfg5 step 1606, 2^32 x 2 x 2: 28.6 -> 12.4 ms; step 693: 9.1 -> 1.9 ms), and it
+    // also takes the TMA steps with K x N <= 16 (cfg5 steps 1624 / 1628: 3.6 -> 2.7 ms;
+    // larger K x N stay on the tensor cores, e.g. cfg4 step 1040: 2.4 vs 4.9 ms).
+    // STN_DEBUG lanes=0 disables it, lanes=all takes every eligible step.
+    const char *lp = stn::debug_opt("lanes");
+    const int lanes_policy = lp ? (std::string(lp) == "all" ? 2 : std::atoi(lp) != 0) : 1;
+    const bool lanes_ok = sp.lane_tab && sp.lane_eff >= 0.5 && big >= (int64_t(1) << 16) &&
+                          lanes_policy > 0;
+    const int kn_bits = int(sp.kbits.size() + sp.nbits.size());
+    if (lanes_ok && (lanes_policy == 2 || (kn_bits <= 4 && !(sp.direct_ok && sp.dg.L >= 3)))) {
+      sp.kern = Kern::Lanes;
+      return;
     }
     if (!exact && sp.tg) {
       const int kn = int(sp.kbits.size() + sp.nbits.size());
@@ -847,6 +850,10 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     }
     if (sp.direct_ok && sp.dg.L >= direct_min_L && sp.dg.kb + sp.dg.nb <= direct_max) {
       sp.kern = Kern::AbsorbDirect;
+      return;
+    }
+    if (lanes_ok && !(sp.direct_ok && sp.dg.L >= 3)) {  // instead of the tiled SIMT absorb
+      sp.kern = Kern::Lanes;
       return;
     }
     if (!sp.tc_ok && sp.ag.xt_bits == 0) {  // no tile geometry: direct or generic
@@ -924,18 +931,25 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
   // dense GEMM path: materialise [D|M|K], [D|K|N], run GEMM, permute [D|M|N]
   if (d.M >= 8 && d.N >= 8 && d.K >= 8 && d.mults >= (uint64_t(1) << 18)) {
     sp.gs = {d.D, d.M, d.N, d.K};
-    const bool tc = single && !exact && stn::gemm_tc_supported(sp.gs);
-    sp.kern = tc ? Kern::GemmTc : Kern::GemmSimt;
-    // tcgen05 GEMM: the operand it expands (B -> 2N x 2K real, hi + lo) should be the
-    // small one; with a larger rhs compute C^T = B^T A^T ([D|N|K] x [D|K|M] -> [D|N|M])
+    // fused-split kernel (gemm_tcf.cu) unless STN_DEBUG tcf=0; else the pre-split one
+    const char *tcf_opt = stn::debug_opt("tcf");
+    const bool tcf_on = !(tcf_opt && std::atoi(tcf_opt) == 0);
+    auto tc_ok = [&](const stn::GemmShape &g) {
+      return tcf_on ? stn::gemm_tcf_supported(g) : stn::gemm_tc_supported(g);
+    };
+    const bool tc_fwd = single && !exact && tc_ok(sp.gs);
+    // tcgen05 GEMM: the operand it expands (B -> 2N x 2K real) should be the small one;
+    // with a larger rhs compute C^T = B^T A^T ([D|N|K] x [D|K|M] -> [D|N|M])
     sp.gemm_swap = false;
-    if (tc && sp.rsize > sp.lsize) {
-      const stn::GemmShape t{d.D, d.N, d.M, d.K};
-      if (stn::gemm_tc_supported(t)) {
-        sp.gemm_swap = true;
-        sp.gs = t;
-      }
+    const stn::GemmShape t{d.D, d.N, d.M, d.K};
+    const bool tc_swp = single && !exact && tc_ok(t);
+    if (tc_swp && (sp.rsize > sp.lsize || !tc_fwd)) {
+      sp.gemm_swap = true;
+      sp.gs = t;
     }
+    const bool tc = sp.gemm_swap || tc_fwd;
+    sp.kern = tc ? Kern::GemmTc : Kern::GemmSimt;
+    sp.tcf = tc && tcf_on;
     const int nd = d.nd, nm = d.nm, nk = d.nk, nn = d.nn;
     if (!sp.gemm_swap) {
       sp.gl = sp.lperm;
@@ -1462,8 +1476,8 @@ void build_program(stn_plan &P, Program &prog, int which /*0 build, 1 cache, 2 n
     if (sp.kern != Kern::GemmSimt && sp.kern != Kern::GemmTc) continue;
     // A needs no scratch when the skinny GEMM gathers it through its offset table or the
     // tile permute writes it straight into the tcgen05 workspace (a_fused in launch_op)
-    const bool a_in_place = sp.skinny_tab ||
-                            (sp.kern == Kern::GemmTc && sp.pa_bases && stn::gemm_tc_supported(sp.gs));
+    const bool a_in_place = sp.skinny_tab || (sp.kern == Kern::GemmTc && !sp.tcf && sp.pa_bases &&
+                                              stn::gemm_tc_supported(sp.gs));
     if (!sp.a_id && !a_in_place)
       scr[k][0] = new_item(sp.gemm_swap ? sp.rsize : sp.lsize, int64_t(k), int64_t(k));
     if (!sp.b_id) scr[k][1] = new_item(sp.gemm_swap ? sp.lsize : sp.rsize, int64_t(k), int64_t(k));
@@ -2078,7 +2092,7 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
       int64_t ga_bs = ra.bs, gb_bs = rb.bs;
       // tcgen05 GEMM with a permuted A: the tile permute writes A's TF32 hi / lo planes
       // straight into the GEMM workspace (one pass instead of permute + split)
-      const bool a_fused = sp.kern == Kern::GemmTc && !sp.a_id && sp.pa_bases &&
+      const bool a_fused = sp.kern == Kern::GemmTc && !sp.tcf && !sp.a_id && sp.pa_bases &&
                            stn::gemm_tc_supported(sp.gs);
       if (a_fused) {
         stn::BatchPtrs pp{nullptr, rb.ptr, nullptr, asize, rb.bs, 0, nb};
@@ -2128,7 +2142,15 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
       const double gbytes = es * (asize * (ga_bs ? nb : 1) + bsize * (gb_bs ? nb : 1) +
                                   double(sp.osize) * nb);
       bool done = false;
-      if (sp.kern == Kern::GemmTc) {
+      if (sp.kern == Kern::GemmTc && sp.tcf) {
+        const size_t ws = stn::gemm_tcf_workspace_bytes(sp.gs, p);
+        P.tc_workspace.reserve(std::max<size_t>(ws, 16));
+        cuda_check(stn::launch_gemm_tcf(sp.gs, p, P.tc_workspace.ptr, ws, st),
+                   "tcgen05 fused-split gemm");
+        prof.done(STN_KERNEL_GEMM_TC, gbytes, flops);
+        done = true;
+      }
+      if (sp.kern == Kern::GemmTc && !done) {
         size_t ws = stn::gemm_tc_workspace_bytes(sp.gs, p);
         P.tc_workspace.reserve(std::max<size_t>(ws, 16));
         cudaError_t e =
@@ -2670,8 +2692,20 @@ int stn_selftest_gemm_tc(int64_t M, int64_t N, int64_t K, int32_t batches, int32
                          double *ms_gemm, double *ms_simt, double *simt_rel_err) {
   return guarded([&] {
     stn::GemmShape s{1, M, N, K};
-    require(stn::gemm_tc_supported(s) && batches >= 1 && reps >= 1, STN_ERR_INVALID_ARGUMENT,
-            "shape not supported by the tensor-core GEMM");
+    // the fused-split kernel (gemm_tcf.cu) unless STN_DEBUG tcf=0 selects the pre-split one
+    const char *tcf_opt = stn::debug_opt("tcf");
+    const bool tcf = !(tcf_opt && std::atoi(tcf_opt) == 0);
+    require((tcf ? stn::gemm_tcf_supported(s) : stn::gemm_tc_supported(s)) && batches >= 1 &&
+                reps >= 1,
+            STN_ERR_INVALID_ARGUMENT, "shape not supported by the tensor-core GEMM");
+    auto run_tc = [&](const stn::BatchPtrs &pp, void *w, size_t wb, cudaStream_t ss,
+                      cudaEvent_t *gev) {
+      if (!tcf) return stn::launch_gemm_tc(s, pp, w, wb, ss, gev);
+      if (gev) cudaEventRecord(gev[0], ss);
+      cudaError_t e = stn::launch_gemm_tcf(s, pp, w, wb, ss);
+      if (gev) cudaEventRecord(gev[1], ss);
+      return e;
+    };
     const int64_t na = a_batched ? batches : 1, nbb = b_batched ? batches : 1;
     std::vector<float> ha(size_t(2 * M * K * na)), hb(size_t(2 * K * N * nbb));
     uint64_t x = 0x9E3779B97F4A7C15ull;
@@ -2695,12 +2729,12 @@ int stn_selftest_gemm_tc(int64_t M, int64_t N, int64_t K, int32_t batches, int32
                      batches};
     stn::BatchPtrs pd{Ad.ptr, Bd.ptr, Cd.ptr, a_batched ? M * K : 0, b_batched ? K * N : 0,
                       M * N, batches};
-    size_t wsb = stn::gemm_tc_workspace_bytes(s, p);
-    ws.reserve(wsb);
+    size_t wsb = tcf ? stn::gemm_tcf_workspace_bytes(s, p) : stn::gemm_tc_workspace_bytes(s, p);
+    ws.reserve(std::max<size_t>(wsb, 16));
     cudaStream_t st = nullptr;
     cudaEvent_t ev[4];
     for (auto &e : ev) cuda_check(cudaEventCreate(&e), "event");
-    cuda_check(stn::launch_gemm_tc(s, p, ws.ptr, wsb, st), "tc gemm");
+    cuda_check(run_tc(p, ws.ptr, wsb, st, nullptr), "tc gemm");
     cuda_check(stn::launch_gemm_simt<double>(s, pd, false, st), "simt gemm");
     cuda_check(cudaStreamSynchronize(st), "sync");
     std::vector<float> cf(size_t(2 * M * N * batches));
@@ -2715,7 +2749,7 @@ int stn_selftest_gemm_tc(int64_t M, int64_t N, int64_t K, int32_t batches, int32
     double tot = 0, gm = 0;
     for (int r = 0; r < reps; ++r) {
       cuda_check(cudaEventRecord(ev[0], st), "event");
-      cuda_check(stn::launch_gemm_tc(s, p, ws.ptr, wsb, st, &ev[2]), "tc gemm");
+      cuda_check(run_tc(p, ws.ptr, wsb, st, &ev[2]), "tc gemm");
       cuda_check(cudaEventRecord(ev[1], st), "event");
       cuda_check(cudaEventSynchronize(ev[1]), "sync");
       float a = 0, b = 0;

@@ -15,6 +15,7 @@ def _needs_gpu():
         pytest.skip("no CUDA device")
 
 
+@pytest.mark.parametrize("kernel", ["tcf", "presplit"])
 @pytest.mark.parametrize("M,N,K,batches,ab,bb", [
     (128, 128, 32, 1, 1, 1),
     (256, 128, 64, 3, 1, 0),
@@ -22,15 +23,23 @@ def _needs_gpu():
     (1024, 512, 1024, 1, 1, 1),
     (4096, 1024, 1024, 1, 1, 1),
     (256, 128, 16384, 1, 1, 1),  # long K: chunked TMEM accumulation keeps fp32 accuracy
+    (4096, 32, 8192, 1, 1, 1),   # cfg5's skinny steps (2N = 64: the 128 x 64 fused tile)
+    (512, 96, 512, 2, 1, 1),     # 2N = 192: 128 x 64 tiles
 ])
-def test_tc_gemm_matches_fp64(M, N, K, batches, ab, bb):
+def test_tc_gemm_matches_fp64(M, N, K, batches, ab, bb, kernel, monkeypatch):
+    """Both tcgen05 GEMMs: the fused-split one (gemm_tcf.cu, raw fp32 TMA tiles, lo
+    formed in shared memory) and the pre-split one (gemm_tc.cu, hi / lo planes)."""
     from paper_2005_06787_b200 import abi
+    if kernel == "presplit":
+        if (2 * N) % 128:
+            pytest.skip("the pre-split kernel needs 2N % 128 == 0")
+        monkeypatch.setenv("STN_DEBUG", "tcf=0")
     lib = abi.load_library()
     err, ms, msg, mss, serr = (C.c_double() for _ in range(5))
     abi.check(lib.stn_selftest_gemm_tc(M, N, K, batches, ab, bb, 3, C.byref(err), C.byref(ms),
                                        C.byref(msg), C.byref(mss), C.byref(serr)))
     fl = 8.0 * M * N * K * batches
-    print(f"tc gemm {M}x{N}x{K}x{batches}: rel err {err.value:.2e}, "
+    print(f"{kernel} gemm {M}x{N}x{K}x{batches}: rel err {err.value:.2e}, "
           f"{ms.value:.3f} ms total ({fl / ms.value / 1e9:.1f} TFLOP/s), {msg.value:.3f} ms gemm "
           f"({fl / msg.value / 1e9:.1f} TFLOP/s); simt fp32 {mss.value:.3f} ms "
           f"({fl / mss.value / 1e9:.1f} TFLOP/s), simt fp32 rel err {serr.value:.2e}")
