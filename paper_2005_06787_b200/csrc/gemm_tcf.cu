@@ -407,7 +407,7 @@ int pick_bn(const GemmShape &s) {
 }  // namespace
 
 bool gemm_tcf_supported(const GemmShape &s) {
-  return s.M % BM == 0 && (2 * s.N) % 64 == 0 && (2 * s.K) % BK == 0 && s.M >= BM &&
+  return s.M % BM == 0 && s.N % 32 == 0 && s.K % 32 == 0 && s.M >= BM &&
          s.M <= (int64_t(1) << 31) && s.N <= (int64_t(1) << 30) && s.K <= (int64_t(1) << 30);
 }
 

@@ -32,7 +32,7 @@ namespace stn {
 //   plan_dump, plan_timing                 per-step kernel choice / plan-build timing
 //   bitperm_legacy         legacy bit-permute kernel for the selftest
 //   sweep_only=..., no_bulk, tma_lag=N, tma_nsr=N, perm_tb=N   pipeline experiments
-//   tcf=0                  GEMM steps on the pre-split kernels of gemm_tc.cu
+//   tcf=0|1|2              fused-split GEMM never / for 2N <= 128 (default) / always
 //   tcf_bn=64|128|256      fused-split GEMM tile width
 //   mma_v1, mma_dbg=N, tma_dbg=N, absorb_loader=tma|gather, gemm_bn=N   kernel experiments
 // Returns the value ("" for a bare key) or nullptr when the key is absent. Read at

@@ -932,10 +932,18 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
   if (d.M >= 8 && d.N >= 8 && d.K >= 8 && d.mults >= (uint64_t(1) << 18)) {
     sp.gs = {d.D, d.M, d.N, d.K};
     // fused-split kernel (gemm_tcf.cu) unless STN_DEBUG tcf=0; else the pre-split one
+    // Measured on B200 (profiles/r02_gemm_tcf.txt): the fused-split kernel wins where
+    // the GEMM is operand-bandwidth bound (2N <= 128: cfg5's 32 x 32768 x 8192 step
+    // 7.6 -> 2.6 ms on tensor cores at all), the pre-split 128 x 256 kernel on the
+    // compute-bound wide GEMMs (212 vs 95 TFLOP/s at 4096 x 1024 x 1024).
     const char *tcf_opt = stn::debug_opt("tcf");
-    const bool tcf_on = !(tcf_opt && std::atoi(tcf_opt) == 0);
+    const int tcf_mode = tcf_opt ? std::atoi(tcf_opt) : 1;  // 0 never, 1 narrow, 2 always
+    auto use_tcf = [&](const stn::GemmShape &g) {
+      if (tcf_mode == 0 || !stn::gemm_tcf_supported(g)) return false;
+      return tcf_mode == 2 || 2 * g.N <= 128 || !stn::gemm_tc_supported(g);
+    };
     auto tc_ok = [&](const stn::GemmShape &g) {
-      return tcf_on ? stn::gemm_tcf_supported(g) : stn::gemm_tc_supported(g);
+      return stn::gemm_tc_supported(g) || use_tcf(g);
     };
     const bool tc_fwd = single && !exact && tc_ok(sp.gs);
     // tcgen05 GEMM: the operand it expands (B -> 2N x 2K real) should be the small one;
@@ -949,7 +957,7 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
     }
     const bool tc = sp.gemm_swap || tc_fwd;
     sp.kern = tc ? Kern::GemmTc : Kern::GemmSimt;
-    sp.tcf = tc && tcf_on;
+    sp.tcf = tc && use_tcf(sp.gs);
     const int nd = d.nd, nm = d.nm, nk = d.nk, nn = d.nn;
     if (!sp.gemm_swap) {
       sp.gl = sp.lperm;
@@ -2694,7 +2702,7 @@ int stn_selftest_gemm_tc(int64_t M, int64_t N, int64_t K, int32_t batches, int32
     stn::GemmShape s{1, M, N, K};
     // the fused-split kernel (gemm_tcf.cu) unless STN_DEBUG tcf=0 selects the pre-split one
     const char *tcf_opt = stn::debug_opt("tcf");
-    const bool tcf = !(tcf_opt && std::atoi(tcf_opt) == 0);
+    const bool tcf = !(tcf_opt && std::atoi(tcf_opt) == 0);  // selftest: 0 pre-split, else fused
     require((tcf ? stn::gemm_tcf_supported(s) : stn::gemm_tc_supported(s)) && batches >= 1 &&
                 reps >= 1,
             STN_ERR_INVALID_ARGUMENT, "shape not supported by the tensor-core GEMM");
