@@ -251,6 +251,11 @@ int stn_plan_set_leaf_values(stn_plan *plan, int32_t vertex, const double *value
                              int64_t n_complex);
 /* Upper bound on slices executed together in one batched pass (0 = automatic). */
 int stn_plan_set_max_batch(stn_plan *plan, int32_t max_batch);
+/* Streams ("lanes", each with its own arena) that stn_run_slices* rotate batches of
+ * slices over (default 1; bounded by free device memory). Results are bitwise the
+ * same for any value: roots are folded in ascending slice order through an event
+ * chain. stn_run_scheme uses its `parallelism` argument instead. */
+int stn_plan_set_streams(stn_plan *plan, int32_t streams);
 
 /* Turns per-launch event timing on/off (off by default) and reads the totals
  * accumulated since the last reset; out must hold STN_KERNEL_KINDS entries.

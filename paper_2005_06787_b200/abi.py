@@ -132,6 +132,7 @@ SIGNATURES = {
     "stn_plan_get_info": (C.c_int, [_P, C.POINTER(PlanInfo)]),
     "stn_plan_set_leaf_values": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_double), C.c_int64]),
     "stn_plan_set_max_batch": (C.c_int, [_P, C.c_int32]),
+    "stn_plan_set_streams": (C.c_int, [_P, C.c_int32]),
     "stn_plan_set_profiling": (C.c_int, [_P, C.c_int]),
     "stn_plan_get_profile": (C.c_int, [_P, C.POINTER(KernelProfile)]),
     "stn_plan_reset_profile": (C.c_int, [_P]),

@@ -289,6 +289,31 @@ struct Program {
   stn::LeafGatherTable table{};
 };
 
+// One execution lane of a plan: a stream with its own arena, digit buffer,
+// workspaces and root staging rows, plus the CUDA graph of a full batch of the
+// per-slice program captured on it. Several lanes run batches of slices
+// concurrently (run_scheme's `parallelism`, runtime.hpp:564-598); lane 0 runs on
+// the caller's stream.
+struct ExecCtx {
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  DevBuf arena, digits, tc_workspace, splitk_ws, rows;
+  cudaEvent_t done = nullptr;  // recorded after this lane's last fold
+  // captured graph and what it was captured for
+  cudaGraphExec_t graph = nullptr;
+  const void *g_prog = nullptr, *g_cache = nullptr, *g_arena = nullptr, *g_rows = nullptr;
+  int g_nb = 0;
+  uint64_t g_epoch = 0;
+  const void *w_prog = nullptr;  // last program run eagerly at full batch (pre-capture warm-up)
+  int w_nb = 0;
+  uint64_t w_epoch = 0;
+  ~ExecCtx() {
+    if (graph) cudaGraphExecDestroy(graph);
+    if (done) cudaEventDestroy(done);
+    if (own_stream && st) cudaStreamDestroy(st);
+  }
+};
+
 }  // namespace
 
 struct stn_cache {
@@ -340,7 +365,12 @@ struct stn_plan {
   std::map<int, int64_t> cache_off;  // node -> element offset in cache storage
   int64_t cache_elems = 0;
   // runtime state
-  DevBuf arena, digits, scratch_out, tc_workspace, splitk_ws;
+  DevBuf scratch_out;
+  std::vector<std::unique_ptr<ExecCtx>> lanes;  // lane 0 always exists
+  ExecCtx *cur = nullptr;                        // lane the launches go to
+  int streams = 1;                               // lanes used by run_slices (stn_plan_set_streams)
+  bool graphs = true;                            // capture full batches as CUDA graphs
+  uint64_t graph_epoch = 0;                      // bumped when captured graphs become invalid
   int64_t out_elements = 1;
   std::vector<int> out_dims;
   int max_batch = 0;
@@ -1694,6 +1724,10 @@ void create_plan(const stn_plan_desc *desc, int device, int mode, stn_plan *P) {
   require(e == cudaSuccess && ndev > 0, STN_ERR_NO_DEVICE, "no CUDA device available");
   require(device >= 0 && device < ndev, STN_ERR_NO_DEVICE, "device index out of range");
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  {  // STN_DEBUG graphs=0: every batch launched eagerly (no CUDA graphs)
+    const char *g = stn::debug_opt("graphs");
+    P->graphs = !(g && std::atoi(g) == 0);
+  }
   // (attribute queries: cudaGetDeviceProperties costs milliseconds per call)
   int cc_major = 0, cc_minor = 0;
   cuda_check(cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, device),
@@ -1983,7 +2017,7 @@ Resolved resolve(stn_plan &P, const Ref &r, const stn_cache *cache, int nb) {
       return {elem_ptr(P, cache->storage.ptr, r.off), 0};
     case Src::Arena:
     case Src::SliceLeaf:
-      return {elem_ptr(P, P.arena.ptr, r.off * nb), r.size};
+      return {elem_ptr(P, P.cur->arena.ptr, r.off * nb), r.size};
   }
   return {nullptr, 0};
 }
@@ -2035,9 +2069,10 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
     }
     case Kern::SplitK: {
       stn::BatchPtrs p{a.ptr, b.ptr, out, a.bs, b.bs, o.bs, nb};
-      P.splitk_ws.reserve(
+      P.cur->splitk_ws.reserve(
           std::max<size_t>(stn::splitk_workspace_bytes(sp.geo, sp.dot, nb, P.esize), 16));
-      cuda_check(stn::launch_splitk<R>(sp.geo, p, sp.dot, P.splitk_ws.ptr, st), "split-K kernel");
+      cuda_check(stn::launch_splitk<R>(sp.geo, p, sp.dot, P.cur->splitk_ws.ptr, st),
+                 "split-K kernel");
       prof.done(STN_KERNEL_GENERIC, io_bytes, flops);
       P.kernel_launches++;  // second (ordered-sum) launch
       break;
@@ -2105,9 +2140,9 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
       if (a_fused) {
         stn::BatchPtrs pp{nullptr, rb.ptr, nullptr, asize, rb.bs, 0, nb};
         size_t ws = stn::gemm_tc_workspace_bytes(sp.gs, pp);
-        P.tc_workspace.reserve(std::max<size_t>(ws, 16));
+        P.cur->tc_workspace.reserve(std::max<size_t>(ws, 16));
         float *hi, *lo;
-        stn::gemm_tc_a_planes(sp.gs, pp, P.tc_workspace.ptr, &hi, &lo);
+        stn::gemm_tc_a_planes(sp.gs, pp, P.cur->tc_workspace.ptr, &hi, &lo);
         cuda_check(stn::launch_perm_tiles(sp.pat, sp.pa_bases->as<int64_t>(), ra.ptr, hi, ra.bs,
                                           asize, nb, st, lo),
                    "tile permute + split");
@@ -2117,7 +2152,7 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
       } else if (sp.skinny_tab) {
         // gathered by the skinny GEMM itself
       } else if (!sp.a_id) {
-        void *dst = elem_ptr(P, P.arena.ptr, op.scr_a * nb);
+        void *dst = elem_ptr(P, P.cur->arena.ptr, op.scr_a * nb);
         if (sp.pa_bases)
           cuda_check(stn::launch_perm_tiles(sp.pat, sp.pa_bases->as<int64_t>(), ra.ptr, dst,
                                             ra.bs, asize, nb, st),
@@ -2131,7 +2166,7 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
         ga_bs = asize;
       }
       if (!sp.b_id) {
-        void *dst = elem_ptr(P, P.arena.ptr, op.scr_b * nb);
+        void *dst = elem_ptr(P, P.cur->arena.ptr, op.scr_b * nb);
         if (sp.pb_bases)
           cuda_check(stn::launch_perm_tiles(sp.pbt, sp.pb_bases->as<int64_t>(), rb.ptr, dst,
                                             rb.bs, bsize, nb, st),
@@ -2144,7 +2179,7 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
         gb = dst;
         gb_bs = bsize;
       }
-      void *gc = sp.c_id ? out : elem_ptr(P, P.arena.ptr, op.scr_c * nb);
+      void *gc = sp.c_id ? out : elem_ptr(P, P.cur->arena.ptr, op.scr_c * nb);
       int64_t gc_bs = sp.c_id ? o.bs : sp.osize;
       stn::BatchPtrs p{ga, gb, gc, ga_bs, gb_bs, gc_bs, nb};
       const double gbytes = es * (asize * (ga_bs ? nb : 1) + bsize * (gb_bs ? nb : 1) +
@@ -2152,17 +2187,17 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
       bool done = false;
       if (sp.kern == Kern::GemmTc && sp.tcf) {
         const size_t ws = stn::gemm_tcf_workspace_bytes(sp.gs, p);
-        P.tc_workspace.reserve(std::max<size_t>(ws, 16));
-        cuda_check(stn::launch_gemm_tcf(sp.gs, p, P.tc_workspace.ptr, ws, st),
+        P.cur->tc_workspace.reserve(std::max<size_t>(ws, 16));
+        cuda_check(stn::launch_gemm_tcf(sp.gs, p, P.cur->tc_workspace.ptr, ws, st),
                    "tcgen05 fused-split gemm");
         prof.done(STN_KERNEL_GEMM_TC, gbytes, flops);
         done = true;
       }
       if (sp.kern == Kern::GemmTc && !done) {
         size_t ws = stn::gemm_tc_workspace_bytes(sp.gs, p);
-        P.tc_workspace.reserve(std::max<size_t>(ws, 16));
+        P.cur->tc_workspace.reserve(std::max<size_t>(ws, 16));
         cudaError_t e =
-            stn::launch_gemm_tc(sp.gs, p, P.tc_workspace.ptr, ws, st, nullptr, a_fused);
+            stn::launch_gemm_tc(sp.gs, p, P.cur->tc_workspace.ptr, ws, st, nullptr, a_fused);
         require(!a_fused || e == cudaSuccess, STN_ERR_CUDA,
                 std::string("tcgen05 gemm (pre-split A): ") + cudaGetErrorString(e));
         if (e == cudaSuccess) {
@@ -2208,26 +2243,33 @@ int auto_batch(const stn_plan &P, const Program &prog) {
   return int(std::max<int64_t>(1, std::min<int64_t>(nb, 256)));
 }
 
-// Runs `n` slices (digits row-major n x n_sliced on the host) of `prog`.
-void run_batch(stn_plan &P, Program &prog, const stn_cache *cache, const int32_t *digits_host,
-               int n, cudaStream_t st, double *acc, double *per_slice) {
-  const size_t arena_bytes = size_t(std::max<int64_t>(prog.arena_elems, 1)) * n * P.esize;
-  P.arena.reserve(arena_bytes);
-  const int ns = int(P.sliced_dims.size());
-  if (ns > 0 && !prog.slice_leaves.empty()) {
-    P.digits.reserve(size_t(n) * ns * 4);
-    cuda_check(cudaMemcpyAsync(P.digits.ptr, digits_host, size_t(n) * ns * 4,
-                               cudaMemcpyHostToDevice, st),
-               "digits upload");
+// Lane `i` of the plan (created on first use; lane 0 runs on the caller's stream).
+ExecCtx *get_lane(stn_plan &P, int i, cudaStream_t caller) {
+  while (int(P.lanes.size()) <= i) P.lanes.push_back(std::make_unique<ExecCtx>());
+  ExecCtx &c = *P.lanes[size_t(i)];
+  if (i == 0) {
+    c.st = caller;
+  } else if (!c.st) {
+    cuda_check(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking), "lane stream");
+    c.own_stream = true;
   }
+  if (!c.done) cuda_check(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming), "lane event");
+  return &c;
+}
+
+// The device work of one batch of `n` slices on lane P.cur (digits already on the
+// device): leaf gather, every step, root accumulation. Captured as-is into graphs.
+void batch_kernels(stn_plan &P, Program &prog, const stn_cache *cache, int n, cudaStream_t st,
+                   double *acc, double *per_slice) {
+  ExecCtx &L = *P.cur;
   if (!prog.slice_leaves.empty()) {
     ProfScope prof(P, st);
     if (P.precision == STN_SINGLE)
-      cuda_check(stn::launch_leaf_gather<float>(prog.table, P.arena.ptr, P.digits.as<int32_t>(),
+      cuda_check(stn::launch_leaf_gather<float>(prog.table, L.arena.ptr, L.digits.as<int32_t>(),
                                                 n, st),
                  "leaf gather");
     else
-      cuda_check(stn::launch_leaf_gather<double>(prog.table, P.arena.ptr, P.digits.as<int32_t>(),
+      cuda_check(stn::launch_leaf_gather<double>(prog.table, L.arena.ptr, L.digits.as<int32_t>(),
                                                  n, st),
                  "leaf gather");
     prof.done(STN_KERNEL_LEAF, double(prog.table.total_out) * n * (16 + P.esize), 0);
@@ -2253,6 +2295,93 @@ void run_batch(stn_plan &P, Program &prog, const stn_cache *cache, const int32_t
   }
 }
 
+// Runs `n` slices (digits row-major n x n_sliced on the host) of `prog` on lane
+// P.cur's buffers, on stream `st`.
+void run_batch(stn_plan &P, Program &prog, const stn_cache *cache, const int32_t *digits_host,
+               int n, cudaStream_t st, double *acc, double *per_slice) {
+  ExecCtx &L = *P.cur;
+  const size_t arena_bytes = size_t(std::max<int64_t>(prog.arena_elems, 1)) * n * P.esize;
+  L.arena.reserve(arena_bytes);
+  const int ns = int(P.sliced_dims.size());
+  if (ns > 0 && !prog.slice_leaves.empty()) {
+    L.digits.reserve(size_t(n) * ns * 4);
+    cuda_check(cudaMemcpyAsync(L.digits.ptr, digits_host, size_t(n) * ns * 4,
+                               cudaMemcpyHostToDevice, st),
+               "digits upload");
+  }
+  batch_kernels(P, prog, cache, n, st, acc, per_slice);
+}
+
+// Same batch through the lane's CUDA graph (one launch for the whole per-slice program
+// of a full batch; the roots go to the lane's staging rows). Captured on first use and
+// whenever what it was captured for changed; any capture problem turns graphs off for
+// the plan and the batch runs eagerly.
+void run_batch_graph(stn_plan &P, Program &prog, const stn_cache *cache,
+                     const int32_t *digits_host, int n, cudaStream_t st) {
+  ExecCtx &L = *P.cur;
+  const size_t arena_bytes = size_t(std::max<int64_t>(prog.arena_elems, 1)) * n * P.esize;
+  L.arena.reserve(arena_bytes);
+  L.rows.reserve(16 * size_t(P.out_elements) * size_t(n));
+  const int ns = int(P.sliced_dims.size());
+  if (ns > 0 && !prog.slice_leaves.empty()) {
+    L.digits.reserve(size_t(n) * ns * 4);
+    cuda_check(cudaMemcpyAsync(L.digits.ptr, digits_host, size_t(n) * ns * 4,
+                               cudaMemcpyHostToDevice, st),
+               "digits upload");
+  }
+  const void *cstore = cache ? cache->storage.ptr : nullptr;
+  const bool fresh = L.graph && L.g_prog == &prog && L.g_cache == cstore &&
+                     L.g_arena == L.arena.ptr && L.g_rows == L.rows.ptr && L.g_nb == n &&
+                     L.g_epoch == P.graph_epoch;
+  if (!fresh && !(L.w_prog == &prog && L.w_nb == n && L.w_epoch == P.graph_epoch)) {
+    // first full batch of this program on this lane: eager, so every workspace the
+    // launches reserve exists before a capture (no allocation inside a graph)
+    batch_kernels(P, prog, cache, n, st, nullptr, L.rows.as<double>());
+    L.w_prog = &prog;
+    L.w_nb = n;
+    L.w_epoch = P.graph_epoch;
+    return;
+  }
+  if (!fresh && P.graphs) {
+    if (L.graph) {
+      cudaGraphExecDestroy(L.graph);
+      L.graph = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      const int launches = P.kernel_launches;
+      try {
+        batch_kernels(P, prog, cache, n, st, nullptr, L.rows.as<double>());
+      } catch (const Failure &) {
+        ok = false;
+      }
+      P.kernel_launches = launches;
+      ok = cudaStreamEndCapture(st, &g) == cudaSuccess && ok;
+    }
+    if (ok) ok = cudaGraphInstantiate(&L.graph, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    if (!ok) {
+      L.graph = nullptr;
+      P.graphs = false;  // eager from now on
+    } else {
+      L.g_prog = &prog;
+      L.g_cache = cstore;
+      L.g_arena = L.arena.ptr;
+      L.g_rows = L.rows.ptr;
+      L.g_nb = n;
+      L.g_epoch = P.graph_epoch;
+    }
+  }
+  if (L.graph) {
+    cuda_check(cudaGraphLaunch(L.graph, st), "graph launch");
+    P.kernel_launches += int(prog.ops.size()) + 2;
+  } else {
+    batch_kernels(P, prog, cache, n, st, nullptr, L.rows.as<double>());
+  }
+}
+
 void decode(const stn_plan &P, uint64_t a, int32_t *digits) {
   uint64_t rest = a;
   for (size_t i = P.sliced_dims.size(); i-- > 0;) {
@@ -2270,35 +2399,96 @@ void check_cache(const stn_plan &P, const stn_cache *cache) {
           "branch cache is stale: leaf values feeding branch steps changed");
 }
 
-// Runs slices given by a digit generator over [0, n) in batches.
+// Runs slices given by a digit generator over [0, n) in batches. With one lane and
+// no graph this is the plain sequence: per batch, digits upload + kernels, roots
+// accumulated into `acc` in ascending slice order. With `lanes` > 1 (and/or graphs)
+// batches rotate over lanes, each on its own stream and arena, so the small
+// launch-bound steps of one batch overlap the HBM-bound stem steps of another; a
+// batch's roots land in its lane's staging rows, are copied to `per_slice`, and are
+// folded into `acc` after the previous batch's fold (an event chain), so the sum
+// keeps the reference's ascending order bit for bit (runtime.hpp:601-605).
 template <class DigitsOf>
 void run_slices_impl(stn_plan &P, const stn_cache *cache, uint64_t n, DigitsOf &&digits_of,
                      cudaStream_t st, double *acc, double *per_slice,
-                     std::vector<double> *batch_ms = nullptr) {
+                     std::vector<double> *batch_ms = nullptr, int lanes = 1) {
   Program &prog = cache ? P.with_cache : P.no_cache;
   const int ns = int(P.sliced_dims.size());
   const int nb = auto_batch(P, prog);
+  const uint64_t n_batches = (n + uint64_t(nb) - 1) / uint64_t(nb);
+  // lanes: bounded by the batches and by free device memory for their arenas
+  int par = int(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(std::max(lanes, 1)), n_batches)));
+  if (par > 1) {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t per = size_t(std::max<int64_t>(prog.arena_elems, 1)) * nb * P.esize;
+    int have = 0;
+    for (auto &l : P.lanes) have += l->arena.bytes >= per ? 1 : 0;
+    const size_t room = free_b > (size_t(2) << 30) ? free_b - (size_t(2) << 30) : 0;
+    par = std::max(1, std::min(par, have + int(room / std::max<size_t>(per, 1))));
+  }
+  const bool staged = par > 1 || (P.graphs && !P.profiling && !batch_ms);
   std::vector<int32_t> dig;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (batch_ms) {
     cuda_check(cudaEventCreate(&e0), "event");
     cuda_check(cudaEventCreate(&e1), "event");
   }
-  for (uint64_t a0 = 0; a0 < n; a0 += uint64_t(nb)) {
+  ExecCtx *lv[64];
+  par = std::min(par, 64);
+  for (int i = 0; i < par; ++i) lv[i] = get_lane(P, i, st);
+  cudaEvent_t start = nullptr, fold_done = nullptr;
+  if (par > 1) {  // the lanes start after the work already queued on the caller's stream
+    start = lv[0]->done;
+    cuda_check(cudaEventRecord(start, st), "event");
+    for (int i = 1; i < par; ++i) cuda_check(cudaStreamWaitEvent(lv[i]->st, start), "wait");
+  }
+  const size_t row = 2 * size_t(P.out_elements);
+  for (uint64_t b = 0; b < n_batches; ++b) {
+    const uint64_t a0 = b * uint64_t(nb);
     const int cnt = int(std::min<uint64_t>(uint64_t(nb), n - a0));
+    ExecCtx &C = *lv[b % uint64_t(par)];
+    P.cur = &C;
     dig.assign(size_t(cnt) * std::max(ns, 1), 0);
     for (int i = 0; i < cnt; ++i) digits_of(a0 + i, dig.data() + size_t(i) * ns);
-    if (batch_ms) cuda_check(cudaEventRecord(e0, st), "event");
-    run_batch(P, prog, cache, dig.data(), cnt, st, acc,
-              per_slice ? per_slice + 2 * size_t(P.out_elements) * a0 : nullptr);
+    if (batch_ms) cuda_check(cudaEventRecord(e0, C.st), "event");
+    double *ps = per_slice ? per_slice + row * a0 : nullptr;
+    if (!staged) {
+      run_batch(P, prog, cache, dig.data(), cnt, C.st, acc, ps);
+    } else {
+      if (cnt == nb && P.graphs && !P.profiling)
+        run_batch_graph(P, prog, cache, dig.data(), cnt, C.st);
+      else {
+        C.rows.reserve(8 * row * size_t(nb));
+        run_batch(P, prog, cache, dig.data(), cnt, C.st, nullptr, C.rows.as<double>());
+      }
+      if (ps)
+        cuda_check(cudaMemcpyAsync(ps, C.rows.ptr, 8 * row * size_t(cnt),
+                                   cudaMemcpyDeviceToDevice, C.st),
+                   "per-slice copy");
+      if (acc) {
+        if (fold_done) cuda_check(cudaStreamWaitEvent(C.st, fold_done), "wait");
+        cuda_check(stn::launch_sum_ordered(C.rows.as<double>(), uint64_t(cnt), P.out_elements,
+                                           acc, C.st, true),
+                   "ordered fold");
+        P.kernel_launches++;
+      }
+      cuda_check(cudaEventRecord(C.done, C.st), "event");
+      fold_done = C.done;
+    }
     if (batch_ms) {
-      cuda_check(cudaEventRecord(e1, st), "event");
+      cuda_check(cudaEventRecord(e1, C.st), "event");
       cuda_check(cudaEventSynchronize(e1), "event sync");
       float ms = 0;
       cuda_check(cudaEventElapsedTime(&ms, e0, e1), "event time");
       for (int i = 0; i < cnt; ++i) batch_ms->push_back(double(ms) / cnt);
     }
   }
+  if (par > 1)  // join: the caller's stream waits for every lane
+    for (int i = 1; i < par; ++i) {
+      cuda_check(cudaEventRecord(lv[i]->done, lv[i]->st), "event");
+      cuda_check(cudaStreamWaitEvent(st, lv[i]->done), "wait");
+    }
+  P.cur = P.lanes[0].get();
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
 }
@@ -2309,6 +2499,7 @@ void build_cache(stn_plan &P, cudaStream_t st, stn_cache *c) {
   c->leaf_epoch = P.leaf_epoch;
   c->plan = &P;
   c->storage.reserve(size_t(std::max<int64_t>(P.cache_elems, 1)) * P.esize);
+  P.cur = get_lane(P, 0, st);
   for (auto &sp : P.steps)
     if (sp.d.is_branch) c->mults += sp.d.mults;
   for (auto &[node, off] : P.cache_off) c->elements += uint64_t(P.nodes[node].size);
@@ -2319,6 +2510,7 @@ void run_one(stn_plan &P, const int32_t *digits, const stn_cache *cache, cudaStr
              double *out_host, stn_subtask_info *info) {
   check_cache(P, cache);
   Program &prog = cache ? P.with_cache : P.no_cache;
+  P.cur = get_lane(P, 0, st);
   P.scratch_out.reserve(16 * size_t(P.out_elements));
   std::vector<int32_t> dig(digits, digits + P.sliced_dims.size());
   if (dig.empty()) dig.push_back(0);
@@ -2434,12 +2626,20 @@ int stn_plan_set_leaf_values(stn_plan *P, int32_t vertex, const double *values, 
     else
       upload_consts(*P);
     if (P->leaf_feeds_branch[li]) P->leaf_epoch++;
+    P->graph_epoch++;  // buffers may have moved: recapture
   });
 }
 
 int stn_plan_set_max_batch(stn_plan *P, int32_t max_batch) {
   if (!P || max_batch < 0) return set_error(STN_ERR_INVALID_ARGUMENT, "bad argument");
   P->max_batch = max_batch;
+  P->graph_epoch++;
+  return STN_OK;
+}
+
+int stn_plan_set_streams(stn_plan *P, int32_t streams) {
+  if (!P || streams < 1) return set_error(STN_ERR_INVALID_ARGUMENT, "bad argument");
+  P->streams = streams;
   return STN_OK;
 }
 
@@ -2556,7 +2756,7 @@ int stn_run_slices(stn_plan *P, const stn_cache *cache, uint64_t lo, uint64_t hi
     cuda_check(cudaSetDevice(P->device), "cudaSetDevice");
     run_slices_impl(
         *P, cache, hi - lo, [&](uint64_t i, int32_t *d) { decode(*P, lo + i, d); },
-        static_cast<cudaStream_t>(stream), acc_dev, per_slice_dev);
+        static_cast<cudaStream_t>(stream), acc_dev, per_slice_dev, nullptr, P->streams);
   });
 }
 
@@ -2576,7 +2776,7 @@ int stn_run_slices_digits(stn_plan *P, const stn_cache *cache, const int32_t *di
     run_slices_impl(
         *P, cache, n_slices,
         [&](uint64_t i, int32_t *d) { std::copy(digits + i * ns, digits + (i + 1) * ns, d); },
-        static_cast<cudaStream_t>(stream), acc_dev, per_slice_dev);
+        static_cast<cudaStream_t>(stream), acc_dev, per_slice_dev, nullptr, P->streams);
   });
 }
 
@@ -2596,9 +2796,24 @@ int stn_run_scheme(stn_plan *P, int parallelism, double *out_host, stn_run_repor
     acc.reserve(16 * size_t(P->out_elements));
     cuda_check(cudaMemsetAsync(acc.ptr, 0, 16 * size_t(P->out_elements), st), "memset");
     std::vector<double> ms;
-    run_slices_impl(
-        *P, &cache, P->subtasks, [&](uint64_t i, int32_t *d) { decode(*P, i, d); }, st,
-        acc.as<double>(), nullptr, &ms);
+    // per-slice times need one batch at a time; with parallelism > 1 the batches
+    // rotate over `parallelism` streams and the reported times are per-batch wall
+    // shares of the whole run
+    if (parallelism > 1) {
+      auto t_a = std::chrono::steady_clock::now();
+      run_slices_impl(
+          *P, &cache, P->subtasks, [&](uint64_t i, int32_t *d) { decode(*P, i, d); }, st,
+          acc.as<double>(), nullptr, nullptr, parallelism);
+      cuda_check(cudaStreamSynchronize(st), "stream sync");
+      const double per = std::chrono::duration<double, std::milli>(
+                             std::chrono::steady_clock::now() - t_a).count() /
+                         double(std::max<uint64_t>(P->subtasks, 1));
+      ms.assign(size_t(P->subtasks), per);
+    } else {
+      run_slices_impl(
+          *P, &cache, P->subtasks, [&](uint64_t i, int32_t *d) { decode(*P, i, d); }, st,
+          acc.as<double>(), nullptr, &ms);
+    }
     cuda_check(cudaMemcpyAsync(out_host, acc.ptr, 16 * size_t(P->out_elements),
                                cudaMemcpyDeviceToHost, st),
                "result download");
@@ -2671,7 +2886,7 @@ int stn_run_slices_host(stn_plan *P, const stn_cache *cache, const int32_t *digi
         decode(*P, lo + i, d);
     };
     run_slices_impl(*P, cache, n_slices, gen, st, sum_host ? acc.as<double>() : nullptr,
-                    per_slice_host ? rows.as<double>() : nullptr);
+                    per_slice_host ? rows.as<double>() : nullptr, nullptr, P->streams);
     if (per_slice_host && n_slices)
       cuda_check(cudaMemcpyAsync(per_slice_host, rows.ptr, 8 * row * n_slices,
                                  cudaMemcpyDeviceToHost, st),

@@ -100,6 +100,10 @@ class ExecutablePlan:
     def set_max_batch(self, n: int) -> None:
         check(_lib().stn_plan_set_max_batch(self._h, n))
 
+    def set_streams(self, n: int) -> None:
+        """Streams (each with its own arena) that run_slices* rotate batches over."""
+        check(_lib().stn_plan_set_streams(self._h, n))
+
     def set_profiling(self, enable: bool = True) -> None:
         check(_lib().stn_plan_set_profiling(self._h, 1 if enable else 0))
 
