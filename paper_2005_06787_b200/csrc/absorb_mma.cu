@@ -426,7 +426,8 @@ template <int KB, int NM>
 cudaError_t launch_mma_impl(const DirectGeom &g, const BatchPtrs &p, cudaStream_t stream) {
   using Lay = MmaLayout<KB == 6 ? 64 : 32, NM>;
   auto kern = k_absorb_mma<KB, NM>;
-  static bool set = false;
+  static bool set_on[kMaxDevices] = {};
+  bool &set = set_on[current_device()];
   if (!set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(Lay::SMEM));
@@ -711,7 +712,8 @@ template <int KB, int NM>
 cudaError_t launch_mma2_impl(const DirectGeom &g, const BatchPtrs &p, cudaStream_t stream) {
   using Lay = Mma2Layout<KB, NM>;
   auto kern = k_absorb_mma2<KB, NM>;
-  static bool set = false;
+  static bool set_on[kMaxDevices] = {};
+  bool &set = set_on[current_device()];
   if (!set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(Lay::SMEM));

@@ -353,7 +353,8 @@ cudaError_t launch_tc_absorb_impl(const AbsorbGeom &g, const BatchPtrs &p, cudaS
   const size_t smem = tc_absorb_smem<KP, NP>(g);
   if (smem > 220 * 1024) return cudaErrorNotSupported;
   auto kern = k_absorb_tc<KP, NP>;
-  static bool set = false;
+  static bool set_on[kMaxDevices] = {};
+  bool &set = set_on[current_device()];
   if (!set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          220 * 1024);

@@ -519,7 +519,8 @@ cudaError_t launch_tma_impl(const TmaAbsorbGeom &g, const BatchPtrs &p, cudaStre
     }
     gl = t;
   }
-  static bool set = false;
+  static bool set_on[kMaxDevices] = {};
+  bool &set = set_on[current_device()];
   if (!set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(227 * 1024));

@@ -610,7 +610,8 @@ cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspa
       !make_map(&mbh, bhi, 2 * s.K, 2 * s.N, nbB, bn) ||
       !make_map(&mbl, blo, 2 * s.K, 2 * s.N, nbB, bn))
     return cudaErrorNotSupported;
-  static bool attr_set = false;
+  static bool attr_on[kMaxDevices] = {};
+  bool &attr_set = attr_on[current_device()];
   if (!attr_set) {
     cudaError_t e =
         cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SMEM_BYTES));

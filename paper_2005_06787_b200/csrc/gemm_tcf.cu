@@ -382,13 +382,14 @@ template <int BN>
 cudaError_t launch_bn(const CUtensorMap &ma, const CUtensorMap &mb, const TcfArgs &args,
                       dim3 grid, cudaStream_t stream) {
   using C = Cfg<BN>;
-  static std::once_flag once;
-  static cudaError_t attr = cudaSuccess;
-  std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(k_gemm_tcf<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(C::SMEM));
-  });
-  if (attr != cudaSuccess) return attr;
+  static bool set_on[kMaxDevices] = {};
+  bool &set = set_on[current_device()];
+  if (!set) {
+    const cudaError_t attr = cudaFuncSetAttribute(
+        k_gemm_tcf<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+    if (attr != cudaSuccess) return attr;
+    set = true;
+  }
   k_gemm_tcf<BN><<<grid, C::THREADS, C::SMEM, stream>>>(ma, mb, args);
   return cudaGetLastError();
 }

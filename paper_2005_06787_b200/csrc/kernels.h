@@ -60,6 +60,15 @@ inline const char *debug_opt(const char *key) {
   return nullptr;
 }
 
+// Index of the current CUDA device: function attributes (dynamic shared-memory
+// opt-in) are per device context, so "set once" flags are kept per device.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
+
 constexpr int kMaxAxes = 40;
 
 // Generic strided contraction (any bond dimensions, D batches included):

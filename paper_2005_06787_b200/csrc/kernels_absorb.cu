@@ -408,7 +408,8 @@ cudaError_t launch_absorb3_impl(const AbsorbGeom &g, const BatchPtrs &p, cudaStr
   const size_t smem = absorb3_smem_bytes(g, PERMUTE);
   if (smem > 220 * 1024) return cudaErrorNotSupported;
   auto kern = k_absorb3<EXACT, PERMUTE, KC, NC, BLOCKED>;
-  static bool set = false;
+  static bool set_on[kMaxDevices] = {};
+  bool &set = set_on[current_device()];
   if (!set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          220 * 1024);
@@ -445,7 +446,8 @@ template <bool EXACT, bool PERMUTE, int KC, int NC, bool BLOCKED = false>
 cudaError_t launch_absorb2_impl(const AbsorbGeom &g, const BatchPtrs &p, cudaStream_t stream) {
   const size_t smem = absorb2_smem_bytes(g, PERMUTE);
   auto kern = k_absorb2<EXACT, PERMUTE, KC, NC, BLOCKED>;
-  static int set_bytes = 0;
+  static int set_bytes_on[kMaxDevices] = {};
+  int &set_bytes = set_bytes_on[current_device()];
   if (int(smem) > set_bytes) {
     const int want = smem > 48 * 1024 ? 200 * 1024 : 48 * 1024;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, want);

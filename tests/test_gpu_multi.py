@@ -77,3 +77,26 @@ def test_run_slices_host_envelope():
     # a sub-envelope [5, 12)
     r2, _ = run_slices_host(plan, cache, 5, 7, total=False)
     assert np.array_equal(bits(r2), bits(rows[5:12]))
+
+
+def test_multi_cfg2_on_distinct_gpus_bitwise():
+    """cfg2 (64 slices, every kernel family incl. the tensor-core ones) over the
+    distinct GPUs of the box: EXACT chained fold == the reference's run_scheme sum."""
+    from paper_2005_06787_b200 import MultiPlan
+    g = _gpus()
+    if g < 2:
+        pytest.skip("needs two GPUs")
+    try:
+        _, _, want, _, _ = read_ref("cfg2_grid5x6_m16", "single")
+    except FileNotFoundError:
+        pytest.skip("no reference values")
+    if want is None:
+        pytest.skip("no reference run_scheme sum recorded")
+    mp = MultiPlan(_desc("cfg2_grid5x6_m16", "single"), list(range(min(g, 4))), mode="exact")
+    got, _ = mp.run_scheme(deterministic=True)
+    assert np.array_equal(bits(got.ravel()), bits(want))
+    fast = MultiPlan(_desc("cfg2_grid5x6_m16", "single"), list(range(min(g, 4))), mode="fast")
+    f1, _ = fast.run_scheme(deterministic=True)
+    f2, _ = fast.run_scheme(deterministic=False)
+    assert np.abs(f1.ravel() - want).max() <= 1e-4 * np.abs(want).max()
+    assert np.abs(f2.ravel() - f1.ravel()).max() <= 1e-12 * np.abs(f1).max()
