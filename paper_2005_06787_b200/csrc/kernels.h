@@ -183,6 +183,41 @@ cudaError_t launch_absorb_lanes(const LaneTables *T, const LaneGeom &g, const Ba
 cudaError_t launch_absorb_direct(const DirectGeom &g, const BatchPtrs &p, bool exact,
                                  cudaStream_t stream);
 
+// Fused stem chain (kernels_chain.cu): consecutive bond-2 absorbs in one HBM pass,
+// a warp = 32 columns of the passive (never contracted) stem bits, a thread = the
+// active tile of its column (<= 2^kChainMaxLog complex values).
+constexpr int kChainMaxStages = 8;
+constexpr int kChainMaxLog = 4;
+constexpr int kChainMaxTab = 2 * kChainMaxStages * (1 << kChainMaxLog);  // rd + wr slots
+constexpr int kChainMaxW = kChainMaxStages * 256;
+struct ChainStage {
+  int lr, lk, ln;   // log2 of the stage's R (other active lines), K and N
+  int rd_off;       // tab offset: slot of input (r, k), [R][K]
+  int wr_off;       // tab offset: slot of output (r, n), [R][N]
+  int w_off;        // widx offset: W element of (k, n), [K][N]
+  int w_smem;       // offset of the stage's W in shared memory
+};
+struct ChainGeom {
+  int n_stages;
+  int li, lo;                       // log2 input / output elements per column
+  int64_t rows;                     // rows of 32 columns (per batch)
+  int w_total;                      // W elements of all stages
+  ChainStage st[kChainMaxStages];
+  const void *w[kChainMaxStages];   // filled at launch
+  int64_t w_bs[kChainMaxStages];
+};
+struct ChainTables {                // device memory, one per chain
+  int64_t xr[4][256], orow[4][256]; // X / O offsets of the row bytes
+  int64_t xl[32], ol[32];           // X / O offsets of the lane bits
+  int64_t xin[1 << kChainMaxLog];   // X offset of input element i (first stage's layout)
+  int64_t oout[1 << kChainMaxLog];  // O offset of output element j (last stage's layout)
+  uint8_t tab[kChainMaxTab];        // rd / wr slot tables of all stages
+  int32_t widx[kChainMaxW];         // W element offsets, [K][N] per stage
+};
+size_t chain_smem_bytes(const ChainGeom &g);
+cudaError_t launch_chain(const ChainTables *T, const ChainGeom &g, const BatchPtrs &p, bool exact,
+                         cudaStream_t stream);
+
 // Fused stem sweep: a chain of consecutive bond-2 absorbs S_{j+1} = S_j x W_j
 // executed tile by tile in shared memory. Only S_0 is read from and S_r written
 // to HBM; the intermediate stems never exist in memory. Every stage sums its K

@@ -357,6 +357,8 @@ struct stn_plan {
     stn::SweepGeom geom{};
     std::shared_ptr<DevBuf> tables;
     double io_bytes = 0;  // S_0 + S_r + W's per slice, in elements
+    bool chain = false;   // lane-column fused chain (kernels_chain.cu) instead of a tile sweep
+    stn::ChainGeom cgeom{};
   };
   std::vector<Sweep> sweeps;
   std::map<int, int> sweep_of_step;
@@ -1104,6 +1106,168 @@ bool sweep_candidate(const stn_plan &P, const StepPlan &sp) {
          sp.kbits.size() <= 6 && sp.nbits.size() <= 6;
 }
 
+bool chain_candidate(const stn_plan &P, const StepPlan &sp) {
+  return P.precision == STN_SINGLE && !sp.d.is_branch && sp.has_bits &&
+         (sp.kern == Kern::Absorb || sp.kern == Kern::AbsorbDirect || sp.kern == Kern::AbsorbTc ||
+          sp.kern == Kern::AbsorbTma || sp.kern == Kern::AbsorbMma || sp.kern == Kern::Lanes) &&
+         int(sp.kbits.size()) <= stn::kChainMaxLog && int(sp.nbits.size()) <= stn::kChainMaxLog;
+}
+
+// Fused stem chain over steps [steps] (kernels.h ChainGeom). Follows every bit
+// ("line") of the stem through the chain: X bits no stage contracts are passive
+// (they only move; the lowest five are the warp's lanes, the rest rows), the
+// others are active and live in a thread's tile (<= 2^kChainMaxLog values). Slot
+// layout at a stage boundary: element index over the alive active lines in list
+// order. Stage s reads [r][k] (k bit j = the step's K bit j, ascending X position:
+// the reference's k order) and writes [r][n] (n bit j = N bit j, ascending O
+// position). False when the chain does not fit or would not coalesce.
+bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Sweep *out) {
+  const int ns = int(steps.size());
+  if (ns < 2 || ns > stn::kChainMaxStages) return false;
+  const StepPlan &s0 = P.steps[steps[0]];
+  const int xr0 = s0.xr;
+  // line bookkeeping
+  std::vector<int> pos2line(static_cast<size_t>(xr0));
+  std::iota(pos2line.begin(), pos2line.end(), 0);
+  int n_lines = xr0;
+  std::vector<int> consumed_by(64, -1);  // line -> stage
+  struct StageLines {
+    std::vector<int> k, n;  // K lines (k bit order), N lines (n bit order)
+  };
+  std::vector<StageLines> sl(static_cast<size_t>(ns));
+  for (int si = 0; si < ns; ++si) {
+    const StepPlan &sp = P.steps[steps[si]];
+    if (int(pos2line.size()) != sp.xr) return false;
+    for (auto &[xp, wp] : sp.kbits) {
+      const int ln = pos2line[size_t(xp)];
+      sl[size_t(si)].k.push_back(ln);
+      consumed_by[size_t(ln)] = si;
+    }
+    std::vector<int> nxt(static_cast<size_t>(sp.orank_), -1);
+    for (auto &[xp, op] : sp.mbits) nxt[size_t(op)] = pos2line[size_t(xp)];
+    for (auto &[op, wp] : sp.nbits) {
+      if (n_lines >= 64) return false;
+      nxt[size_t(op)] = n_lines;
+      sl[size_t(si)].n.push_back(n_lines++);
+    }
+    for (int v : nxt)
+      if (v < 0) return false;
+    pos2line.swap(nxt);
+  }
+  const std::vector<int> &final_pos2line = pos2line;
+  std::vector<int> opos_of(static_cast<size_t>(n_lines), -1);
+  for (int op = 0; op < int(final_pos2line.size()); ++op) opos_of[size_t(final_pos2line[size_t(op)])] = op;
+  // input-active: X lines consumed in the chain (ascending X position)
+  std::vector<int> L;
+  std::vector<int> passive;  // X lines never consumed
+  for (int xp = 0; xp < xr0; ++xp) (consumed_by[size_t(xp)] >= 0 ? L : passive).push_back(xp);
+  const int li = int(L.size());
+  if (li > stn::kChainMaxLog || passive.size() < 5) return false;
+  for (int ln : passive)
+    if (opos_of[size_t(ln)] < 0) return false;
+  auto T = std::make_unique<stn::ChainTables>();
+  memset(T.get(), 0, sizeof(stn::ChainTables));
+  stn::ChainGeom g{};
+  g.n_stages = ns;
+  g.li = li;
+  for (int e = 0; e < (1 << li); ++e)
+    for (int i = 0; i < li; ++i)
+      if ((e >> i) & 1) T->xin[e] += int64_t(1) << L[size_t(i)];
+  int tab = 0, widx = 0, wsm = 0;
+  for (int si = 0; si < ns; ++si) {
+    const StepPlan &sp = P.steps[steps[si]];
+    const StageLines &st = sl[size_t(si)];
+    std::vector<int> R;
+    for (int ln : L)
+      if (std::find(st.k.begin(), st.k.end(), ln) == st.k.end()) R.push_back(ln);
+    const int lr = int(R.size()), lk = int(st.k.size()), ln_ = int(st.n.size());
+    if (lr + lk > stn::kChainMaxLog || lr + ln_ > stn::kChainMaxLog) return false;
+    if (int(R.size()) + lk != int(L.size())) return false;  // a K line not in the tile
+    auto slot_in = [&](int ln) {
+      return int(std::find(L.begin(), L.end(), ln) - L.begin());
+    };
+    stn::ChainStage &cs = g.st[si];
+    cs.lr = lr;
+    cs.lk = lk;
+    cs.ln = ln_;
+    cs.rd_off = tab;
+    for (int r = 0; r < (1 << lr); ++r)
+      for (int k = 0; k < (1 << lk); ++k) {
+        int e = 0;
+        for (int i = 0; i < lr; ++i)
+          if ((r >> i) & 1) e |= 1 << slot_in(R[size_t(i)]);
+        for (int j = 0; j < lk; ++j)
+          if ((k >> j) & 1) e |= 1 << slot_in(st.k[size_t(j)]);
+        T->tab[tab++] = uint8_t(e);
+      }
+    cs.wr_off = tab;
+    for (int r = 0; r < (1 << lr); ++r)
+      for (int n = 0; n < (1 << ln_); ++n) T->tab[tab++] = uint8_t(r | (n << lr));
+    cs.w_off = widx;
+    cs.w_smem = wsm;
+    for (int k = 0; k < (1 << lk); ++k)
+      for (int n = 0; n < (1 << ln_); ++n) {
+        int32_t off = 0;
+        for (int j = 0; j < lk; ++j)
+          if ((k >> j) & 1) off += int32_t(1) << sp.kbits[size_t(j)].second;
+        for (int j = 0; j < ln_; ++j)
+          if ((n >> j) & 1) off += int32_t(1) << sp.nbits[size_t(j)].second;
+        T->widx[widx++] = off;
+      }
+    wsm += 1 << (lk + ln_);
+    if (tab > stn::kChainMaxTab || widx > stn::kChainMaxW) return false;
+    // next layout: R lines, then the stage's N lines
+    L = R;
+    L.insert(L.end(), st.n.begin(), st.n.end());
+  }
+  g.lo = int(L.size());
+  for (int ln : L)
+    if (opos_of[size_t(ln)] < 0) return false;
+  for (int e = 0; e < (1 << g.lo); ++e)
+    for (int i = 0; i < g.lo; ++i)
+      if ((e >> i) & 1) T->oout[e] += int64_t(1) << opos_of[size_t(L[size_t(i)])];
+  g.w_total = wsm;
+  // passive lines: the 5 lowest X positions are the lanes, the rest the rows
+  const int rb = int(passive.size()) - 5;
+  if (rb > 32) return false;
+  for (int l = 0; l < 32; ++l)
+    for (int j = 0; j < 5; ++j)
+      if ((l >> j) & 1) {
+        T->xl[l] += int64_t(1) << passive[size_t(j)];
+        T->ol[l] += int64_t(1) << opos_of[size_t(passive[size_t(j)])];
+      }
+  for (int c = 0; c < 4; ++c)
+    for (int v = 0; v < 256; ++v)
+      for (int j = 0; j < 8; ++j)
+        if (((v >> j) & 1) && 8 * c + j < rb) {
+          const int ln = passive[size_t(5 + 8 * c + j)];
+          T->xr[c][v] += int64_t(1) << ln;
+          T->orow[c][v] += int64_t(1) << opos_of[size_t(ln)];
+        }
+  g.rows = int64_t(1) << rb;
+  // coalescing: 32-byte sectors one warp row touches, against the bytes it moves
+  auto efficiency = [&](const int64_t *lane_off, const int64_t *elem_off, int ne) {
+    std::set<int64_t> sectors;
+    for (int e = 0; e < ne; ++e)
+      for (int l = 0; l < 32; ++l) sectors.insert((lane_off[l] + elem_off[e]) >> 2);
+    return double(32 * ne) / (4.0 * double(sectors.size()));
+  };
+  if (efficiency(T->xl, T->xin, 1 << li) < 0.5 || efficiency(T->ol, T->oout, 1 << g.lo) < 0.5)
+    return false;
+  if (stn::chain_smem_bytes(g) > 100 * 1024) return false;
+  if (out) {
+    out->steps = steps;
+    out->chain = true;
+    out->cgeom = g;
+    out->tables = std::make_shared<DevBuf>();
+    out->tables->reserve(sizeof(stn::ChainTables));
+    cuda_check(cudaMemcpy(out->tables->ptr, T.get(), sizeof(stn::ChainTables),
+                          cudaMemcpyHostToDevice),
+               "chain tables");
+  }
+  return true;
+}
+
 // Tile-buffer swizzle of kernels_sweep.cu (linear over GF(2)).
 int sweep_phys(int l) { return l ^ (((l >> 4) ^ (l >> 8)) & 15); }
 
@@ -1314,6 +1478,65 @@ bool build_sweep(const stn_plan &P, const std::vector<int> &steps, int max_bits,
   return true;
 }
 
+// Fused stem chains (default): maximal runs of consecutive stem absorbs (a step's
+// output is the next step's stem operand) cut greedily into the longest segments
+// build_chain accepts; only segments whose intermediate stems are large enough to
+// matter are fused. STN_DEBUG chain=0 disables it; chain_min_bits=B (default 24):
+// fuse only when an intermediate stem has >= 2^B elements.
+void plan_chains(stn_plan &P) {
+  const char *opt = stn::debug_opt("chain");
+  if (opt && std::atoi(opt) == 0) return;
+  const char *mb = stn::debug_opt("chain_min_bits");
+  const int min_bits = mb ? std::atoi(mb) : 24;
+  const int n = int(P.steps.size());
+  std::vector<int> next(n, -1), has_prev(n, 0);
+  for (int i = 0; i < n; ++i) {
+    const StepPlan &sp = P.steps[i];
+    if (!chain_candidate(P, sp)) continue;
+    const int c = P.nodes[sp.d.node].consumer;
+    if (c < 0 || !chain_candidate(P, P.steps[c])) continue;
+    const StepPlan &cp = P.steps[c];
+    if ((cp.x_is_lhs ? cp.d.lhs : cp.d.rhs) != sp.d.node) continue;
+    next[i] = c;
+    has_prev[c] = 1;
+  }
+  for (int i = 0; i < n; ++i) {
+    if (has_prev[i] || next[i] < 0) continue;
+    std::vector<int> chain{i};
+    while (next[chain.back()] >= 0) chain.push_back(next[chain.back()]);
+    size_t a = 0;
+    while (a < chain.size()) {
+      size_t best = a;
+      for (size_t b = a + 1; b < chain.size(); ++b) {
+        std::vector<int> seg(chain.begin() + a, chain.begin() + b + 1);
+        if (build_chain(P, seg, nullptr))
+          best = b;
+        else
+          break;
+      }
+      if (best > a) {
+        std::vector<int> seg(chain.begin() + a, chain.begin() + best + 1);
+        int64_t largest_mid = 0;
+        for (size_t q = 0; q + 1 < seg.size(); ++q)
+          largest_mid = std::max<int64_t>(largest_mid, P.steps[seg[q]].osize);
+        stn_plan::Sweep sw;
+        if (largest_mid >= (int64_t(1) << min_bits) && build_chain(P, seg, &sw)) {
+          const int id = int(P.sweeps.size());
+          if (stn::debug_opt("sweep_debug")) {
+            fprintf(stderr, "chain %d: steps", id);
+            for (int q : seg) fprintf(stderr, " %d", q);
+            fprintf(stderr, " | li %d lo %d rows 2^%d\n", sw.cgeom.li, sw.cgeom.lo,
+                    __builtin_ctzll(uint64_t(sw.cgeom.rows)));
+          }
+          for (int st : seg) P.sweep_of_step[st] = id;
+          P.sweeps.push_back(std::move(sw));
+        }
+      }
+      a = best + 1;
+    }
+  }
+}
+
 void plan_sweeps(stn_plan &P) {
   P.sweeps.clear();
   P.sweep_of_step.clear();
@@ -1323,7 +1546,7 @@ void plan_sweeps(stn_plan &P) {
   // (e.g. 12) enables it; read per plan so tests can toggle it.
   const char *env_bits = stn::debug_opt("sweep_bits");
   const int max_bits = env_bits ? std::atoi(env_bits) : 0;
-  if (max_bits <= 0) return;
+  if (max_bits <= 0) return plan_chains(P);
   const int n = int(P.steps.size());
   std::vector<int> next(n, -1), has_prev(n, 0);
   for (int i = 0; i < n; ++i) {
@@ -2022,7 +2245,28 @@ Resolved resolve(stn_plan &P, const Ref &r, const stn_cache *cache, int nb) {
   return {nullptr, 0};
 }
 
+void launch_chain_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaStream_t st) {
+  const stn_plan::Sweep &sw = P.sweeps[op.sweep];
+  stn::ChainGeom g = sw.cgeom;
+  Resolved x = resolve(P, op.a, cache, nb), o = resolve(P, op.out, cache, nb);
+  double bytes = 8.0 * (x.bs ? nb : 1) * op.a.size + 8.0 * nb * op.out.size, flops = 0;
+  for (size_t j = 0; j < op.wrefs.size(); ++j) {
+    Resolved w = resolve(P, op.wrefs[j], cache, nb);
+    g.w[j] = w.ptr;
+    g.w_bs[j] = w.bs;
+    bytes += 8.0 * (w.bs ? nb : 1) * op.wrefs[j].size;
+  }
+  for (int stp : sw.steps) flops += 8.0 * double(P.steps[stp].d.mults) * nb;
+  ProfScope prof(P, st, sw.steps.front());
+  stn::BatchPtrs p{x.ptr, nullptr, const_cast<void *>(o.ptr), x.bs, 0, o.bs, nb};
+  cuda_check(stn::launch_chain(sw.tables->as<stn::ChainTables>(), g, p,
+                               P.mode == STN_MODE_EXACT, st),
+             "fused stem chain kernel");
+  prof.done(STN_KERNEL_SWEEP, bytes, flops);
+}
+
 void launch_sweep_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaStream_t st) {
+  if (P.sweeps[op.sweep].chain) return launch_chain_op(P, op, cache, nb, st);
   const stn_plan::Sweep &sw = P.sweeps[op.sweep];
   stn::SweepGeom g = sw.geom;
   Resolved x = resolve(P, op.a, cache, nb), o = resolve(P, op.out, cache, nb);
