@@ -32,22 +32,34 @@ namespace stn {
 namespace {
 using namespace dev;
 
-constexpr int kChThreads = 256;
+constexpr int kChThreads = 128;
 constexpr int kChWarps = kChThreads / 32;
 constexpr int kChTile = 1 << kChainMaxLog;  // slots per column
+constexpr int kChRing = 3;                  // rows of inputs in flight per warp (cp.async)
+constexpr int kChBufs = kChRing + 2;        // + two work buffers the stages ping-pong on
+constexpr int kChBuf = kChTile * 32;        // float2 per buffer: [slot][lane]
 
-__device__ __forceinline__ int64_t row_off(const int64_t (*t)[256], uint32_t r) {
-  return t[0][r & 255] + t[1][(r >> 8) & 255] + t[2][(r >> 16) & 255] + t[3][r >> 24];
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
 }
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 
 // One stage on one column: y[r][n] = sum_k x[r][k] w[k][n], r processed in chunks of
 // RC rows so the live registers stay at RC x (K + N) <= 16 complex values (a separate
 // function per shape: its registers do not add up with the other shapes').
 template <bool EXACT, int LR, int LK, int LN>
-__device__ __noinline__ void chain_stage(float2 *__restrict__ tile, int lane,
-                                            const uint8_t *__restrict__ rd,
-                                            const uint8_t *__restrict__ wr,
-                                            const float2 *__restrict__ w) {
+__device__ __noinline__ void chain_stage(const float2 *__restrict__ in, float2 *__restrict__ out,
+                                         int lane, const uint8_t *__restrict__ rd,
+                                         const uint8_t *__restrict__ wr,
+                                         const float2 *__restrict__ w) {
   constexpr int R = 1 << LR, K = 1 << LK, N = 1 << LN;
   // rows per chunk: RC (K + N) <= 16 complex values live
   constexpr int RCMAX = 16 / (K + N) > 0 ? 16 / (K + N) : 1;
@@ -56,7 +68,7 @@ __device__ __noinline__ void chain_stage(float2 *__restrict__ tile, int lane,
 #pragma unroll 1
   for (int r0 = 0; r0 < R; r0 += RC) {
 #pragma unroll
-    for (int i = 0; i < RC * K; ++i) x[i] = tile[rd[r0 * K + i] * 32 + lane];
+    for (int i = 0; i < RC * K; ++i) x[i] = in[rd[r0 * K + i] * 32 + lane];
 #pragma unroll
     for (int i = 0; i < RC * N; ++i) y[i] = make_float2(0.f, 0.f);
 #pragma unroll
@@ -68,17 +80,18 @@ __device__ __noinline__ void chain_stage(float2 *__restrict__ tile, int lane,
         for (int r = 0; r < RC; ++r) cmac<EXACT>(y[r * N + n], x[r * K + k], wv);
       }
 #pragma unroll
-    for (int i = 0; i < RC * N; ++i) tile[wr[r0 * N + i] * 32 + lane] = y[i];
+    for (int i = 0; i < RC * N; ++i) out[wr[r0 * N + i] * 32 + lane] = y[i];
   }
 }
 
 template <bool EXACT>
-__device__ __forceinline__ void run_stage(const ChainStage &st, float2 *tile, int lane,
-                                          const uint8_t *rd, const uint8_t *wr, const float2 *w) {
+__device__ __forceinline__ void run_stage(const ChainStage &st, const float2 *in, float2 *out,
+                                          int lane, const uint8_t *rd, const uint8_t *wr,
+                                          const float2 *w) {
   // every (log R, log K, log N) with R K <= 16 and R N <= 16 (kChainMaxLog = 4)
 #define STN_CH(a, b, c)                                                          \
   if (st.lr == a && st.lk == b && st.ln == c) {                                  \
-    chain_stage<EXACT, a, b, c>(tile, lane, rd, wr, w);                          \
+    chain_stage<EXACT, a, b, c>(in, out, lane, rd, wr, w);                       \
     return;                                                                      \
   }
   STN_CH(0, 0, 0) STN_CH(0, 0, 1) STN_CH(0, 0, 2) STN_CH(0, 0, 3) STN_CH(0, 0, 4)
@@ -95,25 +108,24 @@ __device__ __forceinline__ void run_stage(const ChainStage &st, float2 *tile, in
 #undef STN_CH
 }
 
+// The grid is persistent over rows; warp w of the grid takes rows w, w + W, ...
+// Each warp keeps kChRing rows of inputs in flight with cp.async straight into
+// shared memory (no registers held), so the HBM stream continues while a row's
+// stages run; a lane only ever touches its own column, so no warp barrier is
+// needed between the copies, the stages and the stores.
 template <bool EXACT>
-__global__ void __launch_bounds__(kChThreads, 3)
+__global__ void __launch_bounds__(kChThreads, 2)
     k_chain(const ChainTables *__restrict__ T, const __grid_constant__ ChainGeom g,
             const BatchPtrs p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  int64_t(*sxr)[256] = reinterpret_cast<int64_t(*)[256]>(smem_raw);
-  int64_t(*sor)[256] = sxr + 4;
-  int64_t *sxin = reinterpret_cast<int64_t *>(sor + 4);  // [kChTile]
-  int64_t *sout = sxin + kChTile;                        // [kChTile]
-  uint8_t *stab = reinterpret_cast<uint8_t *>(sout + kChTile);  // rd / wr tables
+  int64_t *sxin = reinterpret_cast<int64_t *>(smem_raw);  // [kChTile]
+  int64_t *sout = sxin + kChTile;                          // [kChTile]
+  uint8_t *stab = reinterpret_cast<uint8_t *>(sout + kChTile);   // rd / wr tables
   float2 *sw = reinterpret_cast<float2 *>(stab + kChainMaxTab);  // W of all stages
-  float2 *tiles = sw + g.w_total;                                 // [warp][slot][lane]
+  float2 *bufs = sw + ((g.w_total + 1) & ~1);                   // [warp][kChBufs][slot][lane]
   const int b = blockIdx.y;
   const float2 *X = static_cast<const float2 *>(p.a) + int64_t(b) * p.a_bs;
   float2 *O = static_cast<float2 *>(p.out) + int64_t(b) * p.out_bs;
-  for (int i = threadIdx.x; i < 1024; i += kChThreads) {
-    sxr[i >> 8][i & 255] = T->xr[i >> 8][i & 255];
-    sor[i >> 8][i & 255] = T->orow[i >> 8][i & 255];
-  }
   for (int i = threadIdx.x; i < kChTile; i += kChThreads) {
     sxin[i] = T->xin[i];
     sout[i] = T->oout[i];
@@ -128,42 +140,62 @@ __global__ void __launch_bounds__(kChThreads, 3)
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t xl = T->xl[lane], ol = T->ol[lane];
-  float2 *tile = tiles + warp * kChTile * 32;
+  float2 *wb = bufs + int64_t(warp) * kChBufs * kChBuf;
+  float2 *ring = wb, *work0 = wb + kChRing * kChBuf, *work1 = work0 + kChBuf;
   const int ni = 1 << g.li, no = 1 << g.lo;
-  const int64_t warps = int64_t(gridDim.x) * kChWarps;
-  for (int64_t row = int64_t(blockIdx.x) * kChWarps + warp; row < g.rows; row += warps) {
-    const int64_t bx = row_off(sxr, uint32_t(row)) + xl;
-    const int64_t bo = row_off(sor, uint32_t(row)) + ol;
-    {  // every input of the column in flight before any is stored
-      float2 v[kChTile];
-#pragma unroll
-      for (int i = 0; i < kChTile; ++i)
-        if (i < ni) v[i] = __ldcs(X + bx + sxin[i]);
-#pragma unroll
-      for (int i = 0; i < kChTile; ++i)
-        if (i < ni) tile[i * 32 + lane] = v[i];
+  const int64_t step = int64_t(gridDim.x) * kChWarps;
+  const int64_t row0 = int64_t(blockIdx.x) * kChWarps + warp;
+  // row -> X / O offsets through the per-byte tables (global, L1-resident)
+  auto row_x = [&](int64_t row) {
+    const uint32_t r = uint32_t(row);
+    return __ldg(&T->xr[0][r & 255]) + __ldg(&T->xr[1][(r >> 8) & 255]) +
+           __ldg(&T->xr[2][(r >> 16) & 255]) + __ldg(&T->xr[3][r >> 24]);
+  };
+  auto row_o = [&](int64_t row) {
+    const uint32_t r = uint32_t(row);
+    return __ldg(&T->orow[0][r & 255]) + __ldg(&T->orow[1][(r >> 8) & 255]) +
+           __ldg(&T->orow[2][(r >> 16) & 255]) + __ldg(&T->orow[3][r >> 24]);
+  };
+  auto issue = [&](int64_t row, float2 *dst) {
+    if (row < g.rows) {
+      const float2 *src = X + row_x(row) + xl;
+      for (int i = 0; i < ni; ++i) cp_async8(dst + i * 32 + lane, src + sxin[i]);
     }
+    cp_commit();  // one group per ring slot, empty past the end
+  };
+#pragma unroll
+  for (int q = 0; q < kChRing; ++q) issue(row0 + q * step, ring + q * kChBuf);
+  int slot = 0;
+  for (int64_t row = row0; row < g.rows; row += step) {
+    cp_wait<kChRing - 1>();  // this row's inputs have landed (own column only)
+    const float2 *cur = ring + slot * kChBuf;
+    float2 *dst = work0;
     for (int s = 0; s < g.n_stages; ++s) {
       const ChainStage &st = g.st[s];
-      run_stage<EXACT>(st, tile, lane, stab + st.rd_off, stab + st.wr_off, sw + st.w_smem);
+      run_stage<EXACT>(st, cur, dst, lane, stab + st.rd_off, stab + st.wr_off, sw + st.w_smem);
+      if (s == 0)  // the ring slot is consumed: refill it with the row kChRing steps ahead
+        issue(row + kChRing * step, ring + slot * kChBuf);
+      cur = dst;
+      dst = dst == work0 ? work1 : work0;
     }
-    {
-      float2 v[kChTile];
+    const int64_t bo = row_o(row) + ol;
+    float2 v[kChTile];
 #pragma unroll
-      for (int i = 0; i < kChTile; ++i)
-        if (i < no) v[i] = tile[i * 32 + lane];
+    for (int i = 0; i < kChTile; ++i)
+      if (i < no) v[i] = cur[i * 32 + lane];
 #pragma unroll
-      for (int i = 0; i < kChTile; ++i)
-        if (i < no) __stcs(O + bo + sout[i], v[i]);
-    }
+    for (int i = 0; i < kChTile; ++i)
+      if (i < no) __stcs(O + bo + sout[i], v[i]);
+    slot = slot + 1 == kChRing ? 0 : slot + 1;
   }
+  cp_wait<0>();
 }
 
 }  // namespace
 
 size_t chain_smem_bytes(const ChainGeom &g) {
-  return 8 * 2 * 1024 + 8 * 2 * kChTile + kChainMaxTab + 8 * size_t(g.w_total) +
-         size_t(kChWarps) * kChTile * 32 * 8;
+  return 8 * 2 * kChTile + kChainMaxTab + 8 * size_t((g.w_total + 1) & ~1) +
+         size_t(kChWarps) * kChBufs * kChBuf * 8;
 }
 
 cudaError_t launch_chain(const ChainTables *T, const ChainGeom &g, const BatchPtrs &p, bool exact,
@@ -180,8 +212,13 @@ cudaError_t launch_chain(const ChainTables *T, const ChainGeom &g, const BatchPt
     set = true;
   }
   if (smem > 110 * 1024) return cudaErrorNotSupported;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kChThreads, smem) !=
+          cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
   const int64_t want = (g.rows + kChWarps * 4 - 1) / (kChWarps * 4);
-  const int64_t cap = std::max<int64_t>(1, 148 * 3 / std::max(1, p.nbatch));
+  const int64_t cap = std::max<int64_t>(1, 148 * per_sm / std::max(1, p.nbatch));
   dim3 grid(unsigned(std::max<int64_t>(1, std::min(want, cap))), unsigned(p.nbatch));
   kern<<<grid, kChThreads, smem, stream>>>(T, g, p);
   return cudaGetLastError();
