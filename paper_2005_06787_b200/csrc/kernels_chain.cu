@@ -56,7 +56,7 @@ __device__ __forceinline__ void cp_wait() {
 // RC rows so the live registers stay at RC x (K + N) <= 16 complex values (a separate
 // function per shape: its registers do not add up with the other shapes').
 template <bool EXACT, int LR, int LK, int LN>
-__device__ __noinline__ void chain_stage(const float2 *__restrict__ in, float2 *__restrict__ out,
+__device__ __forceinline__ void chain_stage(const float2 *__restrict__ in, float2 *__restrict__ out,
                                          int lane, const uint8_t *__restrict__ rd,
                                          const uint8_t *__restrict__ wr,
                                          const float2 *__restrict__ w) {
@@ -89,23 +89,26 @@ __device__ __forceinline__ void run_stage(const ChainStage &st, const float2 *in
                                           int lane, const uint8_t *rd, const uint8_t *wr,
                                           const float2 *w) {
   // every (log R, log K, log N) with R K <= 16 and R N <= 16 (kChainMaxLog = 4)
-#define STN_CH(a, b, c)                                                          \
-  if (st.lr == a && st.lk == b && st.ln == c) {                                  \
-    chain_stage<EXACT, a, b, c>(in, out, lane, rd, wr, w);                       \
-    return;                                                                      \
-  }
-  STN_CH(0, 0, 0) STN_CH(0, 0, 1) STN_CH(0, 0, 2) STN_CH(0, 0, 3) STN_CH(0, 0, 4)
-  STN_CH(0, 1, 0) STN_CH(0, 1, 1) STN_CH(0, 1, 2) STN_CH(0, 1, 3) STN_CH(0, 1, 4)
-  STN_CH(0, 2, 0) STN_CH(0, 2, 1) STN_CH(0, 2, 2) STN_CH(0, 2, 3) STN_CH(0, 2, 4)
-  STN_CH(0, 3, 0) STN_CH(0, 3, 1) STN_CH(0, 3, 2) STN_CH(0, 3, 3) STN_CH(0, 3, 4)
-  STN_CH(0, 4, 0) STN_CH(0, 4, 1) STN_CH(0, 4, 2) STN_CH(0, 4, 3) STN_CH(0, 4, 4)
-  STN_CH(1, 0, 0) STN_CH(1, 0, 1) STN_CH(1, 0, 2) STN_CH(1, 0, 3) STN_CH(1, 1, 0)
-  STN_CH(1, 1, 1) STN_CH(1, 1, 2) STN_CH(1, 1, 3) STN_CH(1, 2, 0) STN_CH(1, 2, 1)
-  STN_CH(1, 2, 2) STN_CH(1, 2, 3) STN_CH(1, 3, 0) STN_CH(1, 3, 1) STN_CH(1, 3, 2)
-  STN_CH(1, 3, 3) STN_CH(2, 0, 0) STN_CH(2, 0, 1) STN_CH(2, 0, 2) STN_CH(2, 1, 0)
-  STN_CH(2, 1, 1) STN_CH(2, 1, 2) STN_CH(2, 2, 0) STN_CH(2, 2, 1) STN_CH(2, 2, 2)
-  STN_CH(3, 0, 0) STN_CH(3, 0, 1) STN_CH(3, 1, 0) STN_CH(3, 1, 1) STN_CH(4, 0, 0)
+  switch ((st.lr * 5 + st.lk) * 5 + st.ln) {  // one jump-table branch per stage
+#define STN_CH(a, b, c)                                       \
+  case (a * 5 + b) * 5 + c:                                   \
+    chain_stage<EXACT, a, b, c>(in, out, lane, rd, wr, w);    \
+    return;
+    STN_CH(0, 0, 0) STN_CH(0, 0, 1) STN_CH(0, 0, 2) STN_CH(0, 0, 3) STN_CH(0, 0, 4)
+    STN_CH(0, 1, 0) STN_CH(0, 1, 1) STN_CH(0, 1, 2) STN_CH(0, 1, 3) STN_CH(0, 1, 4)
+    STN_CH(0, 2, 0) STN_CH(0, 2, 1) STN_CH(0, 2, 2) STN_CH(0, 2, 3) STN_CH(0, 2, 4)
+    STN_CH(0, 3, 0) STN_CH(0, 3, 1) STN_CH(0, 3, 2) STN_CH(0, 3, 3) STN_CH(0, 3, 4)
+    STN_CH(0, 4, 0) STN_CH(0, 4, 1) STN_CH(0, 4, 2) STN_CH(0, 4, 3) STN_CH(0, 4, 4)
+    STN_CH(1, 0, 0) STN_CH(1, 0, 1) STN_CH(1, 0, 2) STN_CH(1, 0, 3) STN_CH(1, 1, 0)
+    STN_CH(1, 1, 1) STN_CH(1, 1, 2) STN_CH(1, 1, 3) STN_CH(1, 2, 0) STN_CH(1, 2, 1)
+    STN_CH(1, 2, 2) STN_CH(1, 2, 3) STN_CH(1, 3, 0) STN_CH(1, 3, 1) STN_CH(1, 3, 2)
+    STN_CH(1, 3, 3) STN_CH(2, 0, 0) STN_CH(2, 0, 1) STN_CH(2, 0, 2) STN_CH(2, 1, 0)
+    STN_CH(2, 1, 1) STN_CH(2, 1, 2) STN_CH(2, 2, 0) STN_CH(2, 2, 1) STN_CH(2, 2, 2)
+    STN_CH(3, 0, 0) STN_CH(3, 0, 1) STN_CH(3, 1, 0) STN_CH(3, 1, 1) STN_CH(4, 0, 0)
 #undef STN_CH
+    default:
+      return;
+  }
 }
 
 // The grid is persistent over rows; warp w of the grid takes rows w, w + W, ...
