@@ -200,6 +200,7 @@ struct ChainStage {
 struct ChainGeom {
   int n_stages;
   int li, lo;                       // log2 input / output elements per column
+  int ma;                           // log2 of the largest tile (slots per column)
   int64_t rows;                     // rows of 32 columns (per batch)
   int w_total;                      // W elements of all stages
   ChainStage st[kChainMaxStages];

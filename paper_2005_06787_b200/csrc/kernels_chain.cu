@@ -37,7 +37,7 @@ constexpr int kChWarps = kChThreads / 32;
 constexpr int kChTile = 1 << kChainMaxLog;  // slots per column
 constexpr int kChRing = 3;                  // rows of inputs in flight per warp (cp.async)
 constexpr int kChBufs = kChRing + 2;        // + two work buffers the stages ping-pong on
-constexpr int kChBuf = kChTile * 32;        // float2 per buffer: [slot][lane]
+// a buffer is [slot][lane], 2^ma slots: the chain's largest tile (g.ma <= kChainMaxLog)
 
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
@@ -88,23 +88,22 @@ template <bool EXACT>
 __device__ __forceinline__ void run_stage(const ChainStage &st, const float2 *in, float2 *out,
                                           int lane, const uint8_t *rd, const uint8_t *wr,
                                           const float2 *w) {
-  // every (log R, log K, log N) with R K <= 16 and R N <= 16 (kChainMaxLog = 4)
+  // every (log R, log K, log N) with R K <= 16, R N <= 16 (kChainMaxLog = 4), K, N <= 8
   switch ((st.lr * 5 + st.lk) * 5 + st.ln) {  // one jump-table branch per stage
 #define STN_CH(a, b, c)                                       \
   case (a * 5 + b) * 5 + c:                                   \
     chain_stage<EXACT, a, b, c>(in, out, lane, rd, wr, w);    \
     return;
-    STN_CH(0, 0, 0) STN_CH(0, 0, 1) STN_CH(0, 0, 2) STN_CH(0, 0, 3) STN_CH(0, 0, 4)
-    STN_CH(0, 1, 0) STN_CH(0, 1, 1) STN_CH(0, 1, 2) STN_CH(0, 1, 3) STN_CH(0, 1, 4)
-    STN_CH(0, 2, 0) STN_CH(0, 2, 1) STN_CH(0, 2, 2) STN_CH(0, 2, 3) STN_CH(0, 2, 4)
-    STN_CH(0, 3, 0) STN_CH(0, 3, 1) STN_CH(0, 3, 2) STN_CH(0, 3, 3) STN_CH(0, 3, 4)
-    STN_CH(0, 4, 0) STN_CH(0, 4, 1) STN_CH(0, 4, 2) STN_CH(0, 4, 3) STN_CH(0, 4, 4)
-    STN_CH(1, 0, 0) STN_CH(1, 0, 1) STN_CH(1, 0, 2) STN_CH(1, 0, 3) STN_CH(1, 1, 0)
-    STN_CH(1, 1, 1) STN_CH(1, 1, 2) STN_CH(1, 1, 3) STN_CH(1, 2, 0) STN_CH(1, 2, 1)
-    STN_CH(1, 2, 2) STN_CH(1, 2, 3) STN_CH(1, 3, 0) STN_CH(1, 3, 1) STN_CH(1, 3, 2)
-    STN_CH(1, 3, 3) STN_CH(2, 0, 0) STN_CH(2, 0, 1) STN_CH(2, 0, 2) STN_CH(2, 1, 0)
-    STN_CH(2, 1, 1) STN_CH(2, 1, 2) STN_CH(2, 2, 0) STN_CH(2, 2, 1) STN_CH(2, 2, 2)
-    STN_CH(3, 0, 0) STN_CH(3, 0, 1) STN_CH(3, 1, 0) STN_CH(3, 1, 1) STN_CH(4, 0, 0)
+    STN_CH(0, 0, 0) STN_CH(0, 0, 1) STN_CH(0, 0, 2) STN_CH(0, 0, 3) STN_CH(0, 1, 0)
+    STN_CH(0, 1, 1) STN_CH(0, 1, 2) STN_CH(0, 1, 3) STN_CH(0, 2, 0) STN_CH(0, 2, 1)
+    STN_CH(0, 2, 2) STN_CH(0, 2, 3) STN_CH(0, 3, 0) STN_CH(0, 3, 1) STN_CH(0, 3, 2)
+    STN_CH(0, 3, 3) STN_CH(1, 0, 0) STN_CH(1, 0, 1) STN_CH(1, 0, 2) STN_CH(1, 0, 3)
+    STN_CH(1, 1, 0) STN_CH(1, 1, 1) STN_CH(1, 1, 2) STN_CH(1, 1, 3) STN_CH(1, 2, 0)
+    STN_CH(1, 2, 1) STN_CH(1, 2, 2) STN_CH(1, 2, 3) STN_CH(1, 3, 0) STN_CH(1, 3, 1)
+    STN_CH(1, 3, 2) STN_CH(1, 3, 3) STN_CH(2, 0, 0) STN_CH(2, 0, 1) STN_CH(2, 0, 2)
+    STN_CH(2, 1, 0) STN_CH(2, 1, 1) STN_CH(2, 1, 2) STN_CH(2, 2, 0) STN_CH(2, 2, 1)
+    STN_CH(2, 2, 2) STN_CH(3, 0, 0) STN_CH(3, 0, 1) STN_CH(3, 1, 0) STN_CH(3, 1, 1)
+    STN_CH(4, 0, 0)
 #undef STN_CH
     default:
       return;
@@ -117,7 +116,7 @@ __device__ __forceinline__ void run_stage(const ChainStage &st, const float2 *in
 // stages run; a lane only ever touches its own column, so no warp barrier is
 // needed between the copies, the stages and the stores.
 template <bool EXACT>
-__global__ void __launch_bounds__(kChThreads, 2)
+__global__ void __launch_bounds__(kChThreads, 4)
     k_chain(const ChainTables *__restrict__ T, const __grid_constant__ ChainGeom g,
             const BatchPtrs p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -143,6 +142,7 @@ __global__ void __launch_bounds__(kChThreads, 2)
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t xl = T->xl[lane], ol = T->ol[lane];
+  const int kChBuf = 32 << g.ma;  // float2 per buffer
   float2 *wb = bufs + int64_t(warp) * kChBufs * kChBuf;
   float2 *ring = wb, *work0 = wb + kChRing * kChBuf, *work1 = work0 + kChBuf;
   const int ni = 1 << g.li, no = 1 << g.lo;
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kChThreads, 2)
 
 size_t chain_smem_bytes(const ChainGeom &g) {
   return 8 * 2 * kChTile + kChainMaxTab + 8 * size_t((g.w_total + 1) & ~1) +
-         size_t(kChWarps) * kChBufs * kChBuf * 8;
+         size_t(kChWarps) * kChBufs * (size_t(32) << g.ma) * 8;
 }
 
 cudaError_t launch_chain(const ChainTables *T, const ChainGeom &g, const BatchPtrs &p, bool exact,

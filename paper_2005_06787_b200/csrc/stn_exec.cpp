@@ -1161,8 +1161,24 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
   std::vector<int> L;
   std::vector<int> passive;  // X lines never consumed
   for (int xp = 0; xp < xr0; ++xp) (consumed_by[size_t(xp)] >= 0 ? L : passive).push_back(xp);
+  if (int(L.size()) > stn::kChainMaxLog || passive.size() < 5) return false;
+  // largest tile along the chain (alive active lines at a stage's input or output)
+  int ma = int(L.size());
+  {
+    int alive = int(L.size());
+    for (int si = 0; si < ns; ++si) {
+      const int a_out = alive - int(sl[size_t(si)].k.size()) + int(sl[size_t(si)].n.size());
+      ma = std::max(ma, std::max(alive, a_out));
+      alive = a_out;
+    }
+  }
+  // small tiles carry a fixed per-row cost (table lookups, the stage dispatch): the
+  // passive lines right above the lanes ride along in the tile as lines no stage
+  // touches, so a column holds 2^kChainMaxLog values and there are fewer rows
+  const int extra = std::max(0, std::min(stn::kChainMaxLog - ma, int(passive.size()) - 5));
+  for (int q = 0; q < extra; ++q) L.push_back(passive[size_t(5 + q)]);
+  passive.erase(passive.begin() + 5, passive.begin() + 5 + extra);
   const int li = int(L.size());
-  if (li > stn::kChainMaxLog || passive.size() < 5) return false;
   for (int ln : passive)
     if (opos_of[size_t(ln)] < 0) return false;
   auto T = std::make_unique<stn::ChainTables>();
@@ -1182,6 +1198,8 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
       if (std::find(st.k.begin(), st.k.end(), ln) == st.k.end()) R.push_back(ln);
     const int lr = int(R.size()), lk = int(st.k.size()), ln_ = int(st.n.size());
     if (lr + lk > stn::kChainMaxLog || lr + ln_ > stn::kChainMaxLog) return false;
+    if (lk > 3 || ln_ > 3) return false;  // stage shapes the kernel instantiates: K, N <= 8
+    g.ma = std::max(g.ma, std::max(lr + lk, lr + ln_));
     if (int(R.size()) + lk != int(L.size())) return false;  // a K line not in the tile
     auto slot_in = [&](int ln) {
       return int(std::find(L.begin(), L.end(), ln) - L.begin());

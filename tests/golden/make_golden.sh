@@ -25,6 +25,11 @@ circuit() {  # name layout cycles open target_cw golden-slices scheme-sum precis
   done
 }
 
+slice0() {  # name precision: the reference's run_subtask on slice 0 only (15-90 CPU-minutes
+            # per 53-qubit slice), no uncached rerun
+  "$TOOL" golden "$HERE/$1" --precision "$2" --slices 0 --scheme 0 --uncached 0 --threads 1 > /dev/null
+}
+
 random_net() {  # name seed vertices extra open hyper mixed target_cw merge
   local name=$1; local d="$HERE/$name"; mkdir -p "$d"
   "$TOOL" gen-random "$d" --seed "$2" --vertices "$3" --extra "$4" --open "$5" --hyper "$6" \
@@ -49,7 +54,16 @@ circuit rt_grid3x4_m8_sliced grid3x4 8 6 6 all 1 single double
 
 # BASELINE.json configs (cfg1..cfg5). Planner: PlannerParams defaults, seed 1.
 circuit cfg1_grid4x5_m14 grid4x5 14 0 16 all 1 single double
-circuit cfg2_grid5x6_m16 grid5x6 16 6 28 sample:3 0 single
+# cfg2: three sampled slices plus the run_scheme sum over all 64 (~1 CPU-hour per precision)
+circuit cfg2_grid5x6_m16 grid5x6 16 6 28 sample:3 1 single double
 circuit cfg3_syc53_m12   sycamore53 12 6 29 none 0
 circuit cfg4_syc53_m14   sycamore53 14 6 29 none 0
 circuit cfg5_syc53_m20   sycamore53 20 6 33 none 0
+# 53-qubit slices: slice 0 through the reference executor itself
+slice0 cfg3_syc53_m12 single
+slice0 cfg3_syc53_m12 double
+slice0 cfg4_syc53_m14 single
+# cfg5: the reference cannot hold its 2^33 stems (Engine::gemm keeps 4 of them, 256 GiB)
+# and refuses every assignment (subtasks() overflows, scheme.hpp:33-37); its slices 0
+# and 1 come from the oracle port on a GPU box host: scripts/cfg5_parity.py ->
+# port_single.bin (tests/test_gpu_parity.py::test_cfg5_2pow33_stems_against_the_oracle_port)

@@ -109,7 +109,9 @@ def test_fast_mode_within_tolerance(name):
     if s is not None:
         total, _ = run_scheme(plan, 1)
         _, _, ds, _, _ = read_ref(name, "double")
-        assert rel_err(total, ds) <= max(RTOL, 2 * rel_err(s, ds))
+        if ds is not None:  # the reference double run_scheme sum, when recorded
+            assert rel_err(total, ds) <= max(RTOL, 2 * rel_err(s, ds))
+        assert rel_err(total, s) <= 2 * E_REF_MAX  # and the reference single sum
 
 
 @pytest.mark.parametrize("name", ["rt_grid3x4_m8_sliced", "cfg1_grid4x5_m14"])
