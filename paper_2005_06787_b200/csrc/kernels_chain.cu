@@ -116,11 +116,13 @@ __device__ __forceinline__ void run_stage(const ChainStage &st, const float2 *in
 // stages run; a lane only ever touches its own column, so no warp barrier is
 // needed between the copies, the stages and the stores.
 template <bool EXACT>
-__global__ void __launch_bounds__(kChThreads, 4)
+__global__ void __launch_bounds__(kChThreads, 2)
     k_chain(const ChainTables *__restrict__ T, const __grid_constant__ ChainGeom g,
             const BatchPtrs p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  int64_t *sxin = reinterpret_cast<int64_t *>(smem_raw);  // [kChTile]
+  int64_t(*sxr)[256] = reinterpret_cast<int64_t(*)[256]>(smem_raw);  // row byte tables
+  int64_t(*sor)[256] = sxr + 4;
+  int64_t *sxin = reinterpret_cast<int64_t *>(sor + 4);  // [kChTile]
   int64_t *sout = sxin + kChTile;                          // [kChTile]
   uint8_t *stab = reinterpret_cast<uint8_t *>(sout + kChTile);   // rd / wr tables
   float2 *sw = reinterpret_cast<float2 *>(stab + kChainMaxTab);  // W of all stages
@@ -128,6 +130,10 @@ __global__ void __launch_bounds__(kChThreads, 4)
   const int b = blockIdx.y;
   const float2 *X = static_cast<const float2 *>(p.a) + int64_t(b) * p.a_bs;
   float2 *O = static_cast<float2 *>(p.out) + int64_t(b) * p.out_bs;
+  for (int i = threadIdx.x; i < 1024; i += kChThreads) {
+    sxr[i >> 8][i & 255] = T->xr[i >> 8][i & 255];
+    sor[i >> 8][i & 255] = T->orow[i >> 8][i & 255];
+  }
   for (int i = threadIdx.x; i < kChTile; i += kChThreads) {
     sxin[i] = T->xin[i];
     sout[i] = T->oout[i];
@@ -148,16 +154,14 @@ __global__ void __launch_bounds__(kChThreads, 4)
   const int ni = 1 << g.li, no = 1 << g.lo;
   const int64_t step = int64_t(gridDim.x) * kChWarps;
   const int64_t row0 = int64_t(blockIdx.x) * kChWarps + warp;
-  // row -> X / O offsets through the per-byte tables (global, L1-resident)
+  // row -> X / O offsets through the per-byte tables
   auto row_x = [&](int64_t row) {
     const uint32_t r = uint32_t(row);
-    return __ldg(&T->xr[0][r & 255]) + __ldg(&T->xr[1][(r >> 8) & 255]) +
-           __ldg(&T->xr[2][(r >> 16) & 255]) + __ldg(&T->xr[3][r >> 24]);
+    return sxr[0][r & 255] + sxr[1][(r >> 8) & 255] + sxr[2][(r >> 16) & 255] + sxr[3][r >> 24];
   };
   auto row_o = [&](int64_t row) {
     const uint32_t r = uint32_t(row);
-    return __ldg(&T->orow[0][r & 255]) + __ldg(&T->orow[1][(r >> 8) & 255]) +
-           __ldg(&T->orow[2][(r >> 16) & 255]) + __ldg(&T->orow[3][r >> 24]);
+    return sor[0][r & 255] + sor[1][(r >> 8) & 255] + sor[2][(r >> 16) & 255] + sor[3][r >> 24];
   };
   auto issue = [&](int64_t row, float2 *dst) {
     if (row < g.rows) {
@@ -197,7 +201,7 @@ __global__ void __launch_bounds__(kChThreads, 4)
 }  // namespace
 
 size_t chain_smem_bytes(const ChainGeom &g) {
-  return 8 * 2 * kChTile + kChainMaxTab + 8 * size_t((g.w_total + 1) & ~1) +
+  return 8 * 2 * 1024 + 8 * 2 * kChTile + kChainMaxTab + 8 * size_t((g.w_total + 1) & ~1) +
          size_t(kChWarps) * kChBufs * (size_t(32) << g.ma) * 8;
 }
 
