@@ -55,79 +55,39 @@ __device__ __forceinline__ void cp_wait() {
 // One stage on one column: y[r][n] = sum_k x[r][k] w[k][n], r processed in chunks of
 // RC rows so the live registers stay at RC x (K + N) <= 16 complex values (a separate
 // function per shape: its registers do not add up with the other shapes').
-// Blackwell packed FP32 FMA (FFMA2): acc += x * w on both lanes of a 64-bit pair.
-__device__ __forceinline__ void ffma2(unsigned long long &acc, const unsigned long long x,
-                                      const unsigned long long w) {
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(x), "l"(w));
-}
-
-// One stage on one column: y[r][n] = sum_k x[r][k] w[k][n], k ascending, r processed in
-// chunks of RC rows so few registers are live. EXACT: separately rounded products and
-// sums (bitwise the reference's crow[n] += amk * brow[n]). FAST: with x = (re, im) as
-// stored and W staged as ((wr, wr), (wi, -wi)), U += x (wr, wr) and V += x (wi, -wi)
-// are two FFMA2 per complex multiply-add; re = U.x + V.y, im = U.y + V.x.
 template <bool EXACT, int LR, int LK, int LN>
 __device__ __forceinline__ void chain_stage(const float2 *__restrict__ in, float2 *__restrict__ out,
                                          int lane, const uint8_t *__restrict__ rd,
                                          const uint8_t *__restrict__ wr,
-                                         const void *__restrict__ wsm) {
+                                         const float2 *__restrict__ w) {
   constexpr int R = 1 << LR, K = 1 << LK, N = 1 << LN;
-  constexpr int LIVE = EXACT ? K + N : K + 2 * N;  // complex-sized values per row
-  constexpr int RCMAX = 16 / LIVE > 0 ? 16 / LIVE : 1;
+  // rows per chunk: RC (K + N) <= 16 complex values live
+  constexpr int RCMAX = 16 / (K + N) > 0 ? 16 / (K + N) : 1;
   constexpr int RC = RCMAX >= R ? R : (RCMAX >= 8 ? 8 : (RCMAX >= 4 ? 4 : (RCMAX >= 2 ? 2 : 1)));
+  float2 x[RC * K], y[RC * N];
 #pragma unroll 1
   for (int r0 = 0; r0 < R; r0 += RC) {
-    if constexpr (EXACT) {
-      const float2 *w = static_cast<const float2 *>(wsm);
-      float2 x[RC * K], y[RC * N];
 #pragma unroll
-      for (int i = 0; i < RC * K; ++i) x[i] = in[rd[r0 * K + i] * 32 + lane];
+    for (int i = 0; i < RC * K; ++i) x[i] = in[rd[r0 * K + i] * 32 + lane];
 #pragma unroll
-      for (int i = 0; i < RC * N; ++i) y[i] = make_float2(0.f, 0.f);
+    for (int i = 0; i < RC * N; ++i) y[i] = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int n = 0; n < N; ++n)
+    for (int n = 0; n < N; ++n)
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const float2 wv = w[k * N + n];
+      for (int k = 0; k < K; ++k) {
+        const float2 wv = w[k * N + n];
 #pragma unroll
-          for (int r = 0; r < RC; ++r) cmac<true>(y[r * N + n], x[r * K + k], wv);
-        }
-#pragma unroll
-      for (int i = 0; i < RC * N; ++i) out[wr[r0 * N + i] * 32 + lane] = y[i];
-    } else {
-      const ulonglong2 *wq = static_cast<const ulonglong2 *>(wsm);
-      const unsigned long long *in64 = reinterpret_cast<const unsigned long long *>(in);
-      unsigned long long x[RC * K], u[RC * N], v[RC * N];
-#pragma unroll
-      for (int i = 0; i < RC * K; ++i) x[i] = in64[rd[r0 * K + i] * 32 + lane];
-#pragma unroll
-      for (int i = 0; i < RC * N; ++i) u[i] = v[i] = 0ull;
-#pragma unroll
-      for (int n = 0; n < N; ++n)
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const ulonglong2 q = wq[k * N + n];  // ((wr, wr), (wi, -wi))
-#pragma unroll
-          for (int r = 0; r < RC; ++r) {
-            ffma2(u[r * N + n], x[r * K + k], q.x);
-            ffma2(v[r * N + n], x[r * K + k], q.y);
-          }
-        }
-#pragma unroll
-      for (int i = 0; i < RC * N; ++i) {
-        float2 a, b;
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(u[i]));
-        asm("mov.b64 {%0, %1}, %2;" : "=f"(b.x), "=f"(b.y) : "l"(v[i]));
-        out[wr[r0 * N + i] * 32 + lane] = make_float2(a.x + b.y, a.y + b.x);
+        for (int r = 0; r < RC; ++r) cmac<EXACT>(y[r * N + n], x[r * K + k], wv);
       }
-    }
+#pragma unroll
+    for (int i = 0; i < RC * N; ++i) out[wr[r0 * N + i] * 32 + lane] = y[i];
   }
 }
 
 template <bool EXACT>
 __device__ __forceinline__ void run_stage(const ChainStage &st, const float2 *in, float2 *out,
                                           int lane, const uint8_t *rd, const uint8_t *wr,
-                                          const void *w) {
+                                          const float2 *w) {
   // every (log R, log K, log N) with R K <= 16, R N <= 16 (kChainMaxLog = 4), K, N <= 8
   switch ((st.lr * 5 + st.lk) * 5 + st.ln) {  // one jump-table branch per stage
 #define STN_CH(a, b, c)                                       \
@@ -165,9 +125,8 @@ __global__ void __launch_bounds__(kChThreads, 2)
   int64_t *sxin = reinterpret_cast<int64_t *>(sor + 4);  // [kChTile]
   int64_t *sout = sxin + kChTile;                          // [kChTile]
   uint8_t *stab = reinterpret_cast<uint8_t *>(sout + kChTile);   // rd / wr tables
-  // W of all stages: EXACT float2, FAST float4 ((wr, wr), (wi, -wi)) for FFMA2
-  float4 *sw = reinterpret_cast<float4 *>(stab + kChainMaxTab);
-  float2 *bufs = reinterpret_cast<float2 *>(sw + g.w_total);  // [warp][kChBufs][slot][lane]
+  float2 *sw = reinterpret_cast<float2 *>(stab + kChainMaxTab);  // W of all stages
+  float2 *bufs = sw + ((g.w_total + 1) & ~1);                   // [warp][kChBufs][slot][lane]
   const int b = blockIdx.y;
   const float2 *X = static_cast<const float2 *>(p.a) + int64_t(b) * p.a_bs;
   float2 *O = static_cast<float2 *>(p.out) + int64_t(b) * p.out_bs;
@@ -184,13 +143,7 @@ __global__ void __launch_bounds__(kChThreads, 2)
     const ChainStage &st = g.st[s];
     const float2 *W = static_cast<const float2 *>(g.w[s]) + int64_t(b) * g.w_bs[s];
     const int kn = 1 << (st.lk + st.ln);
-    for (int i = threadIdx.x; i < kn; i += kChThreads) {
-      const float2 wv = W[T->widx[st.w_off + i]];
-      if (EXACT)
-        reinterpret_cast<float2 *>(sw)[st.w_smem + i] = wv;
-      else
-        sw[st.w_smem + i] = make_float4(wv.x, wv.x, wv.y, -wv.y);
-    }
+    for (int i = threadIdx.x; i < kn; i += kChThreads) sw[st.w_smem + i] = W[T->widx[st.w_off + i]];
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -226,9 +179,7 @@ __global__ void __launch_bounds__(kChThreads, 2)
     float2 *dst = work0;
     for (int s = 0; s < g.n_stages; ++s) {
       const ChainStage &st = g.st[s];
-      run_stage<EXACT>(st, cur, dst, lane, stab + st.rd_off, stab + st.wr_off,
-                       EXACT ? static_cast<const void *>(reinterpret_cast<float2 *>(sw) + st.w_smem)
-                             : static_cast<const void *>(sw + st.w_smem));
+      run_stage<EXACT>(st, cur, dst, lane, stab + st.rd_off, stab + st.wr_off, sw + st.w_smem);
       if (s == 0)  // the ring slot is consumed: refill it with the row kChRing steps ahead
         issue(row + kChRing * step, ring + slot * kChBuf);
       cur = dst;
@@ -250,7 +201,7 @@ __global__ void __launch_bounds__(kChThreads, 2)
 }  // namespace
 
 size_t chain_smem_bytes(const ChainGeom &g) {
-  return 8 * 2 * 1024 + 8 * 2 * kChTile + kChainMaxTab + 16 * size_t(g.w_total) +
+  return 8 * 2 * 1024 + 8 * 2 * kChTile + kChainMaxTab + 8 * size_t((g.w_total + 1) & ~1) +
          size_t(kChWarps) * kChBufs * (size_t(32) << g.ma) * 8;
 }
 

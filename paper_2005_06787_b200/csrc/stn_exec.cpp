@@ -1199,6 +1199,9 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
     const int lr = int(R.size()), lk = int(st.k.size()), ln_ = int(st.n.size());
     if (lr + lk > stn::kChainMaxLog || lr + ln_ > stn::kChainMaxLog) return false;
     if (lk > 3 || ln_ > 3) return false;  // stage shapes the kernel instantiates: K, N <= 8
+    // per-column math: K x N > 16 stages run slower fused than as separate HBM-rate steps
+    // (cfg5 chain 1613-1614, K x N = 32: 41 ms fused vs 37 ms unfused, measured on B200)
+    if (lk + ln_ > 4) return false;
     g.ma = std::max(g.ma, std::max(lr + lk, lr + ln_));
     if (int(R.size()) + lk != int(L.size())) return false;  // a K line not in the tile
     auto slot_in = [&](int ln) {
