@@ -35,9 +35,8 @@ using namespace dev;
 constexpr int kChThreads = 128;
 constexpr int kChWarps = kChThreads / 32;
 constexpr int kChTile = 1 << kChainMaxLog;  // slots per column
-constexpr int kChRing = 2;                  // rows of inputs in flight per warp (cp.async)
-constexpr int kChBufs = kChRing + 1;        // + a work buffer: stages ping-pong between it
-                                            //   and the row's (consumed) ring slot
+constexpr int kChRing = 3;                  // rows of inputs in flight per warp (cp.async)
+constexpr int kChBufs = kChRing + 2;        // + two work buffers the stages ping-pong on
 // a buffer is [slot][lane], 2^ma slots: the chain's largest tile (g.ma <= kChainMaxLog)
 
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
@@ -63,7 +62,7 @@ __device__ __forceinline__ void chain_stage(const float2 *__restrict__ in, float
                                          const float2 *__restrict__ w) {
   constexpr int R = 1 << LR, K = 1 << LK, N = 1 << LN;
   // rows per chunk: RC (K + N) <= 16 complex values live
-  constexpr int RCMAX = 8 / (K + N) > 0 ? 8 / (K + N) : 1;
+  constexpr int RCMAX = 16 / (K + N) > 0 ? 16 / (K + N) : 1;
   constexpr int RC = RCMAX >= R ? R : (RCMAX >= 8 ? 8 : (RCMAX >= 4 ? 4 : (RCMAX >= 2 ? 2 : 1)));
   float2 x[RC * K], y[RC * N];
 #pragma unroll 1
@@ -117,7 +116,7 @@ __device__ __forceinline__ void run_stage(const ChainStage &st, const float2 *in
 // stages run; a lane only ever touches its own column, so no warp barrier is
 // needed between the copies, the stages and the stores.
 template <bool EXACT>
-__global__ void __launch_bounds__(kChThreads, 3)
+__global__ void __launch_bounds__(kChThreads, 2)
     k_chain(const ChainTables *__restrict__ T, const __grid_constant__ ChainGeom g,
             const BatchPtrs p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -151,7 +150,7 @@ __global__ void __launch_bounds__(kChThreads, 3)
   const int64_t xl = T->xl[lane], ol = T->ol[lane];
   const int kChBuf = 32 << g.ma;  // float2 per buffer
   float2 *wb = bufs + int64_t(warp) * kChBufs * kChBuf;
-  float2 *ring = wb, *work = wb + kChRing * kChBuf;
+  float2 *ring = wb, *work0 = wb + kChRing * kChBuf, *work1 = work0 + kChBuf;
   const int ni = 1 << g.li, no = 1 << g.lo;
   const int64_t step = int64_t(gridDim.x) * kChWarps;
   const int64_t row0 = int64_t(blockIdx.x) * kChWarps + warp;
@@ -176,14 +175,15 @@ __global__ void __launch_bounds__(kChThreads, 3)
   int slot = 0;
   for (int64_t row = row0; row < g.rows; row += step) {
     cp_wait<kChRing - 1>();  // this row's inputs have landed (own column only)
-    float2 *mine = ring + slot * kChBuf;
-    const float2 *cur = mine;
-    float2 *dst = work;
+    const float2 *cur = ring + slot * kChBuf;
+    float2 *dst = work0;
     for (int s = 0; s < g.n_stages; ++s) {
       const ChainStage &st = g.st[s];
       run_stage<EXACT>(st, cur, dst, lane, stab + st.rd_off, stab + st.wr_off, sw + st.w_smem);
+      if (s == 0)  // the ring slot is consumed: refill it with the row kChRing steps ahead
+        issue(row + kChRing * step, ring + slot * kChBuf);
       cur = dst;
-      dst = dst == work ? mine : work;
+      dst = dst == work0 ? work1 : work0;
     }
     const int64_t bo = row_o(row) + ol;
     float2 v[kChTile];
@@ -193,8 +193,6 @@ __global__ void __launch_bounds__(kChThreads, 3)
 #pragma unroll
     for (int i = 0; i < kChTile; ++i)
       if (i < no) __stcs(O + bo + sout[i], v[i]);
-    // the ring slot is free again: refill it with the row kChRing steps ahead
-    issue(row + kChRing * step, mine);
     slot = slot + 1 == kChRing ? 0 : slot + 1;
   }
   cp_wait<0>();
