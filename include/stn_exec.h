@@ -385,6 +385,11 @@ int stn_selftest_gemm_tc(int64_t M, int64_t N, int64_t K, int32_t batches, int32
                          int32_t b_batched, int32_t reps, double *max_rel_err, double *ms_total,
                          double *ms_gemm, double *ms_simt, double *simt_rel_err);
 
+/* Code-generation check (no device needed): emits the NVRTC source of a synthetic
+ * fused stem chain (the plan-specialised kernels of chain_jit.cpp) and compiles it
+ * for sm_100a; `log` (may be NULL) receives the compiler log. */
+int stn_selftest_chain_jit(int exact, char *log, int32_t log_cap);
+
 /* Memory-pipeline check: a 2^log2_elems complex64 tensor is bit-permuted by
  * the tiled absorb kernel (perm[i] = source bit of output bit i; identity when
  * NULL) and copied with cudaMemcpyAsync; returns GB/s (read + write) of both

@@ -169,6 +169,7 @@ SIGNATURES = {
     "stn_run_scheme_multi": (C.c_int, [C.POINTER(PlanDesc), C.c_int, C.POINTER(C.c_int32),
                                        C.c_int, C.c_int, C.POINTER(C.c_double),
                                        C.POINTER(RunReport)]),
+    "stn_selftest_chain_jit": (C.c_int, [C.c_int, C.c_char_p, C.c_int32]),
     "stn_selftest_bitperm": (C.c_int, [C.c_int32, C.POINTER(C.c_int32), C.c_int32,
                                        C.POINTER(C.c_double), C.POINTER(C.c_double),
                                        C.POINTER(C.c_int32)]),

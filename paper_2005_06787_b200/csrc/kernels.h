@@ -31,6 +31,8 @@ namespace stn {
 //   sweep_bits=B, sweep_debug, sweep_dbg=N   stem-sweep fusion tile size / traces
 //   plan_dump, plan_timing                 per-step kernel choice / plan-build timing
 //   graphs=0               no CUDA graphs: every batch launched kernel by kernel
+//   chain=0, chain_min_bits=B, chain_jit=0   fused stem chains off / only with
+//                          intermediates >= 2^B elements (default 24) / table kernel only
 //   bitperm_legacy         legacy bit-permute kernel for the selftest
 //   sweep_only=..., no_bulk, tma_lag=N, tma_nsr=N, perm_tb=N   pipeline experiments
 //   tcf=0|1|2              fused-split GEMM never / for 2N <= 128 (default) / always

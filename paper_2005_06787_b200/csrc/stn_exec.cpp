@@ -32,6 +32,7 @@
 
 #include <cuda_runtime.h>
 
+#include "chain_jit.h"
 #include "kernels.h"
 #include "stn_exec.h"
 
@@ -359,6 +360,8 @@ struct stn_plan {
     double io_bytes = 0;  // S_0 + S_r + W's per slice, in elements
     bool chain = false;   // lane-column fused chain (kernels_chain.cu) instead of a tile sweep
     stn::ChainGeom cgeom{};
+    std::shared_ptr<stn::ChainTables> host_tables;  // for the NVRTC-specialised kernel
+    void *jit_fn = nullptr;                          // its CUfunction (chain_jit.cpp)
   };
   std::vector<Sweep> sweeps;
   std::map<int, int> sweep_of_step;
@@ -1285,6 +1288,7 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
     cuda_check(cudaMemcpy(out->tables->ptr, T.get(), sizeof(stn::ChainTables),
                           cudaMemcpyHostToDevice),
                "chain tables");
+    out->host_tables = std::shared_ptr<stn::ChainTables>(T.release());
   }
   return true;
 }
@@ -1555,6 +1559,18 @@ void plan_chains(stn_plan &P) {
       }
       a = best + 1;
     }
+  }
+  // specialise every chain of the plan with NVRTC (STN_DEBUG chain_jit=0: table kernel)
+  const char *jo = stn::debug_opt("chain_jit");
+  if (P.sweeps.empty() || (jo && std::atoi(jo) == 0)) return;
+  std::vector<stn::ChainJitSpec> specs;
+  for (auto &sw : P.sweeps) specs.push_back({&sw.cgeom, sw.host_tables.get()});
+  std::vector<void *> fns;
+  std::string log;
+  if (stn::chain_jit_compile(specs, P.mode == STN_MODE_EXACT, P.device, &fns, &log)) {
+    for (size_t i = 0; i < fns.size(); ++i) P.sweeps[i].jit_fn = fns[i];
+  } else if (stn::debug_opt("sweep_debug")) {
+    fprintf(stderr, "chain jit unavailable: %s\n", log.substr(0, 2000).c_str());
   }
 }
 
@@ -2280,9 +2296,13 @@ void launch_chain_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, 
   for (int stp : sw.steps) flops += 8.0 * double(P.steps[stp].d.mults) * nb;
   ProfScope prof(P, st, sw.steps.front());
   stn::BatchPtrs p{x.ptr, nullptr, const_cast<void *>(o.ptr), x.bs, 0, o.bs, nb};
-  cuda_check(stn::launch_chain(sw.tables->as<stn::ChainTables>(), g, p,
-                               P.mode == STN_MODE_EXACT, st),
-             "fused stem chain kernel");
+  if (sw.jit_fn)
+    cuda_check(stn::chain_jit_launch(sw.jit_fn, g, sw.tables->as<stn::ChainTables>(), p, st),
+               "fused stem chain kernel (specialised)");
+  else
+    cuda_check(stn::launch_chain(sw.tables->as<stn::ChainTables>(), g, p,
+                                 P.mode == STN_MODE_EXACT, st),
+               "fused stem chain kernel");
   prof.done(STN_KERNEL_SWEEP, bytes, flops);
 }
 
@@ -3267,6 +3287,37 @@ int stn_selftest_gemm_tc(int64_t M, int64_t N, int64_t K, int32_t batches, int32
       *simt_rel_err = e2 / std::max(scale, 1e-300);
     }
     for (auto &e : ev) cudaEventDestroy(e);
+  });
+}
+
+int stn_selftest_chain_jit(int exact, char *log, int32_t log_cap) {
+  return guarded([&] {
+    // a synthetic two-stage chain (K = N = 2 each) through the NVRTC code generator
+    stn::ChainGeom g{};
+    auto t = std::make_unique<stn::ChainTables>();
+    memset(t.get(), 0, sizeof(stn::ChainTables));
+    g.n_stages = 2;
+    g.li = 2;
+    g.lo = 2;
+    g.ma = 2;
+    g.rows = 1 << 10;
+    g.w_total = 8;
+    g.st[0] = {1, 1, 1, 0, 4, 0, 0};
+    g.st[1] = {1, 1, 1, 8, 12, 4, 4};
+    const uint8_t tab[16] = {0, 1, 2, 3, 0, 1, 2, 3, 0, 2, 1, 3, 0, 1, 2, 3};
+    memcpy(t->tab, tab, sizeof tab);
+    for (int i = 0; i < 4; ++i) {
+      t->xin[i] = i * 64;
+      t->oout[i] = i * 128;
+      t->widx[i] = t->widx[4 + i] = i;
+    }
+    std::string l;
+    const bool ok = stn::chain_jit_compile_only({{&g, t.get()}}, exact != 0, &l);
+    if (log && log_cap > 0) {
+      strncpy(log, l.c_str(), size_t(log_cap) - 1);
+      log[log_cap - 1] = 0;
+    }
+    require(ok, STN_ERR_CUDA, "NVRTC compilation of a chain kernel failed: " + l.substr(0, 400));
   });
 }
 

@@ -112,3 +112,16 @@ def _load_missing(tmp_path):
         abi.load_library(str(tmp_path / "nope.so"))
     finally:
         abi._lib = saved
+
+
+@pytest.mark.parametrize("exact", [0, 1])
+def test_chain_jit_codegen_compiles_for_sm100a(exact):
+    """The plan-specialised fused-chain kernels (chain_jit.cpp) are generated CUDA
+    compiled by NVRTC at plan creation; the generator's output must build for
+    sm_100a in both arithmetic modes (no GPU needed to compile)."""
+    import ctypes as C
+    from paper_2005_06787_b200 import abi
+    lib = abi.load_library()
+    buf = C.create_string_buffer(4096)
+    st = lib.stn_selftest_chain_jit(exact, buf, 4096)
+    assert st == 0, buf.value.decode()[:2000]
