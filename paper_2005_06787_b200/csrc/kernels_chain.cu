@@ -34,7 +34,7 @@ using namespace dev;
 
 constexpr int kChThreads = 128;
 constexpr int kChWarps = kChThreads / 32;
-constexpr int kChTile = 1 << kChainMaxLog;  // slots per column
+constexpr int kChTile = 1 << kChainTableLog;  // slots per column
 constexpr int kChRing = 3;                  // rows of inputs in flight per warp (cp.async)
 constexpr int kChBufs = kChRing + 2;        // + two work buffers the stages ping-pong on
 // a buffer is [slot][lane], 2^ma slots: the chain's largest tile (g.ma <= kChainMaxLog)
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kChThreads, 2)
     sxr[i >> 8][i & 255] = T->xr[i >> 8][i & 255];
     sor[i >> 8][i & 255] = T->orow[i >> 8][i & 255];
   }
-  for (int i = threadIdx.x; i < kChTile; i += kChThreads) {
+  for (int i = threadIdx.x; i < kChTile; i += kChThreads) {  // (g.li, g.lo <= kChainTableLog)
     sxin[i] = T->xin[i];
     sout[i] = T->oout[i];
   }

@@ -1113,7 +1113,7 @@ bool chain_candidate(const stn_plan &P, const StepPlan &sp) {
   return P.precision == STN_SINGLE && !sp.d.is_branch && sp.has_bits &&
          (sp.kern == Kern::Absorb || sp.kern == Kern::AbsorbDirect || sp.kern == Kern::AbsorbTc ||
           sp.kern == Kern::AbsorbTma || sp.kern == Kern::AbsorbMma || sp.kern == Kern::Lanes) &&
-         int(sp.kbits.size()) <= stn::kChainMaxLog && int(sp.nbits.size()) <= stn::kChainMaxLog;
+         int(sp.kbits.size()) <= 4 && int(sp.nbits.size()) <= 4;
 }
 
 // Fused stem chain over steps [steps] (kernels.h ChainGeom). Follows every bit
@@ -1124,7 +1124,11 @@ bool chain_candidate(const stn_plan &P, const StepPlan &sp) {
 // order. Stage s reads [r][k] (k bit j = the step's K bit j, ascending X position:
 // the reference's k order) and writes [r][n] (n bit j = N bit j, ascending O
 // position). False when the chain does not fit or would not coalesce.
-bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Sweep *out) {
+bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Sweep *out,
+                 bool jit) {
+  // the NVRTC-specialised kernel holds up to 32 values per column in registers; the
+  // table-driven one 16 in shared memory, K, N <= 8 and K x N <= 16 per stage
+  const int max_log = jit ? stn::kChainMaxLog : stn::kChainTableLog;
   const int ns = int(steps.size());
   if (ns < 2 || ns > stn::kChainMaxStages) return false;
   const StepPlan &s0 = P.steps[steps[0]];
@@ -1164,7 +1168,7 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
   std::vector<int> L;
   std::vector<int> passive;  // X lines never consumed
   for (int xp = 0; xp < xr0; ++xp) (consumed_by[size_t(xp)] >= 0 ? L : passive).push_back(xp);
-  if (int(L.size()) > stn::kChainMaxLog || passive.size() < 5) return false;
+  if (int(L.size()) > max_log || passive.size() < 5) return false;
   // largest tile along the chain (alive active lines at a stage's input or output)
   int ma = int(L.size());
   {
@@ -1178,7 +1182,7 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
   // small tiles carry a fixed per-row cost (table lookups, the stage dispatch): the
   // passive lines right above the lanes ride along in the tile as lines no stage
   // touches, so a column holds 2^kChainMaxLog values and there are fewer rows
-  const int extra = std::max(0, std::min(stn::kChainMaxLog - ma, int(passive.size()) - 5));
+  const int extra = std::max(0, std::min(stn::kChainTableLog - ma, int(passive.size()) - 5));
   for (int q = 0; q < extra; ++q) L.push_back(passive[size_t(5 + q)]);
   passive.erase(passive.begin() + 5, passive.begin() + 5 + extra);
   const int li = int(L.size());
@@ -1200,11 +1204,11 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
     for (int ln : L)
       if (std::find(st.k.begin(), st.k.end(), ln) == st.k.end()) R.push_back(ln);
     const int lr = int(R.size()), lk = int(st.k.size()), ln_ = int(st.n.size());
-    if (lr + lk > stn::kChainMaxLog || lr + ln_ > stn::kChainMaxLog) return false;
-    if (lk > 3 || ln_ > 3) return false;  // stage shapes the kernel instantiates: K, N <= 8
-    // per-column math: K x N > 16 stages run slower fused than as separate HBM-rate steps
-    // (cfg5 chain 1613-1614, K x N = 32: 41 ms fused vs 37 ms unfused, measured on B200)
-    if (lk + ln_ > 4) return false;
+    if (lr + lk > max_log || lr + ln_ > max_log) return false;
+    // table kernel: the stage shapes it instantiates (K, N <= 8), and K x N <= 16 (with
+    // larger ones its per-column math is slower than the separate HBM-rate steps: cfg5
+    // chain 1613-1614, K x N = 32, 41 ms fused vs 37 ms unfused, measured on B200)
+    if (!jit && (lk > 3 || ln_ > 3 || lk + ln_ > 4)) return false;
     g.ma = std::max(g.ma, std::max(lr + lk, lr + ln_));
     if (int(R.size()) + lk != int(L.size())) return false;  // a K line not in the tile
     auto slot_in = [&](int ln) {
@@ -1508,9 +1512,33 @@ bool build_sweep(const stn_plan &P, const std::vector<int> &steps, int max_bits,
 // build_chain accepts; only segments whose intermediate stems are large enough to
 // matter are fused. STN_DEBUG chain=0 disables it; chain_min_bits=B (default 24):
 // fuse only when an intermediate stem has >= 2^B elements.
+void plan_chains(stn_plan &P, bool jit);
+
 void plan_chains(stn_plan &P) {
   const char *opt = stn::debug_opt("chain");
   if (opt && std::atoi(opt) == 0) return;
+  const char *jo = stn::debug_opt("chain_jit");
+  const bool jit = stn::chain_jit_available() && !(jo && std::atoi(jo) == 0);
+  plan_chains(P, jit);
+  if (!jit || P.sweeps.empty()) return;
+  // specialise every chain of the plan with NVRTC; if that fails, plan again for the
+  // table-driven kernel (its tile and stage-shape limits are tighter)
+  std::vector<stn::ChainJitSpec> specs;
+  for (auto &sw : P.sweeps) specs.push_back({&sw.cgeom, sw.host_tables.get()});
+  std::vector<void *> fns;
+  std::string log;
+  if (stn::chain_jit_compile(specs, P.mode == STN_MODE_EXACT, P.device, &fns, &log)) {
+    for (size_t i = 0; i < fns.size(); ++i) P.sweeps[i].jit_fn = fns[i];
+    return;
+  }
+  if (stn::debug_opt("sweep_debug"))
+    fprintf(stderr, "chain jit failed, table kernel instead: %s\n", log.substr(0, 2000).c_str());
+  P.sweeps.clear();
+  P.sweep_of_step.clear();
+  plan_chains(P, false);
+}
+
+void plan_chains(stn_plan &P, bool jit) {
   const char *mb = stn::debug_opt("chain_min_bits");
   const int min_bits = mb ? std::atoi(mb) : 24;
   const int n = int(P.steps.size());
@@ -1534,7 +1562,7 @@ void plan_chains(stn_plan &P) {
       size_t best = a;
       for (size_t b = a + 1; b < chain.size(); ++b) {
         std::vector<int> seg(chain.begin() + a, chain.begin() + b + 1);
-        if (build_chain(P, seg, nullptr))
+        if (build_chain(P, seg, nullptr, jit))
           best = b;
         else
           break;
@@ -1545,7 +1573,7 @@ void plan_chains(stn_plan &P) {
         for (size_t q = 0; q + 1 < seg.size(); ++q)
           largest_mid = std::max<int64_t>(largest_mid, P.steps[seg[q]].osize);
         stn_plan::Sweep sw;
-        if (largest_mid >= (int64_t(1) << min_bits) && build_chain(P, seg, &sw)) {
+        if (largest_mid >= (int64_t(1) << min_bits) && build_chain(P, seg, &sw, jit)) {
           const int id = int(P.sweeps.size());
           if (stn::debug_opt("sweep_debug")) {
             fprintf(stderr, "chain %d: steps", id);
@@ -1559,18 +1587,6 @@ void plan_chains(stn_plan &P) {
       }
       a = best + 1;
     }
-  }
-  // specialise every chain of the plan with NVRTC (STN_DEBUG chain_jit=0: table kernel)
-  const char *jo = stn::debug_opt("chain_jit");
-  if (P.sweeps.empty() || (jo && std::atoi(jo) == 0)) return;
-  std::vector<stn::ChainJitSpec> specs;
-  for (auto &sw : P.sweeps) specs.push_back({&sw.cgeom, sw.host_tables.get()});
-  std::vector<void *> fns;
-  std::string log;
-  if (stn::chain_jit_compile(specs, P.mode == STN_MODE_EXACT, P.device, &fns, &log)) {
-    for (size_t i = 0; i < fns.size(); ++i) P.sweeps[i].jit_fn = fns[i];
-  } else if (stn::debug_opt("sweep_debug")) {
-    fprintf(stderr, "chain jit unavailable: %s\n", log.substr(0, 2000).c_str());
   }
 }
 
@@ -2299,6 +2315,8 @@ void launch_chain_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, 
   if (sw.jit_fn)
     cuda_check(stn::chain_jit_launch(sw.jit_fn, g, sw.tables->as<stn::ChainTables>(), p, st),
                "fused stem chain kernel (specialised)");
+  else if (g.ma > stn::kChainTableLog)
+    fail(STN_ERR_CUDA, "fused stem chain planned for the specialised kernel has none");
   else
     cuda_check(stn::launch_chain(sw.tables->as<stn::ChainTables>(), g, p,
                                  P.mode == STN_MODE_EXACT, st),
