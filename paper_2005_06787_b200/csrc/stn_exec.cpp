@@ -1282,7 +1282,7 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
   };
   if (efficiency(T->xl, T->xin, 1 << li) < 0.5 || efficiency(T->ol, T->oout, 1 << g.lo) < 0.5)
     return false;
-  if (stn::chain_smem_bytes(g) > 110 * 1024) return false;
+  if (!jit && stn::chain_smem_bytes(g) > 110 * 1024) return false;  // table kernel's tiles
   if (out) {
     out->steps = steps;
     out->chain = true;
