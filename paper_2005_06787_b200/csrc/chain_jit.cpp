@@ -15,6 +15,13 @@
 #include "chain_jit.h"
 
 #include <dlfcn.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <thread>
 
 #include <cstdio>
 #include <cstring>
@@ -195,12 +202,93 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
   return s.str();
 }
 
-struct Module {
-  CUmodule mod = nullptr;
-  std::vector<CUfunction> fns;
-};
+// One compiled chain kernel per (source, device).
 std::mutex g_mu;
-std::map<std::pair<std::string, int>, Module> g_cache;  // (source, device) -> module
+std::map<std::pair<std::string, int>, CUfunction> g_fns;
+std::map<std::string, std::vector<char>> g_cubins;  // source -> cubin (any device)
+
+const char *const kOpts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "--fmad=false"};
+constexpr int kNOpts = 3;
+
+uint64_t fnv1a(const std::string &s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
+  return h;
+}
+
+// On-disk cubin cache shared by the processes of one host (tests, smoke, bench each
+// create plans): $STN_JIT_CACHE, else jit_cache/ next to this library. Best effort:
+// any I/O problem just means a recompile.
+std::string cache_dir() {
+  const char *e = std::getenv("STN_JIT_CACHE");
+  if (e && *e) return e;
+  Dl_info info;
+  if (dladdr(reinterpret_cast<void *>(&cache_dir), &info) && info.dli_fname) {
+    std::string so = info.dli_fname;
+    const size_t slash = so.rfind('/');
+    if (slash != std::string::npos) return so.substr(0, slash) + "/jit_cache";
+  }
+  return "/tmp/stn_exec_jit";
+}
+
+std::string cache_path(const std::string &src) {
+  char name[64];
+  snprintf(name, sizeof name, "/chain_%016llx_%zu.cubin", (unsigned long long)fnv1a(src),
+           src.size());
+  return cache_dir() + name;
+}
+
+bool read_file(const std::string &path, std::vector<char> *out) {
+  FILE *f = fopen(path.c_str(), "rb");
+  if (!f) return false;
+  fseek(f, 0, SEEK_END);
+  const long n = ftell(f);
+  fseek(f, 0, SEEK_SET);
+  out->resize(size_t(n > 0 ? n : 0));
+  const bool ok = n > 0 && fread(out->data(), 1, size_t(n), f) == size_t(n);
+  fclose(f);
+  return ok;
+}
+
+void write_file(const std::string &path, const std::vector<char> &data) {
+  std::string dir = cache_dir(), cur;
+  for (size_t i = 0; i <= dir.size(); ++i)  // mkdir -p
+    if (i == dir.size() || dir[i] == '/') {
+      if (!cur.empty()) mkdir(cur.c_str(), 0755);
+      if (i < dir.size()) cur += '/';
+    } else {
+      cur += dir[i];
+    }
+  const std::string tmp = path + ".tmp" + std::to_string(getpid());
+  FILE *f = fopen(tmp.c_str(), "wb");
+  if (!f) return;
+  const bool ok = fwrite(data.data(), 1, data.size(), f) == data.size();
+  fclose(f);
+  if (ok) rename(tmp.c_str(), path.c_str());
+  else unlink(tmp.c_str());
+}
+
+bool nvrtc_compile(const std::string &src, std::vector<char> *cubin, std::string *log) {
+  Nvrtc &nv = Nvrtc::get();
+  void *prog = nullptr;
+  if (nv.Create(&prog, src.c_str(), "stn_chain.cu", 0, nullptr, nullptr) != 0) return false;
+  const int rc = nv.Compile(prog, kNOpts, kOpts);
+  if (rc != 0) {
+    size_t n = 0;
+    nv.GetLogSize(prog, &n);
+    std::string l(n, '\0');
+    nv.GetLog(prog, &l[0]);
+    if (log) *log = l;
+    nv.Destroy(&prog);
+    return false;
+  }
+  size_t n = 0;
+  nv.GetCubinSize(prog, &n);
+  cubin->resize(n);
+  nv.GetCubin(prog, cubin->data());
+  nv.Destroy(&prog);
+  return true;
+}
 
 }  // namespace
 
@@ -218,8 +306,7 @@ bool chain_jit_compile_only(const std::vector<ChainJitSpec> &chains, bool exact,
     src += emit(*chains[i].geom, *chains[i].tables, int(i), exact);
   void *prog = nullptr;
   if (nv.Create(&prog, src.c_str(), "stn_chains.cu", 0, nullptr, nullptr) != 0) return false;
-  const char *opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "--fmad=false"};
-  const int rc = nv.Compile(prog, 4, opts);
+  const int rc = nv.Compile(prog, kNOpts, kOpts);
   size_t n = 0;
   nv.GetLogSize(prog, &n);
   std::string l(n, '\0');
@@ -237,47 +324,70 @@ bool chain_jit_compile(const std::vector<ChainJitSpec> &chains, bool exact, int 
     if (log) *log = "NVRTC or the driver module API is not available";
     return false;
   }
-  std::string src = kPrelude;
+  // one program per chain: independent, so they compile on parallel host threads
+  std::vector<std::string> srcs(chains.size());
   for (size_t i = 0; i < chains.size(); ++i)
-    src += emit(*chains[i].geom, *chains[i].tables, int(i), exact);
-  std::lock_guard<std::mutex> lk(g_mu);
-  auto key = std::make_pair(src, device);
-  auto it = g_cache.find(key);
-  if (it == g_cache.end()) {
-    Nvrtc &nv = Nvrtc::get();
-    void *prog = nullptr;
-    if (nv.Create(&prog, src.c_str(), "stn_chains.cu", 0, nullptr, nullptr) != 0) return false;
-    const char *opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
-                          "--fmad=false"};
-    const int rc = nv.Compile(prog, 4, opts);
-    if (rc != 0) {
-      size_t n = 0;
-      nv.GetLogSize(prog, &n);
-      std::string l(n, '\0');
-      nv.GetLog(prog, &l[0]);
-      if (log) *log = l;
-      nv.Destroy(&prog);
-      return false;
-    }
-    size_t n = 0;
-    nv.GetCubinSize(prog, &n);
-    std::vector<char> cubin(n);
-    nv.GetCubin(prog, cubin.data());
-    nv.Destroy(&prog);
-    Module m;
-    if (Driver::get().ModuleLoadData(&m.mod, cubin.data()) != CUDA_SUCCESS) {
-      if (log) *log = "cuModuleLoadData failed";
-      return false;
-    }
+    srcs[i] = std::string(kPrelude) + emit(*chains[i].geom, *chains[i].tables, 0, exact);
+  std::vector<std::vector<char>> cubins(chains.size());
+  std::vector<char> have(chains.size(), 0);
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
     for (size_t i = 0; i < chains.size(); ++i) {
-      CUfunction f = nullptr;
-      const std::string name = "stn_chain_" + std::to_string(i);
-      if (Driver::get().ModuleGetFunction(&f, m.mod, name.c_str()) != CUDA_SUCCESS) return false;
-      m.fns.push_back(f);
+      auto it = g_fns.find({srcs[i], device});
+      if (it != g_fns.end()) {
+        (*fns)[i] = it->second;
+        have[i] = 2;
+        continue;
+      }
+      auto c = g_cubins.find(srcs[i]);
+      if (c != g_cubins.end()) {
+        cubins[i] = c->second;
+        have[i] = 1;
+      }
     }
-    it = g_cache.emplace(key, std::move(m)).first;
   }
-  for (size_t i = 0; i < chains.size(); ++i) (*fns)[i] = it->second.fns[i];
+  for (size_t i = 0; i < chains.size(); ++i)
+    if (!have[i] && read_file(cache_path(srcs[i]), &cubins[i])) have[i] = 1;
+  std::vector<size_t> todo;
+  for (size_t i = 0; i < chains.size(); ++i)
+    if (!have[i]) todo.push_back(i);
+  std::vector<std::string> logs(chains.size());
+  std::vector<char> ok(chains.size(), 1);
+  if (!todo.empty()) {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nt = std::min<size_t>(todo.size(), hw);
+    std::atomic<size_t> next{0};
+    std::vector<std::thread> pool;
+    for (size_t t = 0; t < nt; ++t)
+      pool.emplace_back([&] {
+        for (;;) {
+          const size_t q = next.fetch_add(1);
+          if (q >= todo.size()) return;
+          const size_t i = todo[q];
+          ok[i] = nvrtc_compile(srcs[i], &cubins[i], &logs[i]) ? 1 : 0;
+          if (ok[i]) write_file(cache_path(srcs[i]), cubins[i]);
+        }
+      });
+    for (auto &t : pool) t.join();
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (size_t i = 0; i < chains.size(); ++i) {
+    if (have[i] == 2) continue;
+    if (!ok[i]) {
+      if (log) *log = logs[i];
+      return false;
+    }
+    g_cubins[srcs[i]] = cubins[i];
+    CUmodule mod = nullptr;
+    CUfunction f = nullptr;
+    if (Driver::get().ModuleLoadData(&mod, cubins[i].data()) != CUDA_SUCCESS ||
+        Driver::get().ModuleGetFunction(&f, mod, "stn_chain_0") != CUDA_SUCCESS) {
+      if (log) *log = "cuModuleLoadData / cuModuleGetFunction failed";
+      return false;
+    }
+    g_fns[{srcs[i], device}] = f;
+    (*fns)[i] = f;
+  }
   return true;
 }
 
