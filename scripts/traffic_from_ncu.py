@@ -13,6 +13,8 @@ import sys
 CLASSES = [  # (substring of the kernel name, class)
     ("k_absorb_direct", "absorb"), ("k_absorb3", "absorb"), ("k_absorb2", "absorb"),
     ("k_absorb_lanes", "absorb"), ("k_gemm_skinny", "gemm_simt"), ("k_sum_ordered", "root"),
+    ("stn_chain_", "sweep"), ("k_chain", "sweep"), ("k_sweep", "sweep"), ("k_gemm_tcf", "gemm_tc"),
+    ("k_expand_b_raw", "gemm_tc"),
     ("k_absorb_tma", "absorb_tc"), ("k_absorb_tc", "absorb_tc"), ("k_absorb_mma", "absorb_tc"),
     ("k_gemm_tc", "gemm_tc"), ("k_split_a", "gemm_tc"), ("k_expand_b", "gemm_tc"),
     ("k_perm_tiles", "permute"), ("k_gemm_simt", "gemm_simt"), ("k_generic", "generic"),
