@@ -259,7 +259,7 @@ def run_reference_arm(args):
         "ms_per_step": 1e3 * statistics.median(walls[-args.steps:]),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c64",
         "data": "synthetic (reference-planned random circuit, seed 1)",
-        "config": config_keys(args, 1 if cfg == "cfg5" else threads),
+        "config": config_keys(args, args.slices_per_gpu or SLICES_PER_GPU[cfg]),
         "cpu_baseline": dict(cb, value=v),
         "e2e": {"value": v, "unit": "slices/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -426,6 +426,8 @@ def main():
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = None
     roof["algorithmic_bytes_per_launch"] = d["bytes"] / d["launches"] if d["launches"] else None
+    # (traffic below: ncu dram__bytes_read.sum + dram__bytes_write.sum per launch of the same
+    # class over one slice, committed under profiles/; per-launch averages of one slice)
     tpath = os.path.join(REPO, "profiles", f"dram_traffic_{args.config}.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
