@@ -307,7 +307,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    os.environ.setdefault("NCCL_DEBUG", "WARN")  # rank 0's stdout carries one JSON line
+    # rank 0's stdout carries exactly one JSON line: no NCCL version / info banner
+    os.environ["NCCL_DEBUG"] = os.environ.get("STN_NCCL_DEBUG", "WARN")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
