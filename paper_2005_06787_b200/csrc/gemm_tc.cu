@@ -466,6 +466,169 @@ __global__ void __launch_bounds__(THREADS2, 1)
   }
 }
 
+// ---- 128 x 256 tiles, BK = 16 (64-byte rows, SWIZZLE_64B), four stages ----------------
+// The 128 x 256 kernel above holds two 96 KiB stages; a k-block's TMA latency is then
+// barely covered by one stage of MMAs. Halving the stage (16 real K per stage, 64-byte
+// rows) doubles the ring depth at the same shared memory; chunks stay 256 real K.
+constexpr int BK3 = 16;
+constexpr int STAGES3 = 4;
+constexpr int CHUNK3 = 2 * CHUNK;
+constexpr int A3_TILE_BYTES = BM * BK3 * 4;   // 8 KiB
+constexpr int B3_TILE_BYTES = BN2 * BK3 * 4;  // 16 KiB
+constexpr int STAGE3_BYTES = 2 * A3_TILE_BYTES + 2 * B3_TILE_BYTES;
+constexpr size_t SMEM3_BYTES = size_t(STAGES3) * STAGE3_BYTES + 1024 + 256;
+
+// K-major SWIZZLE_64B descriptor: 8-row x 64 B atoms every 512 B (SBO).
+__device__ __forceinline__ uint64_t smem_desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFFu);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(512 >> 4) << 32;  // SBO
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(4) << 61;         // SWIZZLE_64B
+  return d;
+}
+
+__global__ void __launch_bounds__(THREADS2, 1)
+    k_gemm_tc256s(const __grid_constant__ CUtensorMap map_ahi,
+                 const __grid_constant__ CUtensorMap map_alo,
+                 const __grid_constant__ CUtensorMap map_bhi,
+                 const __grid_constant__ CUtensorMap map_blo, const TcArgs args) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *smem = reinterpret_cast<unsigned char *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES3 * STAGE3_BYTES);
+  uint64_t *empty = full + STAGES3;
+  uint64_t *tmem_full = empty + STAGES3;
+  uint64_t *tmem_empty = tmem_full + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n_tile = blockIdx.x % args.n_tiles, m_tile = blockIdx.x / args.n_tiles;
+  const int bz = blockIdx.z;
+  const int slice = bz / args.D, d = bz % args.D;
+  const int za = args.a_batched ? bz : d;
+  const int zb = args.b_batched ? bz : d;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ahi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_alo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES3; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], 8);  // one arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < args.k_blocks; ++kb) {
+        const int s = kb % STAGES3;
+        const uint32_t phase = (kb / STAGES3) & 1;
+        mbar_wait(&empty[s], phase ^ 1);
+        unsigned char *st = smem + s * STAGE3_BYTES;
+        mbar_expect_tx(&full[s], STAGE3_BYTES);
+        const int kx = kb * BK3;
+        tma_load_3d(st, &map_ahi, &full[s], kx, m_tile * BM, za);
+        tma_load_3d(st + A3_TILE_BYTES, &map_alo, &full[s], kx, m_tile * BM, za);
+        tma_load_3d(st + 2 * A3_TILE_BYTES, &map_bhi, &full[s], kx, n_tile * BN2, zb);
+        tma_load_3d(st + 2 * A3_TILE_BYTES + B3_TILE_BYTES, &map_blo, &full[s], kx, n_tile * BN2,
+                    zb);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int kb = 0; kb < args.k_blocks; ++kb) {
+        const int s = kb % STAGES3;
+        const uint32_t phase = (kb / STAGES3) & 1;
+        const int chunk = kb / CHUNK3, buf = chunk & 1;
+        const bool chunk_first = kb % CHUNK3 == 0;
+        const bool chunk_last = kb % CHUNK3 == CHUNK3 - 1 || kb == args.k_blocks - 1;
+        if (chunk_first) {
+          mbar_wait(&tmem_empty[buf], ((chunk >> 1) & 1) ^ 1);
+          tc_fence_after();
+        }
+        mbar_wait(&full[s], phase);
+        tc_fence_after();
+        const uint32_t st = smem_u32(smem + s * STAGE3_BYTES);
+        const uint64_t ahi = smem_desc_sw64(st);
+        const uint64_t alo = smem_desc_sw64(st + A3_TILE_BYTES);
+        const uint64_t bhi = smem_desc_sw64(st + 2 * A3_TILE_BYTES);
+        const uint64_t blo = smem_desc_sw64(st + 2 * A3_TILE_BYTES + B3_TILE_BYTES);
+        const uint32_t tacc = tmem_base + uint32_t(buf * BN2);
+#pragma unroll
+        for (int k = 0; k < BK3 / UK; ++k) {
+          const uint64_t koff = uint64_t((k * UK * 4) >> 4);
+          const uint32_t acc0 = (!chunk_first || k > 0) ? 1u : 0u;
+          umma_tf32(tacc, ahi + koff, bhi + koff, kIdesc2, acc0);
+          umma_tf32(tacc, ahi + koff, blo + koff, kIdesc2, 1u);
+          umma_tf32(tacc, alo + koff, bhi + koff, kIdesc2, 1u);
+        }
+        umma_commit(&empty[s]);
+        if (chunk_last) umma_commit(&tmem_full[buf]);
+      }
+    }
+  } else {
+    // ---- epilogue: warps 2..9; (warp % 4) = TMEM lane quadrant, half = 128-column half ----
+    const int q4 = warp % 4, half = (warp - 2) / 4;
+    const int lane_base = 32 * q4;
+    const int row = m_tile * BM + lane_base + lane;
+    float acc[128];
+#pragma unroll
+    for (int c = 0; c < 128; ++c) acc[c] = 0.f;
+    const int n_chunks = (args.k_blocks + CHUNK3 - 1) / CHUNK3;
+    for (int chunk = 0; chunk < n_chunks; ++chunk) {
+      const int buf = chunk & 1;
+      mbar_wait(&tmem_full[buf], (chunk >> 1) & 1);
+      tc_fence_after();
+      const uint32_t t0 =
+          tmem_base + (uint32_t(lane_base) << 16) + uint32_t(buf * BN2 + 128 * half);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(t0 + uint32_t(cc * 32), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc[cc * 32 + q] += __uint_as_float(v[q]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[buf]);
+    }
+    float *crow = args.c + int64_t(slice) * args.c_bs + int64_t(d) * args.c_ds +
+                  int64_t(row) * args.two_n + int64_t(n_tile) * BN2 + 128 * half;
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      reinterpret_cast<float4 *>(crow)[q] =
+          make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(512));
+  }
+}
+
 // ---- operand preparation --------------------------------------------------------
 // A (complex M x K per batch) -> hi/lo planes, same M x 2K real layout.
 __global__ void k_split_a(const float *__restrict__ a, int64_t a_bs, int64_t a_ds, int D,
@@ -539,15 +702,16 @@ EncodeFn encode_fn() {
 }
 
 bool make_map(CUtensorMap *map, const float *base, int64_t inner, int64_t rows, int64_t batches,
-              int box_rows) {
+              int box_rows, int box_k = BK) {
   EncodeFn enc = encode_fn();
   if (!enc) return false;
   cuuint64_t dims[3] = {cuuint64_t(inner), cuuint64_t(rows), cuuint64_t(batches)};
   cuuint64_t strides[2] = {cuuint64_t(inner * 4), cuuint64_t(inner * rows * 4)};
-  cuuint32_t box[3] = {cuuint32_t(BK), cuuint32_t(box_rows), 1};
+  cuuint32_t box[3] = {cuuint32_t(box_k), cuuint32_t(box_rows), 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(base), dims, strides,
-             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             box_k == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
@@ -605,10 +769,15 @@ cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspa
   const char *env_bn = stn::debug_opt("gemm_bn");
   const bool wide = (2 * s.N) % BN2 == 0 && !(env_bn && std::atoi(env_bn) == 128);
   const int bn = wide ? BN2 : BN;
+  // 128 x 256 tiles with 16-K stages (four-deep ring): STN_DEBUG gemm_bk=16
+  const char *env_bk = stn::debug_opt("gemm_bk");
+  const bool deep = wide && env_bk && std::atoi(env_bk) == 16;
+  const int bk = deep ? BK3 : BK;
   CUtensorMap mah, mal, mbh, mbl;
-  if (!make_map(&mah, ahi, 2 * s.K, s.M, nbA, BM) || !make_map(&mal, alo, 2 * s.K, s.M, nbA, BM) ||
-      !make_map(&mbh, bhi, 2 * s.K, 2 * s.N, nbB, bn) ||
-      !make_map(&mbl, blo, 2 * s.K, 2 * s.N, nbB, bn))
+  if (!make_map(&mah, ahi, 2 * s.K, s.M, nbA, BM, bk) ||
+      !make_map(&mal, alo, 2 * s.K, s.M, nbA, BM, bk) ||
+      !make_map(&mbh, bhi, 2 * s.K, 2 * s.N, nbB, bn, bk) ||
+      !make_map(&mbl, blo, 2 * s.K, 2 * s.N, nbB, bn, bk))
     return cudaErrorNotSupported;
   static bool attr_on[kMaxDevices] = {};
   bool &attr_set = attr_on[current_device()];
@@ -619,6 +788,9 @@ cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspa
     e = cudaFuncSetAttribute(k_gemm_tc256, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(SMEM2_BYTES));
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_gemm_tc256s, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(SMEM3_BYTES));
+    if (e != cudaSuccess) return e;
     attr_set = true;
   }
   TcArgs args;
@@ -628,12 +800,14 @@ cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspa
   args.D = int(s.D);
   args.a_batched = p.a_bs != 0;
   args.b_batched = p.b_bs != 0;
-  args.k_blocks = int(2 * s.K / BK);
+  args.k_blocks = int(2 * s.K / bk);
   args.two_n = int(2 * s.N);
   args.n_tiles = int(2 * s.N / bn);
   dim3 grid(unsigned((2 * s.N / bn) * (s.M / BM)), 1, unsigned(s.D * p.nbatch));
   if (gemm_events) cudaEventRecord(gemm_events[0], stream);
-  if (wide)
+  if (deep)
+    k_gemm_tc256s<<<grid, THREADS2, SMEM3_BYTES, stream>>>(mah, mal, mbh, mbl, args);
+  else if (wide)
     k_gemm_tc256<<<grid, THREADS2, SMEM2_BYTES, stream>>>(mah, mal, mbh, mbl, args);
   else
     k_gemm_tc<<<grid, THREADS, SMEM_BYTES, stream>>>(mah, mal, mbh, mbl, args);
