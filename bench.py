@@ -269,6 +269,7 @@ def run_reference_arm(args):
 def config_keys(args, slices_per_step: int) -> dict:
     return {"workload": WORKLOAD_TEXT[args.config], "plan": CONFIGS[args.config],
             "slices_per_gpu_per_step": slices_per_step, "mode": args.mode,
+            "streams": args.streams,
             "parallelism": "slices sharded over the GPUs (one process each), chained "
                            "1 KiB fp64 fold across ranks",
             "l2": "stem tensors >> L2 (126 MB); no flush needed"}
@@ -291,6 +292,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--streams", type=int, default=2)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -319,6 +321,9 @@ def main():
     t_setup = time.perf_counter()
     desc = load_desc(plan_file(args.config))
     plan = ExecutablePlan.from_desc(desc, device=local, mode=args.mode)
+    # batches of slices rotate over this many streams, each with its own arena (the
+    # library caps it by free HBM: cfg5's 96 GiB arena runs one lane)
+    plan.set_streams(args.streams)
     cache = build_branch_cache(plan, stream)
     torch.cuda.synchronize(dev)
     setup_s = time.perf_counter() - t_setup
