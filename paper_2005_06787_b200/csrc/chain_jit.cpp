@@ -132,32 +132,10 @@ __device__ __forceinline__ float2 cmx(float2 acc, float2 x, float2 w) {  // EXAC
   float im = __fadd_rn(__fmul_rn(x.x, w.y), __fmul_rn(x.y, w.x));
   return make_float2(__fadd_rn(acc.x, re), __fadd_rn(acc.y, im));
 }
-__device__ __forceinline__ float2 cmf(float2 acc, float2 x, float2 w) {  // FAST (unused)
+__device__ __forceinline__ float2 cmf(float2 acc, float2 x, float2 w) {  // FAST
   acc.x = fmaf(x.x, w.x, acc.x); acc.x = fmaf(-x.y, w.y, acc.x);
   acc.y = fmaf(x.x, w.y, acc.y); acc.y = fmaf(x.y, w.x, acc.y);
   return acc;
-}
-// FAST: complex values as 64-bit (re, im) pairs and packed FP32 FMAs (FFMA2): with W
-// staged as ((wr, wr), (wi, -wi)), U += x (wr, wr) and V += x (wi, -wi);
-// re = U.x + V.y, im = U.y + V.x.
-typedef unsigned long long u64;
-__device__ __forceinline__ u64 ldcs64(const float2 *p) {
-  u64 v; asm volatile("ld.global.cs.b64 %0, [%1];" : "=l"(v) : "l"(p)); return v;
-}
-__device__ __forceinline__ void stcs64(float2 *p, u64 v) {
-  asm volatile("st.global.cs.b64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ u64 pk(float a, float b) {
-  u64 r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b)); return r;
-}
-__device__ __forceinline__ void f2(u64 &acc, u64 x, u64 w) {
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(x), "l"(w));
-}
-__device__ __forceinline__ u64 fin(u64 u, u64 v) {
-  float ux, uy, vx, vy;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(ux), "=f"(uy) : "l"(u));
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(vx), "=f"(vy) : "l"(v));
-  return pk(ux + vy, uy + vx);
 }
 )";
 
@@ -165,29 +143,26 @@ __device__ __forceinline__ u64 fin(u64 u, u64 v) {
 std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) {
   std::ostringstream s;
   const int ni = 1 << g.li, no = 1 << g.lo;
-  // value type of the tile registers: float2 (EXACT) or a packed 64-bit pair (FAST)
-  const char *vt = exact ? "float2" : "u64";
+  const char *cm = exact ? "cmx" : "cmf";
   s << "extern \"C\" __global__ void __launch_bounds__(256) stn_chain_" << id
     << "(const JitArgs a) {\n"
     << "  __shared__ long long sxr[1024], sor[1024];\n"
-    << "  __shared__ " << (exact ? "float2" : "ulonglong2") << " sw["
-    << (g.w_total > 0 ? g.w_total : 1) << "];\n"
+    << "  __shared__ float2 sw[" << (g.w_total > 0 ? g.w_total : 1) << "];\n"
     << "  for (int i = threadIdx.x; i < 1024; i += 256) { sxr[i] = a.tabs[i]; sor[i] = a.tabs[1024 + i]; }\n"
     << "  const long long b = blockIdx.y;\n";
   // W: one staging statement per element (constant offsets)
+  int wi = 0;
   for (int st = 0; st < g.n_stages; ++st) {
     const ChainStage &cs = g.st[st];
     const int kn = 1 << (cs.lk + cs.ln);
     s << "  if (threadIdx.x < " << kn << ") {\n    const int i = threadIdx.x;\n"
       << "    const int widx[" << kn << "] = {";
     for (int i = 0; i < kn; ++i) s << (i ? "," : "") << kt.widx[cs.w_off + i];
-    s << "};\n    const float2 wv = a.w[" << st << "][b * a.w_bs[" << st << "] + widx[i]];\n";
-    if (exact)
-      s << "    sw[" << cs.w_smem << " + i] = wv;\n  }\n";
-    else
-      s << "    sw[" << cs.w_smem
-        << " + i] = make_ulonglong2(pk(wv.x, wv.x), pk(wv.y, -wv.y));\n  }\n";
+    s << "};\n    sw[" << cs.w_smem << " + i] = a.w[" << st << "][b * a.w_bs[" << st
+      << "] + widx[i]];\n  }\n";
+    wi += kn;
   }
+  (void)wi;
   s << "  __syncthreads();\n"
     << "  const int lane = threadIdx.x & 31;\n"
     << "  const long long xl = a.tabs[2048 + lane], ol = a.tabs[2080 + lane];\n"
@@ -196,17 +171,14 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
     << "  long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);\n"
     << "#define RX(r) (sxr[(r) & 255] + sxr[256 + (((r) >> 8) & 255)] + sxr[512 + (((r) >> 16) & 255)] + sxr[768 + (((r) >> 24) & 255)])\n"
     << "#define RO(r) (sor[(r) & 255] + sor[256 + (((r) >> 8) & 255)] + sor[512 + (((r) >> 16) & 255)] + sor[768 + (((r) >> 24) & 255)])\n";
-  const char *ld = exact ? "ldcs2" : "ldcs64";
-  for (int i = 0; i < ni; ++i)
-    s << "  " << vt << " n" << i << (exact ? " = make_float2(0.f, 0.f);\n" : " = 0ull;\n");
+  for (int i = 0; i < ni; ++i) s << "  float2 n" << i << " = make_float2(0.f, 0.f);\n";
   s << "  if (row < a.rows) {\n    const float2 *p = X + RX((unsigned)row) + xl;\n";
-  for (int i = 0; i < ni; ++i) s << "    n" << i << " = " << ld << "(p + " << kt.xin[i] << "LL);\n";
+  for (int i = 0; i < ni; ++i) s << "    n" << i << " = ldcs2(p + " << kt.xin[i] << "LL);\n";
   s << "  }\n  for (; row < a.rows; row += step) {\n";
-  for (int i = 0; i < ni; ++i) s << "    const " << vt << " t0_" << i << " = n" << i << ";\n";
+  for (int i = 0; i < ni; ++i) s << "    const float2 t0_" << i << " = n" << i << ";\n";
   s << "    { const long long nr = row + step;\n      if (nr < a.rows) {\n"
     << "        const float2 *p = X + RX((unsigned)nr) + xl;\n";
-  for (int i = 0; i < ni; ++i)
-    s << "        n" << i << " = " << ld << "(p + " << kt.xin[i] << "LL);\n";
+  for (int i = 0; i < ni; ++i) s << "        n" << i << " = ldcs2(p + " << kt.xin[i] << "LL);\n";
   s << "      }\n    }\n";
   for (int st = 0; st < g.n_stages; ++st) {
     const ChainStage &cs = g.st[st];
@@ -214,33 +186,18 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
     for (int r = 0; r < R; ++r)
       for (int n = 0; n < N; ++n) {
         const int out_slot = kt.tab[cs.wr_off + r * N + n];
-        if (exact) {
-          // EXACT: the reference's crow[n] += amk * brow[n], k ascending, no FMA
-          s << "    float2 t" << st + 1 << "_" << out_slot << " = make_float2(0.f, 0.f);\n";
-          for (int k = 0; k < K; ++k) {
-            const int in_slot = kt.tab[cs.rd_off + r * K + k];
-            s << "    t" << st + 1 << "_" << out_slot << " = cmx(t" << st + 1 << "_" << out_slot
-              << ", t" << st << "_" << in_slot << ", sw[" << cs.w_smem + k * N + n << "]);\n";
-          }
-        } else {
-          s << "    u64 u" << st + 1 << "_" << out_slot << " = 0ull, v" << st + 1 << "_" << out_slot
-            << " = 0ull;\n";
-          for (int k = 0; k < K; ++k) {
-            const int in_slot = kt.tab[cs.rd_off + r * K + k];
-            const int wsl = cs.w_smem + k * N + n;
-            s << "    f2(u" << st + 1 << "_" << out_slot << ", t" << st << "_" << in_slot << ", sw["
-              << wsl << "].x); f2(v" << st + 1 << "_" << out_slot << ", t" << st << "_" << in_slot
-              << ", sw[" << wsl << "].y);\n";
-          }
-          s << "    const u64 t" << st + 1 << "_" << out_slot << " = fin(u" << st + 1 << "_"
-            << out_slot << ", v" << st + 1 << "_" << out_slot << ");\n";
+        s << "    float2 t" << st + 1 << "_" << out_slot << " = make_float2(0.f, 0.f);\n";
+        for (int k = 0; k < K; ++k) {
+          const int in_slot = kt.tab[cs.rd_off + r * K + k];
+          s << "    t" << st + 1 << "_" << out_slot << " = " << cm << "(t" << st + 1 << "_"
+            << out_slot << ", t" << st << "_" << in_slot << ", sw[" << cs.w_smem + k * N + n
+            << "]);\n";
         }
       }
   }
   s << "    float2 *q = O + RO((unsigned)row) + ol;\n";
   for (int j = 0; j < no; ++j)
-    s << "    " << (exact ? "stcs2" : "stcs64") << "(q + " << kt.oout[j] << "LL, t" << g.n_stages
-      << "_" << j << ");\n";
+    s << "    stcs2(q + " << kt.oout[j] << "LL, t" << g.n_stages << "_" << j << ");\n";
   s << "  }\n#undef RX\n#undef RO\n}\n";
   return s.str();
 }
