@@ -80,6 +80,7 @@ struct Driver {
   CUresult (*ModuleGetFunction)(CUfunction *, CUmodule, const char *) = nullptr;
   CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                            unsigned, CUstream, void **, void **) = nullptr;
+  CUresult (*FuncGetAttribute)(int *, CUfunction_attribute, CUfunction) = nullptr;
   bool ok = false;
   static Driver &get() {
     static Driver d;
@@ -99,6 +100,7 @@ struct Driver {
     sym(ModuleLoadData, "cuModuleLoadData");
     sym(ModuleGetFunction, "cuModuleGetFunction");
     sym(LaunchKernel, "cuLaunchKernel");
+    sym(FuncGetAttribute, "cuFuncGetAttribute");
     ok = ModuleLoadData && ModuleGetFunction && LaunchKernel;
   }
 };
@@ -387,6 +389,13 @@ bool chain_jit_compile(const std::vector<ChainJitSpec> &chains, bool exact, int 
     }
     g_fns[{srcs[i], device}] = f;
     (*fns)[i] = f;
+    if (debug_opt("sweep_debug") && Driver::get().FuncGetAttribute) {
+      int regs = 0, local = 0;
+      Driver::get().FuncGetAttribute(&regs, CU_FUNC_ATTRIBUTE_NUM_REGS, f);
+      Driver::get().FuncGetAttribute(&local, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, f);
+      fprintf(stderr, "chain kernel %zu: li %d lo %d stages %d, %d registers, %d B local\n", i,
+              chains[i].geom->li, chains[i].geom->lo, chains[i].geom->n_stages, regs, local);
+    }
   }
   return true;
 }
