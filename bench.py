@@ -189,6 +189,7 @@ def cpu_reference_baseline(cfg: str, threads: int, budget_s: float, calib: dict 
     d = os.path.join(REPO, "tests", "golden", CONFIGS[cfg])
     if not os.path.exists(tool):
         return None
+    threads = min(threads, ref_threads_for_memory(d))
     if calib is None:
         cpath = os.path.join(d, "ref_step_ms.json")
         if os.path.exists(cpath):
@@ -211,6 +212,21 @@ def cpu_reference_baseline(cfg: str, threads: int, budget_s: float, calib: dict 
                        f"({100 * statistics.mean(fracs):.1f}% of a slice on average), scaled "
                        f"to a full slice by the per-step times "
                        f"{calib.get('source', '') if calib else ''}; wall {j['wall_s']:.1f} s")}
+
+
+def ref_threads_for_memory(golden_dir: str) -> int:
+    """Threads of the reference executor that fit this host's free RAM: each holds
+    up to four stem-sized tensors of 2^exec_cw complex64 (Engine::gemm's operands,
+    output and a permute buffer, runtime.hpp:341-453)."""
+    try:
+        with open(os.path.join(golden_dir, "meta.json")) as f:
+            cw = int(json.load(f)["plan"]["exec_cw"])
+        with open("/proc/meminfo") as f:
+            avail = next(int(line.split()[1]) * 1024 for line in f
+                         if line.startswith("MemAvailable:"))
+    except (OSError, KeyError, ValueError, StopIteration):
+        return 1
+    return max(1, int(0.6 * avail) // (4 * 8 << cw))
 
 
 def load_calib(cfg: str):

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstddef>
 #include <cstdlib>
 #include <thread>
 
@@ -49,6 +50,7 @@ struct Nvrtc {
   int (*GetLogSize)(void *, size_t *) = nullptr;
   int (*GetLog)(void *, char *) = nullptr;
   int (*Destroy)(void **) = nullptr;
+  int major = 0, minor = 0;
   bool ok = false;
   static Nvrtc &get() {
     static Nvrtc n;
@@ -57,12 +59,16 @@ struct Nvrtc {
     return n;
   }
   void load() {
-    for (const char *name : {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12",
-                             "/usr/local/cuda/lib64/libnvrtc.so"}) {
+    // the toolkit's NVRTC first: a process that imported torch already has torch's
+    // bundled (older) libnvrtc.so.12 loaded, which the bare soname would return
+    for (const char *name : {"/usr/local/cuda/lib64/libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so",
+                             "libnvrtc.so.12", "libnvrtc.so"}) {
       h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
       if (h) break;
     }
     if (!h) return;
+    auto version = reinterpret_cast<int (*)(int *, int *)>(dlsym(h, "nvrtcVersion"));
+    if (version) version(&major, &minor);
     Create = reinterpret_cast<decltype(Create)>(dlsym(h, "nvrtcCreateProgram"));
     Compile = reinterpret_cast<decltype(Compile)>(dlsym(h, "nvrtcCompileProgram"));
     GetCubinSize = reinterpret_cast<decltype(GetCubinSize)>(dlsym(h, "nvrtcGetCUBINSize"));
@@ -128,6 +134,24 @@ __device__ __forceinline__ float2 ldcs2(const float2 *p) {
 __device__ __forceinline__ void stcs2(float2 *p, float2 v) {
   asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" :: "l"(p), "f"(v.x), "f"(v.y) : "memory");
 }
+__device__ __forceinline__ void ldcs4(const float2 *p, float2 &a, float2 &b) {
+  asm volatile("ld.global.cs.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(a.x), "=f"(a.y), "=f"(b.x), "=f"(b.y) : "l"(p));
+}
+__device__ __forceinline__ void ldcs8(const float2 *p, float2 &a, float2 &b, float2 &c, float2 &d) {
+  asm volatile("ld.global.cs.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(a.x), "=f"(a.y), "=f"(b.x), "=f"(b.y), "=f"(c.x), "=f"(c.y), "=f"(d.x),
+                 "=f"(d.y) : "l"(p));
+}
+__device__ __forceinline__ void stcs4(float2 *p, float2 a, float2 b) {
+  asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};"
+               :: "l"(p), "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y) : "memory");
+}
+__device__ __forceinline__ void stcs8(float2 *p, float2 a, float2 b, float2 c, float2 d) {
+  asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+               :: "l"(p), "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y),
+                  "f"(d.x), "f"(d.y) : "memory");
+}
 // acc + x * w
 __device__ __forceinline__ float2 cmx(float2 acc, float2 x, float2 w) {  // EXACT
   float re = __fsub_rn(__fmul_rn(x.x, w.x), __fmul_rn(x.y, w.y));
@@ -141,47 +165,163 @@ __device__ __forceinline__ float2 cmf(float2 acc, float2 x, float2 w) {  // FAST
 }
 )";
 
+}  // namespace
+
+// 16 / 32-byte accesses for tiles holding the tensors' lowest positions: log2 of the
+// widest group (STN_DEBUG chain_vec=0|1|2 caps it); 32-byte (v8) accesses need PTX
+// ISA 8.8 (NVRTC >= 12.9)
+int chain_vec_max() {
+  const char *cv = debug_opt("chain_vec");
+  const Nvrtc &nv = Nvrtc::get();
+  return std::min(cv ? std::atoi(cv) : 2, nv.major > 12 || (nv.major == 12 && nv.minor >= 9) ? 2 : 1);
+}
+
+namespace {
+
+// Vector width of a tile's HBM accesses: the tile lines at positions 0 and 1 of the
+// tensor (offsets 1 and 2) make groups of 2 or 4 adjacent complex values that one
+// 16- or 32-byte access moves (a whole 32-byte sector per thread instead of one
+// element of it per lane). Returns log2 of the group size and the slot bits.
+int vec_bits(const int64_t *off, int n_log, int *s0, int *s1) {
+  *s0 = *s1 = -1;
+  for (int j = 0; j < n_log; ++j) {
+    if (off[1 << j] == 1) *s0 = j;
+    if (off[1 << j] == 2) *s1 = j;
+  }
+  if (*s0 < 0) return 0;
+  return *s1 < 0 ? 1 : 2;
+}
+
+// "dst = ld(p + off)" for every element of a tile, grouped into vector accesses.
+// `name(i)` is the register of element i; `v` the vector log (<= vmax).
+template <class Name>
+void emit_tile_io(std::ostringstream &s, bool load, const char *ptr, const int64_t *off,
+                  int n_log, int vmax, Name name, const char *indent, bool declare = true) {
+  int s0, s1;
+  int v = std::min(vec_bits(off, n_log, &s0, &s1), vmax);
+  const int m0 = s0 >= 0 ? 1 << s0 : 0, m1 = s1 >= 0 ? 1 << s1 : 0;
+  for (int i = 0; i < (1 << n_log); ++i) {
+    if (v >= 1 && (i & m0)) continue;
+    if (v >= 2 && (i & m1)) continue;
+    s << indent;
+    if (v == 0) {
+      if (load)
+        s << (declare ? "float2 " : "") << name(i) << " = ldcs2(" << ptr << " + " << off[i]
+          << "LL);\n";
+      else s << "stcs2(" << ptr << " + " << off[i] << "LL, " << name(i) << ");\n";
+    } else if (v == 1) {
+      if (load && !declare)
+        s << "ldcs4(" << ptr << " + " << off[i] << "LL, " << name(i) << ", " << name(i | m0)
+          << ");\n";
+      else if (load)
+        s << "float2 " << name(i) << ", " << name(i | m0) << "; ldcs4(" << ptr << " + " << off[i]
+          << "LL, " << name(i) << ", " << name(i | m0) << ");\n";
+      else
+        s << "stcs4(" << ptr << " + " << off[i] << "LL, " << name(i) << ", " << name(i | m0)
+          << ");\n";
+    } else {
+      if (load && !declare)
+        s << "ldcs8(" << ptr << " + " << off[i] << "LL, " << name(i) << ", " << name(i | m0)
+          << ", " << name(i | m1) << ", " << name(i | m0 | m1) << ");\n";
+      else if (load)
+        s << "float2 " << name(i) << ", " << name(i | m0) << ", " << name(i | m1) << ", "
+          << name(i | m0 | m1) << "; ldcs8(" << ptr << " + " << off[i] << "LL, " << name(i)
+          << ", " << name(i | m0) << ", " << name(i | m1) << ", " << name(i | m0 | m1) << ");\n";
+      else
+        s << "stcs8(" << ptr << " + " << off[i] << "LL, " << name(i) << ", " << name(i | m0)
+          << ", " << name(i | m1) << ", " << name(i | m0 | m1) << ");\n";
+    }
+  }
+}
+
+// Warp exchange of tile slot bit s with lane bit j (an involution): afterwards slot
+// bit s indexes what lane bit j did and vice versa.
+void emit_exchange(std::ostringstream &s, const std::string &prefix, int n_log, int j, int sb) {
+  s << "    { const bool lam = (lane >> " << j << ") & 1;\n";
+  for (int i = 0; i < (1 << n_log); ++i) {
+    if ((i >> sb) & 1) continue;
+    const std::string a = prefix + std::to_string(i), b = prefix + std::to_string(i | (1 << sb));
+    s << "      { float2 v = lam ? " << a << " : " << b << "; v.x = __shfl_xor_sync(0xffffffffu, v.x, "
+      << (1 << j) << "); v.y = __shfl_xor_sync(0xffffffffu, v.y, " << (1 << j) << "); if (lam) "
+      << a << " = v; else " << b << " = v; }\n";
+  }
+  s << "    }\n";
+}
+
 // Emits the kernel of one chain. `kt` is the host copy of its tables.
 std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) {
   std::ostringstream s;
-  const int ni = 1 << g.li, no = 1 << g.lo;
+  const int ni = 1 << g.li;
   const char *cm = exact ? "cmx" : "cmf";
+  // software pipelining holds two input tiles in registers: only for tiles of up to
+  // 2^chain_pf_log values (STN_DEBUG chain_pf_log, default 5)
+  const bool prefetch = chain_prefetch(g);
+  const int vmax = chain_vec_max();
+  // lane / tile exchanges that make the HBM accesses whole sectors (chain_lane_swap)
+  int xj = -1, xs = -1, oj = -1, os_ = -1;
+  int64_t xl_p[32], xin_p[1 << kChainMaxLog], ol_p[32], oout_p[1 << kChainMaxLog];
+  const int64_t *xin = kt.xin, *oout = kt.oout;
+  const bool swaps = vmax >= 2 && chain_swaps_allowed(g);
+  const bool xswap = swaps && chain_lane_swap(kt.xl, kt.xin, g.li, &xj, &xs);
+  const bool oswap = swaps && chain_lane_swap(kt.ol, kt.oout, g.lo, &oj, &os_);
+  if (xswap) {
+    chain_apply_swap(kt.xl, kt.xin, g.li, xj, xs, xl_p, xin_p);
+    xin = xin_p;
+  }
+  if (oswap) {
+    chain_apply_swap(kt.ol, kt.oout, g.lo, oj, os_, ol_p, oout_p);
+    oout = oout_p;
+  }
   s << "extern \"C\" __global__ void __launch_bounds__(256) stn_chain_" << id
     << "(const JitArgs a) {\n"
     << "  __shared__ long long sxr[1024], sor[1024];\n"
     << "  __shared__ float2 sw[" << (g.w_total > 0 ? g.w_total : 1) << "];\n"
     << "  for (int i = threadIdx.x; i < 1024; i += 256) { sxr[i] = a.tabs[i]; sor[i] = a.tabs[1024 + i]; }\n"
     << "  const long long b = blockIdx.y;\n";
-  // W: one staging statement per element (constant offsets)
-  int wi = 0;
+  // W: staged through the element offsets of the chain's tables (ChainTables::widx)
+  s << "  const int *widx = (const int *)((const char *)a.tabs + "
+    << offsetof(ChainTables, widx) << ");\n";
   for (int st = 0; st < g.n_stages; ++st) {
     const ChainStage &cs = g.st[st];
     const int kn = 1 << (cs.lk + cs.ln);
-    s << "  if (threadIdx.x < " << kn << ") {\n    const int i = threadIdx.x;\n"
-      << "    const int widx[" << kn << "] = {";
-    for (int i = 0; i < kn; ++i) s << (i ? "," : "") << kt.widx[cs.w_off + i];
-    s << "};\n    sw[" << cs.w_smem << " + i] = a.w[" << st << "][b * a.w_bs[" << st
-      << "] + widx[i]];\n  }\n";
-    wi += kn;
+    s << "  for (int i = threadIdx.x; i < " << kn << "; i += 256) sw[" << cs.w_smem
+      << " + i] = a.w[" << st << "][b * a.w_bs[" << st << "] + widx[" << cs.w_off << " + i]];\n";
   }
-  (void)wi;
   s << "  __syncthreads();\n"
     << "  const int lane = threadIdx.x & 31;\n"
-    << "  const long long xl = a.tabs[2048 + lane], ol = a.tabs[2080 + lane];\n"
+    << "  const long long xl = a.tabs[2048 + lane]"
+    << (xswap ? " + (((lane >> " + std::to_string(xj) + ") & 1) ? " +
+                    std::to_string(xl_p[1 << xj] - kt.xl[1 << xj]) + "LL : 0LL)"
+              : std::string())
+    << ", ol = a.tabs[2080 + lane]"
+    << (oswap ? " + (((lane >> " + std::to_string(oj) + ") & 1) ? " +
+                    std::to_string(ol_p[1 << oj] - kt.ol[1 << oj]) + "LL : 0LL)"
+              : std::string())
+    << ";\n"
     << "  const float2 *X = a.x + b * a.x_bs;\n  float2 *O = a.o + b * a.o_bs;\n"
     << "  const long long step = (long long)gridDim.x * 8;\n"
     << "  long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);\n"
     << "#define RX(r) (sxr[(r) & 255] + sxr[256 + (((r) >> 8) & 255)] + sxr[512 + (((r) >> 16) & 255)] + sxr[768 + (((r) >> 24) & 255)])\n"
     << "#define RO(r) (sor[(r) & 255] + sor[256 + (((r) >> 8) & 255)] + sor[512 + (((r) >> 16) & 255)] + sor[768 + (((r) >> 24) & 255)])\n";
-  for (int i = 0; i < ni; ++i) s << "  float2 n" << i << " = make_float2(0.f, 0.f);\n";
-  s << "  if (row < a.rows) {\n    const float2 *p = X + RX((unsigned)row) + xl;\n";
-  for (int i = 0; i < ni; ++i) s << "    n" << i << " = ldcs2(p + " << kt.xin[i] << "LL);\n";
-  s << "  }\n  for (; row < a.rows; row += step) {\n";
-  for (int i = 0; i < ni; ++i) s << "    const float2 t0_" << i << " = n" << i << ";\n";
-  s << "    { const long long nr = row + step;\n      if (nr < a.rows) {\n"
-    << "        const float2 *p = X + RX((unsigned)nr) + xl;\n";
-  for (int i = 0; i < ni; ++i) s << "        n" << i << " = ldcs2(p + " << kt.xin[i] << "LL);\n";
-  s << "      }\n    }\n";
+  if (prefetch) {
+    for (int i = 0; i < ni; ++i) s << "  float2 n" << i << " = make_float2(0.f, 0.f);\n";
+    auto nn = [](int i) { return "n" + std::to_string(i); };
+    s << "  if (row < a.rows) {\n    const float2 *p = X + RX((unsigned)row) + xl;\n";
+    emit_tile_io(s, true, "p", xin, g.li, vmax, nn, "    ", false);
+    s << "  }\n  for (; row < a.rows; row += step) {\n";
+    for (int i = 0; i < ni; ++i) s << "    float2 t0_" << i << " = n" << i << ";\n";
+    if (xswap) emit_exchange(s, "t0_", g.li, xj, xs);
+    s << "    { const long long nr = row + step;\n      if (nr < a.rows) {\n"
+      << "        const float2 *p = X + RX((unsigned)nr) + xl;\n";
+    emit_tile_io(s, true, "p", xin, g.li, vmax, nn, "        ", false);
+    s << "      }\n    }\n";
+  } else {  // large tiles: the other warps of the SM hide the load latency
+    s << "  for (; row < a.rows; row += step) {\n"
+      << "    const float2 *p = X + RX((unsigned)row) + xl;\n";
+    emit_tile_io(s, true, "p", xin, g.li, vmax, [](int i) { return "t0_" + std::to_string(i); },
+                 "    ");
+    if (xswap) emit_exchange(s, "t0_", g.li, xj, xs);
+  }
   for (int st = 0; st < g.n_stages; ++st) {
     const ChainStage &cs = g.st[st];
     const int R = 1 << cs.lr, K = 1 << cs.lk, N = 1 << cs.ln;
@@ -198,8 +338,11 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
       }
   }
   s << "    float2 *q = O + RO((unsigned)row) + ol;\n";
-  for (int j = 0; j < no; ++j)
-    s << "    stcs2(q + " << kt.oout[j] << "LL, t" << g.n_stages << "_" << j << ");\n";
+  const int last = g.n_stages;
+  if (oswap) emit_exchange(s, "t" + std::to_string(last) + "_", g.lo, oj, os_);
+  emit_tile_io(s, false, "q", oout, g.lo, vmax,
+               [last](int j) { return "t" + std::to_string(last) + "_" + std::to_string(j); },
+               "    ");
   s << "  }\n#undef RX\n#undef RO\n}\n";
   return s.str();
 }
@@ -313,7 +456,9 @@ bool chain_jit_compile_only(const std::vector<ChainJitSpec> &chains, bool exact,
   nv.GetLogSize(prog, &n);
   std::string l(n, '\0');
   nv.GetLog(prog, &l[0]);
-  if (log) *log = l + (rc == 0 ? "" : "\n--- source ---\n" + src);
+  l.resize(strlen(l.c_str()));  // the log's terminating NUL
+  if (log)
+    *log = l + (rc == 0 && !debug_opt("chain_src") ? "" : "\n--- source ---\n" + src);
   nv.Destroy(&prog);
   return rc == 0;
 }
@@ -400,8 +545,53 @@ bool chain_jit_compile(const std::vector<ChainJitSpec> &chains, bool exact, int 
   return true;
 }
 
+bool chain_prefetch(const ChainGeom &g) {
+  const char *pf = debug_opt("chain_pf_log");
+  const int pf_log = pf ? std::atoi(pf) : 5;
+  return g.li <= pf_log && g.lo <= pf_log;
+}
+
+bool chain_swaps_allowed(const ChainGeom &g) {
+  // the exchange keeps both halves of every pair live: only for kernels whose tiles
+  // leave registers to spare (~2 per float of the input tile(s) and the largest tile)
+  // -- cfg5 chain 1162-1170 (li 5, prefetched, ma 5) spilled with it: 10.3 -> 13.4 ms
+  const int est = 2 * (1 << g.li) * (chain_prefetch(g) ? 2 : 1) + 2 * (1 << g.ma);
+  return est <= 160;
+}
+
+bool chain_lane_swap(const int64_t *lane_off, const int64_t *elem_off, int n_log, int *j, int *s) {
+  const char *sw = debug_opt("chain_swap");  // STN_DEBUG chain_swap=0: no exchanges
+  if (sw && std::atoi(sw) == 0) return false;
+  int l0 = -1, s1 = -1, s0 = -1;
+  for (int b = 0; b < 5; ++b)
+    if (lane_off[1 << b] == 1) l0 = b;
+  for (int b = 0; b < n_log; ++b) {
+    if (elem_off[1 << b] == 1) s0 = b;
+    if (elem_off[1 << b] == 2) s1 = b;
+  }
+  if (l0 < 0 || s1 < 0 || s0 >= 0) return false;
+  int best = -1;  // the tile line at the highest position moves to the lanes
+  for (int b = 0; b < n_log; ++b)
+    if (b != s1 && (best < 0 || elem_off[1 << b] > elem_off[1 << best])) best = b;
+  if (best < 0) return false;
+  *j = l0;
+  *s = best;
+  return true;
+}
+
+void chain_apply_swap(const int64_t *lane_off, const int64_t *elem_off, int n_log, int j, int s,
+                      int64_t *lane_out, int64_t *elem_out) {
+  const int64_t dl = lane_off[1 << j], ds = elem_off[1 << s];
+  for (int l = 0; l < 32; ++l) lane_out[l] = lane_off[l] + (((l >> j) & 1) ? ds - dl : 0);
+  for (int i = 0; i < (1 << n_log); ++i) elem_out[i] = elem_off[i] + (((i >> s) & 1) ? dl - ds : 0);
+}
+
 cudaError_t chain_jit_launch(void *fn, const ChainGeom &g, const ChainTables *T,
                              const BatchPtrs &p, cudaStream_t stream) {
+  // the 32-byte tile accesses need 32-byte aligned tensors (arena blocks are)
+  if ((reinterpret_cast<uintptr_t>(p.a) | reinterpret_cast<uintptr_t>(p.out)) % 32 != 0 ||
+      (p.nbatch > 1 && (p.a_bs % 4 != 0 || p.out_bs % 4 != 0)))
+    return cudaErrorMisalignedAddress;
   JitArgs a{};
   a.x = p.a;
   a.o = p.out;

@@ -189,7 +189,8 @@ cudaError_t launch_absorb_direct(const DirectGeom &g, const BatchPtrs &p, bool e
 // a warp = 32 columns of the passive (never contracted) stem bits, a thread = the
 // active tile of its column (<= 2^kChainMaxLog complex values).
 constexpr int kChainMaxStages = 8;
-constexpr int kChainMaxLog = 5;      // tile limit of the NVRTC-specialised kernels (chain_jit.cpp)
+constexpr int kChainMaxLog = 6;      // tile limit of the NVRTC-specialised kernels (chain_jit.cpp)
+constexpr int kChainMultiLog = 5;    // ... for chains of more than one stage
 constexpr int kChainTableLog = 4;    // tile limit of the table-driven kernel (kernels_chain.cu)
 constexpr int kChainMaxTab = 2 * kChainMaxStages * (1 << kChainMaxLog);  // rd + wr slots
 constexpr int kChainMaxW = kChainMaxStages * 256;

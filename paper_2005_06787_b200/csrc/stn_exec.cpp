@@ -1113,7 +1113,7 @@ bool chain_candidate(const stn_plan &P, const StepPlan &sp) {
   return P.precision == STN_SINGLE && !sp.d.is_branch && sp.has_bits &&
          (sp.kern == Kern::Absorb || sp.kern == Kern::AbsorbDirect || sp.kern == Kern::AbsorbTc ||
           sp.kern == Kern::AbsorbTma || sp.kern == Kern::AbsorbMma || sp.kern == Kern::Lanes) &&
-         int(sp.kbits.size()) <= 4 && int(sp.nbits.size()) <= 4;
+         int(sp.kbits.size()) <= stn::kChainMaxLog && int(sp.nbits.size()) <= stn::kChainMaxLog;
 }
 
 // Fused stem chain over steps [steps] (kernels.h ChainGeom). Follows every bit
@@ -1124,13 +1124,44 @@ bool chain_candidate(const stn_plan &P, const StepPlan &sp) {
 // order. Stage s reads [r][k] (k bit j = the step's K bit j, ascending X position:
 // the reference's k order) and writes [r][n] (n bit j = N bit j, ascending O
 // position). False when the chain does not fit or would not coalesce.
+// Sector efficiency of ONE warp access of a tile (what the L1/L2 see per instruction,
+// not what eventually reaches DRAM): the lanes' offsets plus the vector group the
+// specialised kernel moves per access (tile elements at offsets 1, 2: chain_jit.cpp
+// vec_bits), against the 32-byte sectors they touch.
+double access_efficiency(const int64_t *lane_off_in, const int64_t *elem_off_in, int n_log,
+                         bool jit, bool swaps) {
+  const int vmax = jit ? stn::chain_vec_max() : 0;
+  int64_t lane_sw[32], elem_sw[1 << stn::kChainMaxLog];
+  const int64_t *lane_off = lane_off_in, *elem_off = elem_off_in;
+  int j, sb;
+  if (vmax >= 2 && swaps && stn::chain_lane_swap(lane_off_in, elem_off_in, n_log, &j, &sb)) {
+    stn::chain_apply_swap(lane_off_in, elem_off_in, n_log, j, sb, lane_sw, elem_sw);
+    lane_off = lane_sw;
+    elem_off = elem_sw;
+  }
+  int v = 0;
+  if (jit) {
+    bool b0 = false, b1 = false;
+    for (int j = 0; j < n_log; ++j) {
+      b0 = b0 || elem_off[1 << j] == 1;
+      b1 = b1 || elem_off[1 << j] == 2;
+    }
+    v = std::min(vmax, b0 ? (b1 ? 2 : 1) : 0);
+  }
+  std::set<int64_t> sectors;
+  for (int l = 0; l < 32; ++l)
+    for (int e = 0; e < (1 << v); ++e) sectors.insert((lane_off[l] + e) >> 2);
+  return double(32 << v) / (4.0 * double(sectors.size()));
+}
+
 bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Sweep *out,
-                 bool jit) {
-  // the NVRTC-specialised kernel holds up to 32 values per column in registers; the
-  // table-driven one 16 in shared memory, K, N <= 8 and K x N <= 16 per stage
-  const int max_log = jit ? stn::kChainMaxLog : stn::kChainTableLog;
+                 bool jit, double *eff_in, double *eff_out) {
+  // the NVRTC-specialised kernel holds up to 32 values per column in registers (64 in a
+  // one-stage chain); the table-driven one 16 in shared memory, K, N <= 8 and K x N <= 16
+  // per stage
   const int ns = int(steps.size());
-  if (ns < 2 || ns > stn::kChainMaxStages) return false;
+  const int max_log = !jit ? stn::kChainTableLog : ns == 1 ? stn::kChainMaxLog : stn::kChainMultiLog;
+  if (ns < 1 || ns > stn::kChainMaxStages || (ns == 1 && !jit)) return false;
   const StepPlan &s0 = P.steps[steps[0]];
   const int xr0 = s0.xr;
   // line bookkeeping
@@ -1218,6 +1249,9 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
     cs.lr = lr;
     cs.lk = lk;
     cs.ln = ln_;
+    if (tab + (1 << lr) * ((1 << lk) + (1 << ln_)) > stn::kChainMaxTab ||
+        widx + (1 << (lk + ln_)) > stn::kChainMaxW)
+      return false;
     cs.rd_off = tab;
     for (int r = 0; r < (1 << lr); ++r)
       for (int k = 0; k < (1 << lk); ++k) {
@@ -1243,7 +1277,6 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
         T->widx[widx++] = off;
       }
     wsm += 1 << (lk + ln_);
-    if (tab > stn::kChainMaxTab || widx > stn::kChainMaxW) return false;
     // next layout: R lines, then the stage's N lines
     L = R;
     L.insert(L.end(), st.n.begin(), st.n.end());
@@ -1282,6 +1315,9 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
   };
   if (efficiency(T->xl, T->xin, 1 << li) < 0.5 || efficiency(T->ol, T->oout, 1 << g.lo) < 0.5)
     return false;
+  const bool swaps = jit && stn::chain_swaps_allowed(g);
+  if (eff_in) *eff_in = access_efficiency(T->xl, T->xin, li, jit, swaps);
+  if (eff_out) *eff_out = access_efficiency(T->ol, T->oout, g.lo, jit, swaps);
   if (!jit && stn::chain_smem_bytes(g) > 110 * 1024) return false;  // table kernel's tiles
   if (out) {
     out->steps = steps;
@@ -1295,6 +1331,11 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
     out->host_tables = std::shared_ptr<stn::ChainTables>(T.release());
   }
   return true;
+}
+
+bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Sweep *out,
+                 bool jit) {
+  return build_chain(P, steps, out, jit, nullptr, nullptr);
 }
 
 // Tile-buffer swizzle of kernels_sweep.cu (linear over GF(2)).
@@ -1541,6 +1582,11 @@ void plan_chains(stn_plan &P) {
 void plan_chains(stn_plan &P, bool jit) {
   const char *mb = stn::debug_opt("chain_min_bits");
   const int min_bits = mb ? std::atoi(mb) : 24;
+  // one-stage chains (the specialised kernel) for slow single absorbs; STN_DEBUG
+  // chain_single=0 disables them, =2 takes every step that fits (measurements)
+  const char *so = stn::debug_opt("chain_single");
+  const bool single = jit && !(so && std::atoi(so) == 0);
+  const bool single_all = single && so && std::atoi(so) == 2;
   const int n = int(P.steps.size());
   std::vector<int> next(n, -1), has_prev(n, 0);
   for (int i = 0; i < n; ++i) {
@@ -1554,7 +1600,7 @@ void plan_chains(stn_plan &P, bool jit) {
     has_prev[c] = 1;
   }
   for (int i = 0; i < n; ++i) {
-    if (has_prev[i] || next[i] < 0) continue;
+    if (has_prev[i] || (next[i] < 0 && !(single && chain_candidate(P, P.steps[i])))) continue;
     std::vector<int> chain{i};
     while (next[chain.back()] >= 0) chain.push_back(next[chain.back()]);
     // Segmentation by dynamic programming over the run: a fused segment [a, b] gains
@@ -1564,10 +1610,15 @@ void plan_chains(stn_plan &P, bool jit) {
     // whose largest intermediate has >= 2^min_bits elements are fused.
     const int m = int(chain.size());
     std::vector<std::vector<char>> fits(size_t(m), std::vector<char>(size_t(m), 0));
+    std::vector<double> e_in(size_t(m), 0.0), e_out(size_t(m), 0.0);  // one-stage chains
     for (int a = 0; a < m; ++a)
-      for (int b = a + 1; b < m; ++b) {
+      for (int b = single ? a : a + 1; b < m; ++b) {
         std::vector<int> seg(chain.begin() + a, chain.begin() + b + 1);
-        if (!build_chain(P, seg, nullptr, jit)) break;  // longer ones from a fail too
+        if (!build_chain(P, seg, nullptr, jit, b == a ? &e_in[size_t(a)] : nullptr,
+                         b == a ? &e_out[size_t(a)] : nullptr)) {
+          if (b == a) continue;
+          break;  // longer ones from a fail too
+        }
         fits[size_t(a)][size_t(b)] = 1;
       }
     auto gain = [&](int a, int b) -> double {
@@ -1582,6 +1633,27 @@ void plan_chains(stn_plan &P, bool jit) {
         if (sp.kern == Kern::AbsorbTma || sp.kern == Kern::AbsorbTc || sp.kern == Kern::Absorb)
           g += 0.5 * double(sp.lsize + sp.rsize + sp.osize);
       }
+      if (a == b) {
+        // a one-stage chain (the specialised kernel as a single absorb) replaces the
+        // slower absorb kernels when every warp access of its stem operand moves whole
+        // 32-byte sectors and so do its stores, unless the output is small; measured on
+        // B200 (cfg5 1185: tma 3.2 -> 5.9 TB/s; 1155, stores half-sector: 3.5 -> 3.3)
+        const StepPlan &sp = P.steps[chain[size_t(a)]];
+        const int64_t xsize = sp.x_is_lhs ? sp.lsize : sp.rsize;
+        const bool slow = sp.kern == Kern::AbsorbTma || sp.kern == Kern::AbsorbTc ||
+                          sp.kern == Kern::Absorb || sp.kern == Kern::Lanes ||
+                          sp.kern == Kern::AbsorbMma;
+        // ... and while its math stays under the HBM stream: K x N <= 8 (K + N) complex
+        // multiply-adds per column element moved (cfg2 494 / 536, K x N = 1024 against
+        // 80 / 64 elements: 3.6 -> 2.7 TB/s)
+        const int64_t K = int64_t(1) << sp.kbits.size(), N = int64_t(1) << sp.nbits.size();
+        const bool coalesced = e_in[size_t(a)] > 0.99 &&
+                               (e_out[size_t(a)] > 0.99 || 4 * sp.osize <= xsize) &&
+                               K * N <= 8 * (K + N);
+        g = (single_all || (slow && coalesced)) ? 0.5 * double(sp.lsize + sp.rsize + sp.osize)
+                                                : 0.0;
+        return sp.osize >= (int64_t(1) << min_bits) ? g - 1.0 : -1.0;
+      }
       return largest_mid >= (int64_t(1) << min_bits) ? g : -1.0;
     };
     std::vector<double> best(size_t(m) + 1, 0.0);  // best[i]: steps [i, m)
@@ -1589,7 +1661,8 @@ void plan_chains(stn_plan &P, bool jit) {
     for (int a = m - 1; a >= 0; --a) {
       best[size_t(a)] = best[size_t(a) + 1];  // step a alone
       cut[size_t(a)] = a;
-      for (int b = a + 1; b < m && fits[size_t(a)][size_t(b)]; ++b) {
+      for (int b = single ? a : a + 1; b < m && (b == a || fits[size_t(a)][size_t(b)]); ++b) {
+        if (!fits[size_t(a)][size_t(b)]) continue;
         const double g = gain(a, b);
         if (g > 0 && g + best[size_t(b) + 1] > best[size_t(a)]) {
           best[size_t(a)] = g + best[size_t(b) + 1];
@@ -1599,16 +1672,17 @@ void plan_chains(stn_plan &P, bool jit) {
     }
     for (int a = 0; a < m;) {
       const int b = cut[size_t(a)];
-      if (b > a) {
+      if (b > a || (single && b == a && best[size_t(a)] > best[size_t(a) + 1])) {
         std::vector<int> seg(chain.begin() + a, chain.begin() + b + 1);
         stn_plan::Sweep sw;
-        if (build_chain(P, seg, &sw, jit)) {
+        double ei = 0, eo = 0;
+        if (build_chain(P, seg, &sw, jit, &ei, &eo)) {
           const int id = int(P.sweeps.size());
           if (stn::debug_opt("sweep_debug")) {
             fprintf(stderr, "chain %d: steps", id);
             for (int q : seg) fprintf(stderr, " %d", q);
-            fprintf(stderr, " | li %d lo %d rows 2^%d\n", sw.cgeom.li, sw.cgeom.lo,
-                    __builtin_ctzll(uint64_t(sw.cgeom.rows)));
+            fprintf(stderr, " | li %d lo %d rows 2^%d | access efficiency in %.2f out %.2f\n",
+                    sw.cgeom.li, sw.cgeom.lo, __builtin_ctzll(uint64_t(sw.cgeom.rows)), ei, eo);
           }
           for (int st : seg) P.sweep_of_step[st] = id;
           P.sweeps.push_back(std::move(sw));
@@ -2572,7 +2646,10 @@ int auto_batch(const stn_plan &P, const Program &prog) {
   const int64_t per = std::max<int64_t>(prog.arena_elems, 1) * int64_t(P.esize);
   int64_t nb = P.max_batch > 0 ? int64_t(P.max_batch)
                                : (int64_t(256) << 20) / per;  // aim for >= 256 MiB per pass
-  return int(std::max<int64_t>(1, std::min<int64_t>(nb, 256)));
+  // batched launches put D x nbatch in gridDim.z (<= 65535)
+  int64_t max_d = 1;
+  for (const StepPlan &sp : P.steps) max_d = std::max<int64_t>(max_d, sp.gs.D);
+  return int(std::max<int64_t>(1, std::min<int64_t>({nb, 256, 65535 / max_d})));
 }
 
 // Lane `i` of the plan (created on first use; lane 0 runs on the caller's stream).
@@ -3358,8 +3435,44 @@ int stn_selftest_chain_jit(int exact, char *log, int32_t log_cap) {
       t->oout[i] = i * 128;
       t->widx[i] = t->widx[4 + i] = i;
     }
+    // the same chain with 32-byte loads and 16-byte stores (tile lines at the lowest
+    // positions of X and O)
+    stn::ChainGeom gv = g;
+    auto tv = std::make_unique<stn::ChainTables>(*t);
+    for (int i = 0; i < 4; ++i) {
+      tv->xin[i] = i;
+      tv->oout[i] = (i & 1) + (i >> 1) * 128;
+    }
+    // the same chain with lane / tile exchanges: position 0 is a lane bit, position 1 a
+    // tile line, on both sides
+    auto tx = std::make_unique<stn::ChainTables>(*t);
+    const int64_t lane_bits[5] = {1, 4, 8, 16, 32};
+    for (int l = 0; l < 32; ++l) {
+      tx->xl[l] = tx->ol[l] = 0;
+      for (int q = 0; q < 5; ++q)
+        if ((l >> q) & 1) tx->xl[l] = tx->ol[l] += lane_bits[q];
+    }
+    for (int i = 0; i < 4; ++i) tx->xin[i] = tx->oout[i] = (i & 1) * 2 + (i >> 1) * 64;
+    // a one-stage chain with a 64-value input tile (no software pipelining), K = 64, N = 2
+    stn::ChainGeom g1{};
+    auto t1 = std::make_unique<stn::ChainTables>();
+    memset(t1.get(), 0, sizeof(stn::ChainTables));
+    g1.n_stages = 1;
+    g1.li = 6;
+    g1.lo = 1;
+    g1.ma = 6;
+    g1.rows = 1 << 10;
+    g1.w_total = 128;
+    g1.st[0] = {0, 6, 1, 0, 64, 0, 0};
+    for (int k = 0; k < 64; ++k) t1->tab[k] = uint8_t(k);
+    t1->tab[64] = 0;
+    t1->tab[65] = 1;
+    for (int i = 0; i < 64; ++i) t1->xin[i] = i;
+    t1->oout[1] = 1;
+    for (int i = 0; i < 128; ++i) t1->widx[i] = i;
     std::string l;
-    const bool ok = stn::chain_jit_compile_only({{&g, t.get()}}, exact != 0, &l);
+    const bool ok = stn::chain_jit_compile_only(
+        {{&g, t.get()}, {&gv, tv.get()}, {&g, tx.get()}, {&g1, t1.get()}}, exact != 0, &l);
     if (log && log_cap > 0) {
       strncpy(log, l.c_str(), size_t(log_cap) - 1);
       log[log_cap - 1] = 0;

@@ -308,6 +308,32 @@ def test_stem_sweeps_are_bitwise_the_unfused_steps(name, monkeypatch):
     assert rel_err(run_subtask(fast, a, cache).value, truth) <= tol
 
 
+@pytest.mark.parametrize("name", ["cfg1_grid4x5_m14", "cfg2_grid5x6_m16"])
+@pytest.mark.parametrize("opts", ["chain_min_bits=0,chain_single=1",
+                                  "chain_min_bits=0,chain_single=1,chain_pf_log=3",
+                                  "chain_min_bits=0,chain_jit=0"])
+def test_fused_chains_everywhere_are_bitwise_the_reference(name, opts, monkeypatch):
+    """Fused stem chains on every run of stem absorbs that fits, including one-stage
+    chains (the specialised kernel in place of a single absorb, up to 64-value tiles),
+    without software pipelining, and on the table-driven kernel (chain_jit=0): EXACT
+    mode stays bitwise the reference's values, FAST mode within tolerance."""
+    from paper_2005_06787_b200 import build_branch_cache, run_subtask
+    monkeypatch.setenv("STN_DEBUG", opts)
+    asg, vals, _, _, _ = read_ref(name, "single")
+    plan = load(name, "single", "exact")
+    # the table-driven kernel's stage limits (K, N <= 8, K x N <= 16) fit no cfg1 run
+    assert plan.kernel_mix()["sweeps"] > 0 or (opts.endswith("chain_jit=0") and "cfg1" in name)
+    cache = build_branch_cache(plan)
+    for a, want in list(zip(asg, vals))[:2]:
+        r = run_subtask(plan, int(a), cache)
+        assert np.array_equal(bits(r.value.ravel()), bits(want)), (name, opts, int(a))
+    fast = load(name, "single", "fast")
+    cache = build_branch_cache(fast)
+    a, want = int(asg[0]), vals[0]
+    truth, tol = truth_and_tolerance(name, a, want)
+    assert rel_err(run_subtask(fast, a, cache).value, truth) <= tol
+
+
 def test_tensor_core_absorbs_run_and_meet_tolerance():
     """cfg2's K=N=64 and K=64,N=16 stem absorbs run on the tcgen05 direct
     absorb (absorb_mma.cu) in FAST mode; the slice stays within tolerance."""
