@@ -63,6 +63,7 @@ circuit cfg5_syc53_m20   sycamore53 20 6 33 none 0
 slice0 cfg3_syc53_m12 single
 slice0 cfg3_syc53_m12 double
 slice0 cfg4_syc53_m14 single
+slice0 cfg4_syc53_m14 double
 # cfg5: the reference cannot hold its 2^33 stems (Engine::gemm keeps 4 of them, 256 GiB)
 # and refuses every assignment (subtasks() overflows, scheme.hpp:33-37); its slices 0
 # and 1 come from the oracle port on a GPU box host: scripts/cfg5_parity.py ->
