@@ -164,6 +164,8 @@ struct TcArgs {
   int k_blocks;      // 2K / BK
   int two_n;         // 2N (row stride of C in floats)
   int n_tiles;       // 2N / BN
+  int m_groups;      // M / BM / cluster size (k_gemm_tc256m)
+  int gm;            // cluster m groups per raster band (k_gemm_tc256m)
 };
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -629,6 +631,195 @@ __global__ void __launch_bounds__(THREADS2, 1)
   }
 }
 
+// ---- 128 x 256 tiles, clusters of CL CTAs along M sharing the B tile ----------------
+// The 128 x 256 kernel is bound by L2 -> SM operand traffic (96 KiB per k-block for
+// ~1.5 M MACs). CL CTAs with consecutive m tiles and the same n tile form a cluster;
+// each TMA-loads 1/CL of the B'' hi/lo tile and multicasts it into every CTA of the
+// cluster, so a CTA pulls 32 KiB of A plus 64/CL KiB of B per k-block. A stage is
+// written by every CTA of the cluster, so its "empty" barrier waits for the MMA
+// commits of all CL CTAs (tcgen05.commit multicast).
+__device__ __forceinline__ void tma_load_3d_mc(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                               int x, int y, int z, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z),
+      "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit_mc(uint64_t *bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+template <int CL>
+__global__ void __launch_bounds__(THREADS2, 1)
+    k_gemm_tc256m(const __grid_constant__ CUtensorMap map_ahi,
+                  const __grid_constant__ CUtensorMap map_alo,
+                  const __grid_constant__ CUtensorMap map_bhi,
+                  const __grid_constant__ CUtensorMap map_blo, const TcArgs args) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *smem = reinterpret_cast<unsigned char *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES2 * STAGE2_BYTES);
+  uint64_t *empty = full + STAGES2;
+  uint64_t *tmem_full = empty + STAGES2;
+  uint64_t *tmem_empty = tmem_full + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int rank = int(cluster_rank());
+  // cluster index -> (m group, n tile), in bands of gm m groups: the CTAs resident at
+  // one time cover ~gm x 148 / (gm CL) tiles, so a k-block of A and of B'' is fetched
+  // from HBM once per band instead of once per m group
+  const int group = blockIdx.x / CL;
+  const int per_band = args.gm * args.n_tiles, band = group / per_band;
+  const int first = band * args.gm, gs = min(args.m_groups - first, args.gm);
+  const int r_in = group % per_band;
+  const int n_tile = r_in / gs, m_tile = (first + r_in % gs) * CL + rank;
+  const int bz = blockIdx.z;
+  const int slice = bz / args.D, d = bz % args.D;
+  const int za = args.a_batched ? bz : d;
+  const int zb = args.b_batched ? bz : d;
+  constexpr uint16_t kMask = uint16_t((1u << CL) - 1);
+  constexpr int kBRows = BN2 / CL;                    // B'' rows this CTA loads
+  constexpr int kBPart = B2_TILE_BYTES / CL;          // their bytes in the tile
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_ahi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_alo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_bhi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_blo)) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CL);  // the MMA commits of every CTA of the cluster
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();  // every CTA's barriers exist before any multicast lands
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < args.k_blocks; ++kb) {
+        const int s = kb % STAGES2;
+        const uint32_t phase = (kb / STAGES2) & 1;
+        mbar_wait(&empty[s], phase ^ 1);
+        unsigned char *st = smem + s * STAGE2_BYTES;
+        mbar_expect_tx(&full[s], STAGE2_BYTES);
+        const int kx = kb * BK;
+        tma_load_3d(st, &map_ahi, &full[s], kx, m_tile * BM, za);
+        tma_load_3d(st + A_TILE_BYTES, &map_alo, &full[s], kx, m_tile * BM, za);
+        const int brow = n_tile * BN2 + rank * kBRows;
+        tma_load_3d_mc(st + 2 * A_TILE_BYTES + rank * kBPart, &map_bhi, &full[s], kx, brow, zb,
+                       kMask);
+        tma_load_3d_mc(st + 2 * A_TILE_BYTES + B2_TILE_BYTES + rank * kBPart, &map_blo, &full[s],
+                       kx, brow, zb, kMask);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int kb = 0; kb < args.k_blocks; ++kb) {
+        const int s = kb % STAGES2;
+        const uint32_t phase = (kb / STAGES2) & 1;
+        const int chunk = kb / CHUNK, buf = chunk & 1;
+        const bool chunk_first = kb % CHUNK == 0;
+        const bool chunk_last = kb % CHUNK == CHUNK - 1 || kb == args.k_blocks - 1;
+        if (chunk_first) {
+          mbar_wait(&tmem_empty[buf], ((chunk >> 1) & 1) ^ 1);
+          tc_fence_after();
+        }
+        mbar_wait(&full[s], phase);
+        tc_fence_after();
+        const uint32_t st = smem_u32(smem + s * STAGE2_BYTES);
+        const uint64_t ahi = smem_desc_sw128(st);
+        const uint64_t alo = smem_desc_sw128(st + A_TILE_BYTES);
+        const uint64_t bhi = smem_desc_sw128(st + 2 * A_TILE_BYTES);
+        const uint64_t blo = smem_desc_sw128(st + 2 * A_TILE_BYTES + B2_TILE_BYTES);
+        const uint32_t tacc = tmem_base + uint32_t(buf * BN2);
+#pragma unroll
+        for (int k = 0; k < BK / UK; ++k) {
+          const uint64_t koff = uint64_t((k * UK * 4) >> 4);
+          const uint32_t acc0 = (!chunk_first || k > 0) ? 1u : 0u;
+          umma_tf32(tacc, ahi + koff, bhi + koff, kIdesc2, acc0);
+          umma_tf32(tacc, ahi + koff, blo + koff, kIdesc2, 1u);
+          umma_tf32(tacc, alo + koff, bhi + koff, kIdesc2, 1u);
+        }
+        umma_commit_mc(&empty[s], kMask);  // frees stage s in every CTA of the cluster
+        if (chunk_last) umma_commit(&tmem_full[buf]);
+      }
+    }
+  } else {
+    const int q4 = warp % 4, half = (warp - 2) / 4;
+    const int lane_base = 32 * q4;
+    const int row = m_tile * BM + lane_base + lane;
+    float acc[128];
+#pragma unroll
+    for (int c = 0; c < 128; ++c) acc[c] = 0.f;
+    const int n_chunks = (args.k_blocks + CHUNK - 1) / CHUNK;
+    for (int chunk = 0; chunk < n_chunks; ++chunk) {
+      const int buf = chunk & 1;
+      mbar_wait(&tmem_full[buf], (chunk >> 1) & 1);
+      tc_fence_after();
+      const uint32_t t0 =
+          tmem_base + (uint32_t(lane_base) << 16) + uint32_t(buf * BN2 + 128 * half);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(t0 + uint32_t(cc * 32), v);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc[cc * 32 + q] += __uint_as_float(v[q]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[buf]);
+    }
+    float *crow = args.c + int64_t(slice) * args.c_bs + int64_t(d) * args.c_ds +
+                  int64_t(row) * args.two_n + int64_t(n_tile) * BN2 + 128 * half;
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      reinterpret_cast<float4 *>(crow)[q] =
+          make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+  }
+  tc_fence_before();
+  cluster_sync();  // no CTA leaves while a peer may still multicast into it
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(512));
+  }
+}
+
 // ---- operand preparation --------------------------------------------------------
 // A (complex M x K per batch) -> hi/lo planes, same M x 2K real layout.
 __global__ void k_split_a(const float *__restrict__ a, int64_t a_bs, int64_t a_ds, int D,
@@ -773,11 +964,15 @@ cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspa
   const char *env_bk = stn::debug_opt("gemm_bk");
   const bool deep = wide && env_bk && std::atoi(env_bk) == 16;
   const int bk = deep ? BK3 : BK;
+  // clusters sharing the B tile (STN_DEBUG gemm_mc=1|2|4: cluster size, default 2)
+  const char *env_mc = stn::debug_opt("gemm_mc");
+  int cl = env_mc ? std::atoi(env_mc) : 2;
+  if (!wide || deep || (cl != 2 && cl != 4) || (s.M / BM) % cl != 0) cl = 1;
   CUtensorMap mah, mal, mbh, mbl;
   if (!make_map(&mah, ahi, 2 * s.K, s.M, nbA, BM, bk) ||
       !make_map(&mal, alo, 2 * s.K, s.M, nbA, BM, bk) ||
-      !make_map(&mbh, bhi, 2 * s.K, 2 * s.N, nbB, bn, bk) ||
-      !make_map(&mbl, blo, 2 * s.K, 2 * s.N, nbB, bn, bk))
+      !make_map(&mbh, bhi, 2 * s.K, 2 * s.N, nbB, bn / cl, bk) ||
+      !make_map(&mbl, blo, 2 * s.K, 2 * s.N, nbB, bn / cl, bk))
     return cudaErrorNotSupported;
   static bool attr_on[kMaxDevices] = {};
   bool &attr_set = attr_on[current_device()];
@@ -791,6 +986,12 @@ cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspa
     e = cudaFuncSetAttribute(k_gemm_tc256s, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(SMEM3_BYTES));
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_gemm_tc256m<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(SMEM2_BYTES));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_gemm_tc256m<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(SMEM2_BYTES));
+    if (e != cudaSuccess) return e;
     attr_set = true;
   }
   TcArgs args;
@@ -803,9 +1004,31 @@ cudaError_t launch_gemm_tc(const GemmShape &s, const BatchPtrs &p, void *workspa
   args.k_blocks = int(2 * s.K / bk);
   args.two_n = int(2 * s.N);
   args.n_tiles = int(2 * s.N / bn);
+  args.m_groups = int(s.M / BM / cl);
+  {
+    const char *env_gm = stn::debug_opt("gemm_gm");  // raster band height in m tiles
+    const int gm_tiles = env_gm ? std::atoi(env_gm) : 16;
+    args.gm = std::max(1, std::min(args.m_groups, gm_tiles / cl));
+  }
   dim3 grid(unsigned((2 * s.N / bn) * (s.M / BM)), 1, unsigned(s.D * p.nbatch));
   if (gemm_events) cudaEventRecord(gemm_events[0], stream);
-  if (deep)
+  if (cl > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(THREADS2);
+    cfg.dynamicSmemBytes = SMEM2_BYTES;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(cl);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cl == 4 ? cudaLaunchKernelEx(&cfg, k_gemm_tc256m<4>, mah, mal, mbh, mbl, args)
+                                  : cudaLaunchKernelEx(&cfg, k_gemm_tc256m<2>, mah, mal, mbh, mbl, args);
+    if (e != cudaSuccess) return e;
+  } else if (deep)
     k_gemm_tc256s<<<grid, THREADS2, SMEM3_BYTES, stream>>>(mah, mal, mbh, mbl, args);
   else if (wide)
     k_gemm_tc256<<<grid, THREADS2, SMEM2_BYTES, stream>>>(mah, mal, mbh, mbl, args);
