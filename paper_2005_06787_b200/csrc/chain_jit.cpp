@@ -87,6 +87,7 @@ struct Driver {
   CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                            unsigned, CUstream, void **, void **) = nullptr;
   CUresult (*FuncGetAttribute)(int *, CUfunction_attribute, CUfunction) = nullptr;
+  CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
   bool ok = false;
   static Driver &get() {
     static Driver d;
@@ -107,6 +108,7 @@ struct Driver {
     sym(ModuleGetFunction, "cuModuleGetFunction");
     sym(LaunchKernel, "cuLaunchKernel");
     sym(FuncGetAttribute, "cuFuncGetAttribute");
+    sym(FuncSetAttribute, "cuFuncSetAttribute");
     ok = ModuleLoadData && ModuleGetFunction && LaunchKernel;
   }
 };
@@ -140,6 +142,20 @@ __device__ __forceinline__ void ldcs4(const float2 *p, float2 &a, float2 &b) {
 }
 __device__ __forceinline__ void ldcs8(const float2 *p, float2 &a, float2 &b, float2 &c, float2 &d) {
   asm volatile("ld.global.cs.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(a.x), "=f"(a.y), "=f"(b.x), "=f"(b.y), "=f"(c.x), "=f"(c.y), "=f"(d.x),
+                 "=f"(d.y) : "l"(p));
+}
+// plain (L1-allocating) loads for X tiles that several rows re-read (expansion rows)
+__device__ __forceinline__ float2 ldg2(const float2 *p) {
+  float2 v; asm volatile("ld.global.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void ldg4(const float2 *p, float2 &a, float2 &b) {
+  asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(a.x), "=f"(a.y), "=f"(b.x), "=f"(b.y) : "l"(p));
+}
+__device__ __forceinline__ void ldg8(const float2 *p, float2 &a, float2 &b, float2 &c, float2 &d) {
+  asm volatile("ld.global.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                : "=f"(a.x), "=f"(a.y), "=f"(b.x), "=f"(b.y), "=f"(c.x), "=f"(c.y), "=f"(d.x),
                  "=f"(d.y) : "l"(p));
 }
@@ -196,7 +212,8 @@ int vec_bits(const int64_t *off, int n_log, int *s0, int *s1) {
 // `name(i)` is the register of element i; `v` the vector log (<= vmax).
 template <class Name>
 void emit_tile_io(std::ostringstream &s, bool load, const char *ptr, const int64_t *off,
-                  int n_log, int vmax, Name name, const char *indent, bool declare = true) {
+                  int n_log, int vmax, Name name, const char *indent, bool declare = true,
+                  const std::string &ld = "ldcs") {
   int s0, s1;
   int v = std::min(vec_bits(off, n_log, &s0, &s1), vmax);
   const int m0 = s0 >= 0 ? 1 << s0 : 0, m1 = s1 >= 0 ? 1 << s1 : 0;
@@ -206,26 +223,26 @@ void emit_tile_io(std::ostringstream &s, bool load, const char *ptr, const int64
     s << indent;
     if (v == 0) {
       if (load)
-        s << (declare ? "float2 " : "") << name(i) << " = ldcs2(" << ptr << " + " << off[i]
+        s << (declare ? "float2 " : "") << name(i) << " = " << ld << "2(" << ptr << " + " << off[i]
           << "LL);\n";
       else s << "stcs2(" << ptr << " + " << off[i] << "LL, " << name(i) << ");\n";
     } else if (v == 1) {
       if (load && !declare)
-        s << "ldcs4(" << ptr << " + " << off[i] << "LL, " << name(i) << ", " << name(i | m0)
+        s << ld << "4(" << ptr << " + " << off[i] << "LL, " << name(i) << ", " << name(i | m0)
           << ");\n";
       else if (load)
-        s << "float2 " << name(i) << ", " << name(i | m0) << "; ldcs4(" << ptr << " + " << off[i]
+        s << "float2 " << name(i) << ", " << name(i | m0) << "; " << ld << "4(" << ptr << " + " << off[i]
           << "LL, " << name(i) << ", " << name(i | m0) << ");\n";
       else
         s << "stcs4(" << ptr << " + " << off[i] << "LL, " << name(i) << ", " << name(i | m0)
           << ");\n";
     } else {
       if (load && !declare)
-        s << "ldcs8(" << ptr << " + " << off[i] << "LL, " << name(i) << ", " << name(i | m0)
+        s << ld << "8(" << ptr << " + " << off[i] << "LL, " << name(i) << ", " << name(i | m0)
           << ", " << name(i | m1) << ", " << name(i | m0 | m1) << ");\n";
       else if (load)
         s << "float2 " << name(i) << ", " << name(i | m0) << ", " << name(i | m1) << ", "
-          << name(i | m0 | m1) << "; ldcs8(" << ptr << " + " << off[i] << "LL, " << name(i)
+          << name(i | m0 | m1) << "; " << ld << "8(" << ptr << " + " << off[i] << "LL, " << name(i)
           << ", " << name(i | m0) << ", " << name(i | m1) << ", " << name(i | m0 | m1) << ");\n";
       else
         s << "stcs8(" << ptr << " + " << off[i] << "LL, " << name(i) << ", " << name(i | m0)
@@ -275,15 +292,16 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
   s << "extern \"C\" __global__ void __launch_bounds__(256) stn_chain_" << id
     << "(const JitArgs a) {\n"
     << "  __shared__ long long sxr[1024], sor[1024];\n"
-    << "  __shared__ float2 sw[" << (g.w_total > 0 ? g.w_total : 1) << "];\n"
+    << "  extern __shared__ float2 sw[];  // W of every stage (dynamic: up to 40 KiB)\n"
     << "  for (int i = threadIdx.x; i < 1024; i += 256) { sxr[i] = a.tabs[i]; sor[i] = a.tabs[1024 + i]; }\n"
     << "  const long long b = blockIdx.y;\n";
   // W: staged through the element offsets of the chain's tables (ChainTables::widx)
   s << "  const int *widx = (const int *)((const char *)a.tabs + "
     << offsetof(ChainTables, widx) << ");\n";
+  const std::string ld = g.n_exp > 0 ? "ldg" : "ldcs";  // expansion rows re-read X
   for (int st = 0; st < g.n_stages; ++st) {
     const ChainStage &cs = g.st[st];
-    const int kn = 1 << (cs.lk + cs.ln);
+    const int kn = 1 << (cs.lk + cs.ln + (st == 0 ? g.n_exp : 0));
     s << "  for (int i = threadIdx.x; i < " << kn << "; i += 256) sw[" << cs.w_smem
       << " + i] = a.w[" << st << "][b * a.w_bs[" << st << "] + widx[" << cs.w_off << " + i]];\n";
   }
@@ -307,21 +325,24 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
     for (int i = 0; i < ni; ++i) s << "  float2 n" << i << " = make_float2(0.f, 0.f);\n";
     auto nn = [](int i) { return "n" + std::to_string(i); };
     s << "  if (row < a.rows) {\n    const float2 *p = X + RX((unsigned)row) + xl;\n";
-    emit_tile_io(s, true, "p", xin, g.li, vmax, nn, "    ", false);
+    emit_tile_io(s, true, "p", xin, g.li, vmax, nn, "    ", false, ld);
     s << "  }\n  for (; row < a.rows; row += step) {\n";
     for (int i = 0; i < ni; ++i) s << "    float2 t0_" << i << " = n" << i << ";\n";
     if (xswap) emit_exchange(s, "t0_", g.li, xj, xs);
     s << "    { const long long nr = row + step;\n      if (nr < a.rows) {\n"
       << "        const float2 *p = X + RX((unsigned)nr) + xl;\n";
-    emit_tile_io(s, true, "p", xin, g.li, vmax, nn, "        ", false);
+    emit_tile_io(s, true, "p", xin, g.li, vmax, nn, "        ", false, ld);
     s << "      }\n    }\n";
   } else {  // large tiles: the other warps of the SM hide the load latency
     s << "  for (; row < a.rows; row += step) {\n"
       << "    const float2 *p = X + RX((unsigned)row) + xl;\n";
     emit_tile_io(s, true, "p", xin, g.li, vmax, [](int i) { return "t0_" + std::to_string(i); },
-                 "    ");
+                 "    ", true, ld);
     if (xswap) emit_exchange(s, "t0_", g.li, xj, xs);
   }
+  if (g.n_exp > 0)  // this row's W column block of stage 0 (expansion rows: low row bits)
+    s << "    const int wr = ((int)row & " << ((1 << g.n_exp) - 1) << ") * " << (1 << g.st[0].ln)
+      << ";\n";
   for (int st = 0; st < g.n_stages; ++st) {
     const ChainStage &cs = g.st[st];
     const int R = 1 << cs.lr, K = 1 << cs.lk, N = 1 << cs.ln;
@@ -331,9 +352,10 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
         s << "    float2 t" << st + 1 << "_" << out_slot << " = make_float2(0.f, 0.f);\n";
         for (int k = 0; k < K; ++k) {
           const int in_slot = kt.tab[cs.rd_off + r * K + k];
+          const bool ex = st == 0 && g.n_exp > 0;  // W block [k][e][n]
           s << "    t" << st + 1 << "_" << out_slot << " = " << cm << "(t" << st + 1 << "_"
-            << out_slot << ", t" << st << "_" << in_slot << ", sw[" << cs.w_smem + k * N + n
-            << "]);\n";
+            << out_slot << ", t" << st << "_" << in_slot << ", sw[" << (ex ? "wr + " : "")
+            << cs.w_smem + k * (N << (ex ? g.n_exp : 0)) + n << "]);\n";
         }
       }
   }
@@ -532,6 +554,10 @@ bool chain_jit_compile(const std::vector<ChainJitSpec> &chains, bool exact, int 
       if (log) *log = "cuModuleLoadData / cuModuleGetFunction failed";
       return false;
     }
+    // W lives in dynamic shared memory next to 16 KiB of row tables: opt in to 40 KiB
+    if (Driver::get().FuncSetAttribute)
+      Driver::get().FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                                     8 * kChainMaxW);
     g_fns[{srcs[i], device}] = f;
     (*fns)[i] = f;
     if (debug_opt("sweep_debug") && Driver::get().FuncGetAttribute) {
@@ -546,9 +572,12 @@ bool chain_jit_compile(const std::vector<ChainJitSpec> &chains, bool exact, int 
 }
 
 bool chain_prefetch(const ChainGeom &g) {
+  // the next row's input tile costs 2 registers per complex value: pipelined while
+  // both input tiles and the largest stage tile stay within ~200 registers (a 64-value
+  // output tile with an 8-value input, cfg5 1155, keeps it; 64-value inputs do not)
   const char *pf = debug_opt("chain_pf_log");
   const int pf_log = pf ? std::atoi(pf) : 5;
-  return g.li <= pf_log && g.lo <= pf_log;
+  return g.li <= pf_log && 4 * (1 << g.li) + 2 * (1 << g.ma) <= 200;
 }
 
 bool chain_swaps_allowed(const ChainGeom &g) {
@@ -609,8 +638,9 @@ cudaError_t chain_jit_launch(void *fn, const ChainGeom &g, const ChainTables *T,
   long long gx = 148LL * 8 / (p.nbatch > 0 ? p.nbatch : 1);
   if (gx > want) gx = want;
   if (gx < 1) gx = 1;
+  const unsigned smem = unsigned(8 * std::max(g.w_total, 1));
   const CUresult r = Driver::get().LaunchKernel(static_cast<CUfunction>(fn), unsigned(gx),
-                                                unsigned(p.nbatch), 1, 256, 1, 1, 0,
+                                                unsigned(p.nbatch), 1, 256, 1, 1, smem,
                                                 reinterpret_cast<CUstream>(stream), params,
                                                 nullptr);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;

@@ -193,7 +193,7 @@ constexpr int kChainMaxLog = 6;      // tile limit of the NVRTC-specialised kern
 constexpr int kChainMultiLog = 5;    // ... for chains of more than one stage
 constexpr int kChainTableLog = 4;    // tile limit of the table-driven kernel (kernels_chain.cu)
 constexpr int kChainMaxTab = 2 * kChainMaxStages * (1 << kChainMaxLog);  // rd + wr slots
-constexpr int kChainMaxW = kChainMaxStages * 256;
+constexpr int kChainMaxW = 5120;  // W elements of a chain (shared memory, 40 KiB)
 struct ChainStage {
   int lr, lk, ln;   // log2 of the stage's R (other active lines), K and N
   int rd_off;       // tab offset: slot of input (r, k), [R][K]
@@ -207,6 +207,7 @@ struct ChainGeom {
   int ma;                           // log2 of the largest tile (slots per column)
   int64_t rows;                     // rows of 32 columns (per batch)
   int w_total;                      // W elements of all stages
+  int n_exp;                        // expansion row bits of stage 0 (specialised kernel)
   ChainStage st[kChainMaxStages];
   const void *w[kChainMaxStages];   // filled at launch
   int64_t w_bs[kChainMaxStages];

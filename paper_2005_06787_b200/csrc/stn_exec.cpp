@@ -276,6 +276,12 @@ struct Op {
 
 struct Program {
   std::vector<Op> ops;
+  // intra-slice concurrency: small independent steps (branch-side work that feeds a
+  // later stem absorb) run on a second stream of the lane; wait_other[k] = the latest
+  // op of the other stream op k must follow (RAW / WAR / WAW on arena regions), -1 none
+  std::vector<char> side, need_event;
+  std::vector<int> wait_other;
+  bool has_side = false;
   int n_steps = 0;  // plan steps covered (a sweep op covers several)
   int64_t arena_elems = 0;  // per slice
   std::vector<int> slice_leaves;           // leaf node ids gathered per slice
@@ -308,9 +314,18 @@ struct ExecCtx {
   const void *w_prog = nullptr;  // last program run eagerly at full batch (pre-capture warm-up)
   int w_nb = 0;
   uint64_t w_epoch = 0;
+  // the side stream of the intra-slice schedule (Program::side) and its events
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  std::vector<cudaEvent_t> op_ev;
   ~ExecCtx() {
     if (graph) cudaGraphExecDestroy(graph);
     if (done) cudaEventDestroy(done);
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    for (cudaEvent_t e : op_ev)
+      if (e) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
     if (own_stream && st) cudaStreamDestroy(st);
   }
 };
@@ -1113,7 +1128,8 @@ bool chain_candidate(const stn_plan &P, const StepPlan &sp) {
   return P.precision == STN_SINGLE && !sp.d.is_branch && sp.has_bits &&
          (sp.kern == Kern::Absorb || sp.kern == Kern::AbsorbDirect || sp.kern == Kern::AbsorbTc ||
           sp.kern == Kern::AbsorbTma || sp.kern == Kern::AbsorbMma || sp.kern == Kern::Lanes) &&
-         int(sp.kbits.size()) <= stn::kChainMaxLog && int(sp.nbits.size()) <= stn::kChainMaxLog;
+         int(sp.kbits.size()) <= stn::kChainMaxLog &&
+         int(sp.nbits.size()) <= stn::kChainMaxLog + 10;  // growth steps: expansion rows
 }
 
 // Fused stem chain over steps [steps] (kernels.h ChainGeom). Follows every bit
@@ -1171,6 +1187,7 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
   std::vector<int> consumed_by(64, -1);  // line -> stage
   struct StageLines {
     std::vector<int> k, n;  // K lines (k bit order), N lines (n bit order)
+    std::vector<int> nw;    // W bit position of each N line
   };
   std::vector<StageLines> sl(static_cast<size_t>(ns));
   for (int si = 0; si < ns; ++si) {
@@ -1187,11 +1204,39 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
       if (n_lines >= 64) return false;
       nxt[size_t(op)] = n_lines;
       sl[size_t(si)].n.push_back(n_lines++);
+      sl[size_t(si)].nw.push_back(wp);
     }
     for (int v : nxt)
       if (v < 0) return false;
     pos2line.swap(nxt);
   }
+  // Expansion rows: a first stage that grows the stem (many N lines from W, e.g. cfg5
+  // 1605: 2^24 -> 2^32 elements) keeps the N lines no later stage consumes out of the
+  // tile; they become the lowest row bits (each row reads the same X tile, from L1 /
+  // L2, and a W column selected by its row). Specialised kernel only.
+  std::vector<int> exp_lines, exp_w;
+  const char *eo = stn::debug_opt("chain_exp");  // STN_DEBUG chain_exp=0: no expansion rows
+  if (jit && ns >= 2 && !(eo && std::atoi(eo) == 0)) {
+    StageLines &z = sl[0];
+    std::vector<int> keep, keep_w;
+    for (size_t j = 0; j < z.n.size(); ++j)
+      if (consumed_by[size_t(z.n[j])] < 0) {
+        exp_lines.push_back(z.n[j]);
+        exp_w.push_back(z.nw[j]);
+      } else {
+        keep.push_back(z.n[j]);
+        keep_w.push_back(z.nw[j]);
+      }
+    if (exp_lines.size() >= 3 && int(z.n.size()) > 2) {
+      z.n = keep;
+      z.nw = keep_w;
+    } else {
+      exp_lines.clear();
+      exp_w.clear();
+    }
+  }
+  const int n_exp = int(exp_lines.size());
+  if (n_exp > 10) return false;  // W column block in shared memory
   const std::vector<int> &final_pos2line = pos2line;
   std::vector<int> opos_of(static_cast<size_t>(n_lines), -1);
   for (int op = 0; op < int(final_pos2line.size()); ++op) opos_of[size_t(final_pos2line[size_t(op)])] = op;
@@ -1249,8 +1294,9 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
     cs.lr = lr;
     cs.lk = lk;
     cs.ln = ln_;
+    const int le = si == 0 ? n_exp : 0;  // expansion bits of this stage's W block
     if (tab + (1 << lr) * ((1 << lk) + (1 << ln_)) > stn::kChainMaxTab ||
-        widx + (1 << (lk + ln_)) > stn::kChainMaxW)
+        widx + (1 << (lk + ln_ + le)) > stn::kChainMaxW)
       return false;
     cs.rd_off = tab;
     for (int r = 0; r < (1 << lr); ++r)
@@ -1267,16 +1313,20 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
       for (int n = 0; n < (1 << ln_); ++n) T->tab[tab++] = uint8_t(r | (n << lr));
     cs.w_off = widx;
     cs.w_smem = wsm;
+    // W block [k][e][n]: e = expansion column (row bits), n = tile N index
     for (int k = 0; k < (1 << lk); ++k)
-      for (int n = 0; n < (1 << ln_); ++n) {
-        int32_t off = 0;
-        for (int j = 0; j < lk; ++j)
-          if ((k >> j) & 1) off += int32_t(1) << sp.kbits[size_t(j)].second;
-        for (int j = 0; j < ln_; ++j)
-          if ((n >> j) & 1) off += int32_t(1) << sp.nbits[size_t(j)].second;
-        T->widx[widx++] = off;
-      }
-    wsm += 1 << (lk + ln_);
+      for (int e = 0; e < (1 << le); ++e)
+        for (int n = 0; n < (1 << ln_); ++n) {
+          int32_t off = 0;
+          for (int j = 0; j < lk; ++j)
+            if ((k >> j) & 1) off += int32_t(1) << sp.kbits[size_t(j)].second;
+          for (int j = 0; j < ln_; ++j)
+            if ((n >> j) & 1) off += int32_t(1) << st.nw[size_t(j)];
+          for (int j = 0; j < le; ++j)
+            if ((e >> j) & 1) off += int32_t(1) << exp_w[size_t(j)];
+          T->widx[widx++] = off;
+        }
+    wsm += 1 << (lk + ln_ + le);
     // next layout: R lines, then the stage's N lines
     L = R;
     L.insert(L.end(), st.n.begin(), st.n.end());
@@ -1288,9 +1338,15 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
     for (int i = 0; i < g.lo; ++i)
       if ((e >> i) & 1) T->oout[e] += int64_t(1) << opos_of[size_t(L[size_t(i)])];
   g.w_total = wsm;
-  // passive lines: the 5 lowest X positions are the lanes, the rest the rows
-  const int rb = int(passive.size()) - 5;
+  // passive lines: the 5 lowest X positions are the lanes, the rest the rows (after
+  // the expansion lines, which are the lowest row bits and have no X offset)
+  for (int ln : exp_lines)
+    if (opos_of[size_t(ln)] < 0) return false;
+  std::vector<int> row_lines = exp_lines;
+  row_lines.insert(row_lines.end(), passive.begin() + 5, passive.end());
+  const int rb = int(row_lines.size());
   if (rb > 32) return false;
+  g.n_exp = n_exp;
   for (int l = 0; l < 32; ++l)
     for (int j = 0; j < 5; ++j)
       if ((l >> j) & 1) {
@@ -1301,8 +1357,8 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
     for (int v = 0; v < 256; ++v)
       for (int j = 0; j < 8; ++j)
         if (((v >> j) & 1) && 8 * c + j < rb) {
-          const int ln = passive[size_t(5 + 8 * c + j)];
-          T->xr[c][v] += int64_t(1) << ln;
+          const int ln = row_lines[size_t(8 * c + j)];
+          if (ln < xr0) T->xr[c][v] += int64_t(1) << ln;  // expansion lines: not in X
           T->orow[c][v] += int64_t(1) << opos_of[size_t(ln)];
         }
   g.rows = int64_t(1) << rb;
@@ -1610,12 +1666,14 @@ void plan_chains(stn_plan &P, bool jit) {
     // whose largest intermediate has >= 2^min_bits elements are fused.
     const int m = int(chain.size());
     std::vector<std::vector<char>> fits(size_t(m), std::vector<char>(size_t(m), 0));
-    std::vector<double> e_in(size_t(m), 0.0), e_out(size_t(m), 0.0);  // one-stage chains
+    // warp-access sector efficiency of each segment's stem input and output
+    std::vector<std::vector<double>> e_in(size_t(m), std::vector<double>(size_t(m), 0.0));
+    std::vector<std::vector<double>> e_out = e_in;
     for (int a = 0; a < m; ++a)
       for (int b = single ? a : a + 1; b < m; ++b) {
         std::vector<int> seg(chain.begin() + a, chain.begin() + b + 1);
-        if (!build_chain(P, seg, nullptr, jit, b == a ? &e_in[size_t(a)] : nullptr,
-                         b == a ? &e_out[size_t(a)] : nullptr)) {
+        if (!build_chain(P, seg, nullptr, jit, &e_in[size_t(a)][size_t(b)],
+                         &e_out[size_t(a)][size_t(b)])) {
           if (b == a) continue;
           break;  // longer ones from a fail too
         }
@@ -1647,13 +1705,22 @@ void plan_chains(stn_plan &P, bool jit) {
         // multiply-adds per column element moved (cfg2 494 / 536, K x N = 1024 against
         // 80 / 64 elements: 3.6 -> 2.7 TB/s)
         const int64_t K = int64_t(1) << sp.kbits.size(), N = int64_t(1) << sp.nbits.size();
-        const bool coalesced = e_in[size_t(a)] > 0.99 &&
-                               (e_out[size_t(a)] > 0.99 || 4 * sp.osize <= xsize) &&
+        const bool coalesced = e_in[size_t(a)][size_t(a)] > 0.99 &&
+                               (e_out[size_t(a)][size_t(a)] > 0.99 || 4 * sp.osize <= xsize) &&
                                K * N <= 8 * (K + N);
         g = (single_all || (slow && coalesced)) ? 0.5 * double(sp.lsize + sp.rsize + sp.osize)
                                                 : 0.0;
         return sp.osize >= (int64_t(1) << min_bits) ? g - 1.0 : -1.0;
       }
+      // half-sector warp accesses on the chain's stem input / output cost about a second
+      // pass over those bytes (cfg5 1155-1161, output at 0.5: 13.1 ms unfused, 18.8 fused)
+      const StepPlan &s0 = P.steps[chain[size_t(a)]], &s1 = P.steps[chain[size_t(b)]];
+      const double xin = double(s0.x_is_lhs ? s0.lsize : s0.rsize);
+      g -= (1.0 / std::max(e_in[size_t(a)][size_t(b)], 0.25) - 1.0) * xin;
+      g -= (1.0 / std::max(e_out[size_t(a)][size_t(b)], 0.25) - 1.0) * double(s1.osize);
+      // a growth step fused as expansion rows re-reads its stem operand once per row
+      // group (8 warps of a CTA share it in L1): costly once that operand outgrows L2
+      if (b > a && double(s0.osize) > 4.0 * xin && xin > double(int64_t(1) << 24)) g -= 8.0 * xin;
       return largest_mid >= (int64_t(1) << min_bits) ? g : -1.0;
     };
     std::vector<double> best(size_t(m) + 1, 0.0);  // best[i]: steps [i, m)
@@ -1853,11 +1920,28 @@ void build_program(stn_plan &P, Program &prog, int which /*0 build, 1 cache, 2 n
     }
     return r;
   };
+  // side-stream candidates (per-slice programs): small steps on kernels that use no
+  // lane workspace; their outputs live from the start of the program so that no stem
+  // step's buffer shares their memory (no write-after-read waits between the streams).
+  // Off unless STN_DEBUG side=1: measured on B200 it neither helps nor hurts (cfg5
+  // 122.1 / 122.3, cfg4 51.1 / 51.4, cfg2 7.52 / 7.48 ms per slice without / with)
+  const char *side_opt = stn::debug_opt("side");
+  const bool side_on = which != 0 && side_opt && std::atoi(side_opt) != 0;
+  auto side_ok = [&](int u) {
+    if (!side_on || unit_sweep[u] >= 0) return false;
+    const StepPlan &sp = P.steps[units[u].back()];
+    const bool kern_ok = sp.kern == Kern::Generic || sp.kern == Kern::Outer ||
+                         sp.kern == Kern::AbsorbDirect || sp.kern == Kern::Lanes ||
+                         sp.kern == Kern::Absorb;
+    return kern_ok && sp.osize <= (int64_t(1) << 22);
+  };
+  prog.side.assign(units.size(), 0);
   for (int u = 0; u < int(units.size()); ++u) {
     const StepPlan &last = P.steps[units[u].back()];
     Op op;
     op.step = units[u].back();
     op.sweep = unit_sweep[u];
+    prog.side[size_t(u)] = side_ok(u) ? 1 : 0;
     if (op.sweep >= 0) {
       const StepPlan &first = P.steps[units[u].front()];
       op.a = make_input(first.x_is_lhs ? first.d.lhs : first.d.rhs);
@@ -1876,7 +1960,8 @@ void build_program(stn_plan &P, Program &prog, int which /*0 build, 1 cache, 2 n
       op.out.off = P.cache_off.at(last.d.node);
     } else {
       op.out.kind = Src::Arena;
-      out_off_ptr[last.d.node] = new_item(last.osize, u, end_of(last.d.node));
+      out_off_ptr[last.d.node] =
+          new_item(last.osize, prog.side[size_t(u)] ? -1 : u, end_of(last.d.node));
     }
     prog.ops.push_back(op);
     for (int st : units[u]) {  // SubtaskResult bookkeeping counts every step
@@ -1943,6 +2028,47 @@ void build_program(stn_plan &P, Program &prog, int which /*0 build, 1 cache, 2 n
     op.scr_c = scr[k][2] ? *scr[k][2] : -1;
   }
   for (int node : prog.slice_leaves) prog.slice_leaf_off[node] = *leaf_off_ptr.at(node);
+  // cross-stream ordering of the side-stream schedule
+  {
+    const size_t n_ops = prog.ops.size();
+    prog.wait_other.assign(n_ops, -1);
+    prog.need_event.assign(n_ops, 0);
+    for (size_t k = 0; k < n_ops; ++k) prog.has_side = prog.has_side || prog.side[k];
+    if (prog.has_side) {
+      using Reg = std::pair<int64_t, int64_t>;
+      std::vector<std::vector<Reg>> rd(n_ops), wr(n_ops);
+      auto region = [&](const Ref &r, std::vector<Reg> &v) {
+        if (r.kind == Src::Arena || r.kind == Src::SliceLeaf)
+          v.push_back({r.off, r.off + aligned(r.size)});
+      };
+      for (size_t k = 0; k < n_ops; ++k) {
+        const Op &op = prog.ops[k];
+        region(op.a, rd[k]);
+        if (op.sweep < 0) region(op.b, rd[k]);
+        for (const Ref &w : op.wrefs) region(w, rd[k]);
+        region(op.out, wr[k]);
+        const StepPlan &sp = P.steps[op.step];
+        if (op.scr_a >= 0) wr[k].push_back({op.scr_a, op.scr_a + aligned(sp.gemm_swap ? sp.rsize : sp.lsize)});
+        if (op.scr_b >= 0) wr[k].push_back({op.scr_b, op.scr_b + aligned(sp.gemm_swap ? sp.lsize : sp.rsize)});
+        if (op.scr_c >= 0) wr[k].push_back({op.scr_c, op.scr_c + aligned(sp.osize)});
+      }
+      auto meet = [](const std::vector<Reg> &x, const std::vector<Reg> &y) {
+        for (const Reg &a : x)
+          for (const Reg &b : y)
+            if (a.first < b.second && b.first < a.second) return true;
+        return false;
+      };
+      for (size_t k = 0; k < n_ops; ++k)
+        for (size_t j = k; j-- > 0;) {
+          if (prog.side[j] == prog.side[k]) continue;
+          if (meet(wr[j], rd[k]) || meet(rd[j], wr[k]) || meet(wr[j], wr[k])) {
+            prog.wait_other[k] = int(j);
+            prog.need_event[j] = 1;
+            break;
+          }
+        }
+    }
+  }
   // root
   prog.has_root = which != 0;
   if (prog.has_root) {
@@ -2683,11 +2809,34 @@ void batch_kernels(stn_plan &P, Program &prog, const stn_cache *cache, int n, cu
                  "leaf gather");
     prof.done(STN_KERNEL_LEAF, double(prog.table.total_out) * n * (16 + P.esize), 0);
   }
-  for (const Op &op : prog.ops) {
+  // side stream: small independent steps overlap the stem steps (not while profiling,
+  // which times every step on one stream)
+  const bool two = prog.has_side && !P.profiling;
+  if (two) {
+    if (!L.side) cuda_check(cudaStreamCreateWithFlags(&L.side, cudaStreamNonBlocking), "side stream");
+    for (cudaEvent_t *e : {&L.fork, &L.join})
+      if (!*e) cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "side event");
+    if (L.op_ev.size() < prog.ops.size()) L.op_ev.resize(prog.ops.size(), nullptr);
+    for (size_t k = 0; k < prog.ops.size(); ++k)
+      if (prog.need_event[k] && !L.op_ev[k])
+        cuda_check(cudaEventCreateWithFlags(&L.op_ev[k], cudaEventDisableTiming), "op event");
+    cuda_check(cudaEventRecord(L.fork, st), "fork");
+    cuda_check(cudaStreamWaitEvent(L.side, L.fork, 0), "fork wait");
+  }
+  for (size_t k = 0; k < prog.ops.size(); ++k) {
+    const Op &op = prog.ops[k];
+    cudaStream_t s = two && prog.side[k] ? L.side : st;
+    if (two && prog.wait_other[k] >= 0)
+      cuda_check(cudaStreamWaitEvent(s, L.op_ev[size_t(prog.wait_other[k])], 0), "op wait");
     if (P.precision == STN_SINGLE)
-      launch_op<float>(P, op, cache, n, st);
+      launch_op<float>(P, op, cache, n, s);
     else
-      launch_op<double>(P, op, cache, n, st);
+      launch_op<double>(P, op, cache, n, s);
+    if (two && prog.need_event[k]) cuda_check(cudaEventRecord(L.op_ev[k], s), "op event");
+  }
+  if (two) {
+    cuda_check(cudaEventRecord(L.join, L.side), "join");
+    cuda_check(cudaStreamWaitEvent(st, L.join, 0), "join wait");
   }
   if (prog.has_root && (acc || per_slice)) {
     ProfScope prof(P, st);
@@ -3470,9 +3619,16 @@ int stn_selftest_chain_jit(int exact, char *log, int32_t log_cap) {
     for (int i = 0; i < 64; ++i) t1->xin[i] = i;
     t1->oout[1] = 1;
     for (int i = 0; i < 128; ++i) t1->widx[i] = i;
+    // the two-stage chain with 3 expansion row bits on its first stage (W block [k][e][n])
+    stn::ChainGeom ge = g;
+    ge.n_exp = 3;
+    ge.st[1].w_smem = 32;
+    ge.st[1].w_off = 32;
+    ge.w_total = 36;
     std::string l;
     const bool ok = stn::chain_jit_compile_only(
-        {{&g, t.get()}, {&gv, tv.get()}, {&g, tx.get()}, {&g1, t1.get()}}, exact != 0, &l);
+        {{&g, t.get()}, {&gv, tv.get()}, {&g, tx.get()}, {&g1, t1.get()}, {&ge, t.get()}},
+        exact != 0, &l);
     if (log && log_cap > 0) {
       strncpy(log, l.c_str(), size_t(log_cap) - 1);
       log[log_cap - 1] = 0;
