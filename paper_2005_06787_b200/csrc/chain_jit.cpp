@@ -298,7 +298,7 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
   // W: staged through the element offsets of the chain's tables (ChainTables::widx)
   s << "  const int *widx = (const int *)((const char *)a.tabs + "
     << offsetof(ChainTables, widx) << ");\n";
-  const std::string ld = g.n_exp > 0 ? "ldg" : "ldcs";  // expansion rows re-read X
+  const std::string ld = "ldcs";
   for (int st = 0; st < g.n_stages; ++st) {
     const ChainStage &cs = g.st[st];
     const int kn = 1 << (cs.lk + cs.ln + (st == 0 ? g.n_exp : 0));
@@ -321,7 +321,19 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
     << "  long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);\n"
     << "#define RX(r) (sxr[(r) & 255] + sxr[256 + (((r) >> 8) & 255)] + sxr[512 + (((r) >> 16) & 255)] + sxr[768 + (((r) >> 24) & 255)])\n"
     << "#define RO(r) (sor[(r) & 255] + sor[256 + (((r) >> 8) & 255)] + sor[512 + (((r) >> 16) & 255)] + sor[768 + (((r) >> 24) & 255)])\n";
-  if (prefetch) {
+  if (g.n_exp > 0) {
+    // expansion rows: a warp loads its X tile once per group of 2^n_exp rows (they share
+    // it) and runs the chain for every expansion column of the group in an inner loop
+    s << "  const long long groups = a.rows >> " << g.n_exp << ";\n"
+      << "  for (long long grp = row; grp < groups; grp += step) {\n"
+      << "    const float2 *p = X + RX((unsigned)(grp << " << g.n_exp << ")) + xl;\n";
+    emit_tile_io(s, true, "p", xin, g.li, vmax, [](int i) { return "t0_" + std::to_string(i); },
+                 "    ", true);
+    if (xswap) emit_exchange(s, "t0_", g.li, xj, xs);
+    s << "  for (int e = 0; e < " << (1 << g.n_exp) << "; ++e) {\n"
+      << "    const long long row = (grp << " << g.n_exp << ") | e;\n"
+      << "    const int wr = e * " << (1 << g.st[0].ln) << ";  // W column block of stage 0\n";
+  } else if (prefetch) {
     for (int i = 0; i < ni; ++i) s << "  float2 n" << i << " = make_float2(0.f, 0.f);\n";
     auto nn = [](int i) { return "n" + std::to_string(i); };
     s << "  if (row < a.rows) {\n    const float2 *p = X + RX((unsigned)row) + xl;\n";
@@ -340,9 +352,7 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
                  "    ", true, ld);
     if (xswap) emit_exchange(s, "t0_", g.li, xj, xs);
   }
-  if (g.n_exp > 0)  // this row's W column block of stage 0 (expansion rows: low row bits)
-    s << "    const int wr = ((int)row & " << ((1 << g.n_exp) - 1) << ") * " << (1 << g.st[0].ln)
-      << ";\n";
+
   for (int st = 0; st < g.n_stages; ++st) {
     const ChainStage &cs = g.st[st];
     const int R = 1 << cs.lr, K = 1 << cs.lk, N = 1 << cs.ln;
@@ -365,7 +375,7 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
   emit_tile_io(s, false, "q", oout, g.lo, vmax,
                [last](int j) { return "t" + std::to_string(last) + "_" + std::to_string(j); },
                "    ");
-  s << "  }\n#undef RX\n#undef RO\n}\n";
+  s << (g.n_exp > 0 ? "  }\n  }\n" : "  }\n") << "#undef RX\n#undef RO\n}\n";
   return s.str();
 }
 
@@ -486,8 +496,10 @@ bool chain_jit_compile_only(const std::vector<ChainJitSpec> &chains, bool exact,
 }
 
 bool chain_jit_compile(const std::vector<ChainJitSpec> &chains, bool exact, int device,
-                       std::vector<void *> *fns, std::string *log) {
+                       std::vector<void *> *fns, std::string *log,
+                       std::vector<int> *local_bytes) {
   fns->assign(chains.size(), nullptr);
+  if (local_bytes) local_bytes->assign(chains.size(), 0);
   if (chains.empty()) return true;
   if (!chain_jit_available()) {
     if (log) *log = "NVRTC or the driver module API is not available";
@@ -541,7 +553,12 @@ bool chain_jit_compile(const std::vector<ChainJitSpec> &chains, bool exact, int 
   }
   std::lock_guard<std::mutex> lk(g_mu);
   for (size_t i = 0; i < chains.size(); ++i) {
-    if (have[i] == 2) continue;
+    if (have[i] == 2) {
+      if (local_bytes && Driver::get().FuncGetAttribute)
+        Driver::get().FuncGetAttribute(&(*local_bytes)[i], CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES,
+                                       static_cast<CUfunction>((*fns)[i]));
+      continue;
+    }
     if (!ok[i]) {
       if (log) *log = logs[i];
       return false;
@@ -560,6 +577,8 @@ bool chain_jit_compile(const std::vector<ChainJitSpec> &chains, bool exact, int 
                                      8 * kChainMaxW);
     g_fns[{srcs[i], device}] = f;
     (*fns)[i] = f;
+    if (local_bytes && Driver::get().FuncGetAttribute)
+      Driver::get().FuncGetAttribute(&(*local_bytes)[i], CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, f);
     if (debug_opt("sweep_debug") && Driver::get().FuncGetAttribute) {
       int regs = 0, local = 0;
       Driver::get().FuncGetAttribute(&regs, CU_FUNC_ATTRIBUTE_NUM_REGS, f);

@@ -20,7 +20,8 @@ int chain_vec_max();
 // fns[i] receives chain i's CUfunction. False (and *log) if NVRTC is unavailable or
 // the compilation failed: the chains then run on kernels_chain.cu.
 bool chain_jit_compile(const std::vector<ChainJitSpec> &chains, bool exact, int device,
-                       std::vector<void *> *fns, std::string *log);
+                       std::vector<void *> *fns, std::string *log,
+                       std::vector<int> *local_bytes = nullptr);
 // NVRTC compilation alone (no device needed): the CPU check that generated code builds.
 bool chain_jit_compile_only(const std::vector<ChainJitSpec> &chains, bool exact,
                             std::string *log);

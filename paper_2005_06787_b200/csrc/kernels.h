@@ -190,7 +190,8 @@ cudaError_t launch_absorb_direct(const DirectGeom &g, const BatchPtrs &p, bool e
 // active tile of its column (<= 2^kChainMaxLog complex values).
 constexpr int kChainMaxStages = 8;
 constexpr int kChainMaxLog = 6;      // tile limit of the NVRTC-specialised kernels (chain_jit.cpp)
-constexpr int kChainMultiLog = 5;    // ... for chains of more than one stage
+constexpr int kChainMultiLog = 6;    // ... for chains of more than one stage (spilling
+                                     // kernels are re-planned: stn_exec.cpp plan_chains)
 constexpr int kChainTableLog = 4;    // tile limit of the table-driven kernel (kernels_chain.cu)
 constexpr int kChainMaxTab = 2 * kChainMaxStages * (1 << kChainMaxLog);  // rd + wr slots
 constexpr int kChainMaxW = 5120;  // W elements of a chain (shared memory, 40 KiB)

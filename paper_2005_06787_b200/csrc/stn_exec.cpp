@@ -380,6 +380,7 @@ struct stn_plan {
   };
   std::vector<Sweep> sweeps;
   std::map<int, int> sweep_of_step;
+  std::set<std::vector<int>> chain_banned;  // segments whose specialised kernel spilled
   // programs
   Program build, with_cache, no_cache;
   std::map<int, int64_t> cache_off;  // node -> element offset in cache storage
@@ -1172,12 +1173,24 @@ double access_efficiency(const int64_t *lane_off_in, const int64_t *elem_off_in,
 
 bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Sweep *out,
                  bool jit, double *eff_in, double *eff_out) {
+  // STN_DEBUG chain_why=<step>: why segments starting at that step do not fit
+  const char *why = stn::debug_opt("chain_why");
+  const bool trace = why && !steps.empty() && std::atoi(why) == steps.front();
+#define CHAIN_FAIL(at)                                                                  \
+  do {                                                                                  \
+    if (trace) fprintf(stderr, "chain from %d (%zu steps): no fit at stn_exec.cpp:%d\n", \
+                       steps.front(), steps.size(), at);                                \
+    return false;                                                                       \
+  } while (0)
   // the NVRTC-specialised kernel holds up to 32 values per column in registers (64 in a
   // one-stage chain); the table-driven one 16 in shared memory, K, N <= 8 and K x N <= 16
   // per stage
   const int ns = int(steps.size());
-  const int max_log = !jit ? stn::kChainTableLog : ns == 1 ? stn::kChainMaxLog : stn::kChainMultiLog;
-  if (ns < 1 || ns > stn::kChainMaxStages || (ns == 1 && !jit)) return false;
+  const char *ml = stn::debug_opt("chain_multi_log");  // tile limit of multi-stage chains (6)
+  const int multi_log = ml ? std::max(2, std::min(stn::kChainMaxLog, std::atoi(ml)))
+                           : stn::kChainMultiLog;
+  const int max_log = !jit ? stn::kChainTableLog : ns == 1 ? stn::kChainMaxLog : multi_log;
+  if (ns < 1 || ns > stn::kChainMaxStages || (ns == 1 && !jit)) CHAIN_FAIL(1180);
   const StepPlan &s0 = P.steps[steps[0]];
   const int xr0 = s0.xr;
   // line bookkeeping
@@ -1192,7 +1205,7 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
   std::vector<StageLines> sl(static_cast<size_t>(ns));
   for (int si = 0; si < ns; ++si) {
     const StepPlan &sp = P.steps[steps[si]];
-    if (int(pos2line.size()) != sp.xr) return false;
+    if (int(pos2line.size()) != sp.xr) CHAIN_FAIL(1195);
     for (auto &[xp, wp] : sp.kbits) {
       const int ln = pos2line[size_t(xp)];
       sl[size_t(si)].k.push_back(ln);
@@ -1201,13 +1214,13 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
     std::vector<int> nxt(static_cast<size_t>(sp.orank_), -1);
     for (auto &[xp, op] : sp.mbits) nxt[size_t(op)] = pos2line[size_t(xp)];
     for (auto &[op, wp] : sp.nbits) {
-      if (n_lines >= 64) return false;
+      if (n_lines >= 64) CHAIN_FAIL(1204);
       nxt[size_t(op)] = n_lines;
       sl[size_t(si)].n.push_back(n_lines++);
       sl[size_t(si)].nw.push_back(wp);
     }
     for (int v : nxt)
-      if (v < 0) return false;
+      if (v < 0) CHAIN_FAIL(1210);
     pos2line.swap(nxt);
   }
   // Expansion rows: a first stage that grows the stem (many N lines from W, e.g. cfg5
@@ -1236,7 +1249,7 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
     }
   }
   const int n_exp = int(exp_lines.size());
-  if (n_exp > 10) return false;  // W column block in shared memory
+  if (n_exp > 10) CHAIN_FAIL(1239);  // W column block in shared memory
   const std::vector<int> &final_pos2line = pos2line;
   std::vector<int> opos_of(static_cast<size_t>(n_lines), -1);
   for (int op = 0; op < int(final_pos2line.size()); ++op) opos_of[size_t(final_pos2line[size_t(op)])] = op;
@@ -1244,7 +1257,7 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
   std::vector<int> L;
   std::vector<int> passive;  // X lines never consumed
   for (int xp = 0; xp < xr0; ++xp) (consumed_by[size_t(xp)] >= 0 ? L : passive).push_back(xp);
-  if (int(L.size()) > max_log || passive.size() < 5) return false;
+  if (int(L.size()) > max_log || passive.size() < 5) CHAIN_FAIL(1247);
   // largest tile along the chain (alive active lines at a stage's input or output)
   int ma = int(L.size());
   {
@@ -1263,7 +1276,7 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
   passive.erase(passive.begin() + 5, passive.begin() + 5 + extra);
   const int li = int(L.size());
   for (int ln : passive)
-    if (opos_of[size_t(ln)] < 0) return false;
+    if (opos_of[size_t(ln)] < 0) CHAIN_FAIL(1266);
   auto T = std::make_unique<stn::ChainTables>();
   memset(T.get(), 0, sizeof(stn::ChainTables));
   stn::ChainGeom g{};
@@ -1280,13 +1293,13 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
     for (int ln : L)
       if (std::find(st.k.begin(), st.k.end(), ln) == st.k.end()) R.push_back(ln);
     const int lr = int(R.size()), lk = int(st.k.size()), ln_ = int(st.n.size());
-    if (lr + lk > max_log || lr + ln_ > max_log) return false;
+    if (lr + lk > max_log || lr + ln_ > max_log) CHAIN_FAIL(1283);
     // table kernel: the stage shapes it instantiates (K, N <= 8), and K x N <= 16 (with
     // larger ones its per-column math is slower than the separate HBM-rate steps: cfg5
     // chain 1613-1614, K x N = 32, 41 ms fused vs 37 ms unfused, measured on B200)
-    if (!jit && (lk > 3 || ln_ > 3 || lk + ln_ > 4)) return false;
+    if (!jit && (lk > 3 || ln_ > 3 || lk + ln_ > 4)) CHAIN_FAIL(1287);
     g.ma = std::max(g.ma, std::max(lr + lk, lr + ln_));
-    if (int(R.size()) + lk != int(L.size())) return false;  // a K line not in the tile
+    if (int(R.size()) + lk != int(L.size())) CHAIN_FAIL(1289);  // a K line not in the tile
     auto slot_in = [&](int ln) {
       return int(std::find(L.begin(), L.end(), ln) - L.begin());
     };
@@ -1297,7 +1310,7 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
     const int le = si == 0 ? n_exp : 0;  // expansion bits of this stage's W block
     if (tab + (1 << lr) * ((1 << lk) + (1 << ln_)) > stn::kChainMaxTab ||
         widx + (1 << (lk + ln_ + le)) > stn::kChainMaxW)
-      return false;
+      CHAIN_FAIL(1300);
     cs.rd_off = tab;
     for (int r = 0; r < (1 << lr); ++r)
       for (int k = 0; k < (1 << lk); ++k) {
@@ -1333,7 +1346,7 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
   }
   g.lo = int(L.size());
   for (int ln : L)
-    if (opos_of[size_t(ln)] < 0) return false;
+    if (opos_of[size_t(ln)] < 0) CHAIN_FAIL(1336);
   for (int e = 0; e < (1 << g.lo); ++e)
     for (int i = 0; i < g.lo; ++i)
       if ((e >> i) & 1) T->oout[e] += int64_t(1) << opos_of[size_t(L[size_t(i)])];
@@ -1341,11 +1354,11 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
   // passive lines: the 5 lowest X positions are the lanes, the rest the rows (after
   // the expansion lines, which are the lowest row bits and have no X offset)
   for (int ln : exp_lines)
-    if (opos_of[size_t(ln)] < 0) return false;
+    if (opos_of[size_t(ln)] < 0) CHAIN_FAIL(1344);
   std::vector<int> row_lines = exp_lines;
   row_lines.insert(row_lines.end(), passive.begin() + 5, passive.end());
   const int rb = int(row_lines.size());
-  if (rb > 32) return false;
+  if (rb > 32) CHAIN_FAIL(1348);
   g.n_exp = n_exp;
   for (int l = 0; l < 32; ++l)
     for (int j = 0; j < 5; ++j)
@@ -1370,11 +1383,11 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
     return double(32 * ne) / (4.0 * double(sectors.size()));
   };
   if (efficiency(T->xl, T->xin, 1 << li) < 0.5 || efficiency(T->ol, T->oout, 1 << g.lo) < 0.5)
-    return false;
+    CHAIN_FAIL(1373);
   const bool swaps = jit && stn::chain_swaps_allowed(g);
   if (eff_in) *eff_in = access_efficiency(T->xl, T->xin, li, jit, swaps);
   if (eff_out) *eff_out = access_efficiency(T->ol, T->oout, g.lo, jit, swaps);
-  if (!jit && stn::chain_smem_bytes(g) > 110 * 1024) return false;  // table kernel's tiles
+  if (!jit && stn::chain_smem_bytes(g) > 110 * 1024) CHAIN_FAIL(1377);  // table kernel's tiles
   if (out) {
     out->steps = steps;
     out->chain = true;
@@ -1387,6 +1400,7 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
     out->host_tables = std::shared_ptr<stn::ChainTables>(T.release());
   }
   return true;
+#undef CHAIN_FAIL
 }
 
 bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Sweep *out,
@@ -1616,18 +1630,33 @@ void plan_chains(stn_plan &P) {
   if (opt && std::atoi(opt) == 0) return;
   const char *jo = stn::debug_opt("chain_jit");
   const bool jit = stn::chain_jit_available() && !(jo && std::atoi(jo) == 0);
-  plan_chains(P, jit);
-  if (!jit || P.sweeps.empty()) return;
-  // specialise every chain of the plan with NVRTC; if that fails, plan again for the
-  // table-driven kernel (its tile and stage-shape limits are tighter)
-  std::vector<stn::ChainJitSpec> specs;
-  for (auto &sw : P.sweeps) specs.push_back({&sw.cgeom, sw.host_tables.get()});
-  std::vector<void *> fns;
+  P.chain_banned.clear();
   std::string log;
-  if (stn::chain_jit_compile(specs, P.mode == STN_MODE_EXACT, P.device, &fns, &log)) {
-    for (size_t i = 0; i < fns.size(); ++i) P.sweeps[i].jit_fn = fns[i];
-    return;
+  for (int round = 0; round < 4; ++round) {
+    plan_chains(P, jit);
+    if (!jit || P.sweeps.empty()) return;
+    // specialise every chain of the plan with NVRTC; a kernel that spills (its tiles
+    // exceed the registers: > 64 B of local memory) bans its segment and the runs are
+    // segmented again; if NVRTC fails, plan again for the table-driven kernel
+    std::vector<stn::ChainJitSpec> specs;
+    for (auto &sw : P.sweeps) specs.push_back({&sw.cgeom, sw.host_tables.get()});
+    std::vector<void *> fns;
+    std::vector<int> local;
+    if (!stn::chain_jit_compile(specs, P.mode == STN_MODE_EXACT, P.device, &fns, &log, &local))
+      break;
+    bool banned = false;
+    for (size_t i = 0; i < fns.size(); ++i) {
+      P.sweeps[i].jit_fn = fns[i];
+      if (local[i] > 64 && round < 3) {
+        P.chain_banned.insert(P.sweeps[i].steps);
+        banned = true;
+      }
+    }
+    if (!banned) return;
+    P.sweeps.clear();
+    P.sweep_of_step.clear();
   }
+  if (!P.sweeps.empty() && P.sweeps.front().jit_fn) return;
   if (stn::debug_opt("sweep_debug"))
     fprintf(stderr, "chain jit failed, table kernel instead: %s\n", log.substr(0, 2000).c_str());
   P.sweeps.clear();
@@ -1643,6 +1672,8 @@ void plan_chains(stn_plan &P, bool jit) {
   const char *so = stn::debug_opt("chain_single");
   const bool single = jit && !(so && std::atoi(so) == 0);
   const bool single_all = single && so && std::atoi(so) == 2;
+  const char *ep = stn::debug_opt("chain_exp_pen");
+  const bool exp_pen = !(ep && std::atoi(ep) == 0);
   const int n = int(P.steps.size());
   std::vector<int> next(n, -1), has_prev(n, 0);
   for (int i = 0; i < n; ++i) {
@@ -1666,6 +1697,7 @@ void plan_chains(stn_plan &P, bool jit) {
     // whose largest intermediate has >= 2^min_bits elements are fused.
     const int m = int(chain.size());
     std::vector<std::vector<char>> fits(size_t(m), std::vector<char>(size_t(m), 0));
+    std::vector<std::vector<char>> buildable = fits;  // fits, or built but banned
     // warp-access sector efficiency of each segment's stem input and output
     std::vector<std::vector<double>> e_in(size_t(m), std::vector<double>(size_t(m), 0.0));
     std::vector<std::vector<double>> e_out = e_in;
@@ -1677,6 +1709,8 @@ void plan_chains(stn_plan &P, bool jit) {
           if (b == a) continue;
           break;  // longer ones from a fail too
         }
+        buildable[size_t(a)][size_t(b)] = 1;
+        if (P.chain_banned.count(seg)) continue;
         fits[size_t(a)][size_t(b)] = 1;
       }
     auto gain = [&](int a, int b) -> double {
@@ -1720,7 +1754,8 @@ void plan_chains(stn_plan &P, bool jit) {
       g -= (1.0 / std::max(e_out[size_t(a)][size_t(b)], 0.25) - 1.0) * double(s1.osize);
       // a growth step fused as expansion rows re-reads its stem operand once per row
       // group (8 warps of a CTA share it in L1): costly once that operand outgrows L2
-      if (b > a && double(s0.osize) > 4.0 * xin && xin > double(int64_t(1) << 24)) g -= 8.0 * xin;
+      if (exp_pen && b > a && double(s0.osize) > 4.0 * xin && xin > double(int64_t(1) << 24))
+        g -= 8.0 * xin;
       return largest_mid >= (int64_t(1) << min_bits) ? g : -1.0;
     };
     std::vector<double> best(size_t(m) + 1, 0.0);  // best[i]: steps [i, m)
@@ -1728,7 +1763,7 @@ void plan_chains(stn_plan &P, bool jit) {
     for (int a = m - 1; a >= 0; --a) {
       best[size_t(a)] = best[size_t(a) + 1];  // step a alone
       cut[size_t(a)] = a;
-      for (int b = single ? a : a + 1; b < m && (b == a || fits[size_t(a)][size_t(b)]); ++b) {
+      for (int b = single ? a : a + 1; b < m && (b == a || buildable[size_t(a)][size_t(b)]); ++b) {
         if (!fits[size_t(a)][size_t(b)]) continue;
         const double g = gain(a, b);
         if (g > 0 && g + best[size_t(b) + 1] > best[size_t(a)]) {
