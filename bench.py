@@ -395,6 +395,9 @@ def main():
 
     # ---- per-kernel roofline: the same steps again with CUDA events around every
     # launch on the launch stream ----
+    # one lane here: with several, kernels of different lanes overlap and their event
+    # durations would add up to more than the wall time
+    plan.set_streams(1)
     plan.set_profiling(True)
     plan.reset_profile()
     for k in range(args.steps):
@@ -403,6 +406,7 @@ def main():
     prof = plan.get_profile()
     steps_prof = plan.get_step_profile()
     plan.set_profiling(False)
+    plan.set_streams(args.streams)
 
     # ---- end to end through the C ABI from HOST buffers ----
     lib = abi.load_library()
@@ -496,6 +500,7 @@ def main():
                 "setup": "plan upload (vertex tensors H2D) + branch-cache build, once per "
                          "process like the reference worker's ensure_plan (queue.hpp:204-219)"},
         "gpu_launches": int(launches * args.steps),
+        "arena_bytes_per_slice": int(plan.info.arena_bytes_per_slice),
         "roofline": roof,
         "checksum": float(np.abs(result.cpu().numpy()).sum()),
     }
