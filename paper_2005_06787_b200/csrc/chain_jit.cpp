@@ -174,6 +174,20 @@ __device__ __forceinline__ float2 cmx(float2 acc, float2 x, float2 w) {  // EXAC
   float im = __fadd_rn(__fmul_rn(x.x, w.y), __fmul_rn(x.y, w.x));
   return make_float2(__fadd_rn(acc.x, re), __fadd_rn(acc.y, im));
 }
+// FAST with packed FP32 FMAs (FFMA2): W staged as (wr, wr, wi, -wi); U += x (wr, wr),
+// V += x (wi, -wi) with x = (xr, xi) as held; re = U.x + V.y, im = U.y + V.x
+__device__ __forceinline__ unsigned long long pk(float2 v) {
+  unsigned long long r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y)); return r;
+}
+__device__ __forceinline__ void f2(unsigned long long &a, unsigned long long x, unsigned long long w) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(x), "l"(w));
+}
+__device__ __forceinline__ float2 fin(unsigned long long u, unsigned long long v) {
+  float2 a, c;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(u));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(c.x), "=f"(c.y) : "l"(v));
+  return make_float2(a.x + c.y, a.y + c.x);
+}
 __device__ __forceinline__ float2 cmf(float2 acc, float2 x, float2 w) {  // FAST
   acc.x = fmaf(x.x, w.x, acc.x); acc.x = fmaf(-x.y, w.y, acc.x);
   acc.y = fmaf(x.x, w.y, acc.y); acc.y = fmaf(x.y, w.x, acc.y);
@@ -270,6 +284,11 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
   std::ostringstream s;
   const int ni = 1 << g.li;
   const char *cm = exact ? "cmx" : "cmf";
+  // FAST with packed FP32 FMAs only on request (STN_DEBUG chain_ffma2=1): the U / V
+  // accumulator pairs raise register pressure, more chains spill and are re-planned;
+  // measured on B200 cfg5 88.1 -> 94.5, cfg2 6.78 -> 7.03 ms per slice with them
+  const char *fo = debug_opt("chain_ffma2");
+  const bool ff2 = !exact && fo && std::atoi(fo) != 0;
   // software pipelining holds two input tiles in registers: only for tiles of up to
   // 2^chain_pf_log values (STN_DEBUG chain_pf_log, default 5)
   const bool prefetch = chain_prefetch(g);
@@ -292,7 +311,8 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
   s << "extern \"C\" __global__ void __launch_bounds__(256) stn_chain_" << id
     << "(const JitArgs a) {\n"
     << "  __shared__ long long sxr[1024], sor[1024];\n"
-    << "  extern __shared__ float2 sw[];  // W of every stage (dynamic: up to 40 KiB)\n"
+    << (ff2 ? "  extern __shared__ ulonglong2 sw[];  // W of every stage as (wr, wr, wi, -wi)\n"
+            : "  extern __shared__ float2 sw[];  // W of every stage (dynamic)\n")
     << "  for (int i = threadIdx.x; i < 1024; i += 256) { sxr[i] = a.tabs[i]; sor[i] = a.tabs[1024 + i]; }\n"
     << "  const long long b = blockIdx.y;\n";
   // W: staged through the element offsets of the chain's tables (ChainTables::widx)
@@ -302,8 +322,13 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
   for (int st = 0; st < g.n_stages; ++st) {
     const ChainStage &cs = g.st[st];
     const int kn = 1 << (cs.lk + cs.ln + (st == 0 ? g.n_exp : 0));
-    s << "  for (int i = threadIdx.x; i < " << kn << "; i += 256) sw[" << cs.w_smem
-      << " + i] = a.w[" << st << "][b * a.w_bs[" << st << "] + widx[" << cs.w_off << " + i]];\n";
+    if (ff2)
+      s << "  for (int i = threadIdx.x; i < " << kn << "; i += 256) { const float2 w = a.w[" << st
+        << "][b * a.w_bs[" << st << "] + widx[" << cs.w_off << " + i]]; sw[" << cs.w_smem
+        << " + i] = make_ulonglong2(pk(make_float2(w.x, w.x)), pk(make_float2(w.y, -w.y))); }\n";
+    else
+      s << "  for (int i = threadIdx.x; i < " << kn << "; i += 256) sw[" << cs.w_smem
+        << " + i] = a.w[" << st << "][b * a.w_bs[" << st << "] + widx[" << cs.w_off << " + i]];\n";
   }
   s << "  __syncthreads();\n"
     << "  const int lane = threadIdx.x & 31;\n"
@@ -359,6 +384,18 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
     for (int r = 0; r < R; ++r)
       for (int n = 0; n < N; ++n) {
         const int out_slot = kt.tab[cs.wr_off + r * N + n];
+        if (ff2) {
+          s << "    float2 t" << st + 1 << "_" << out_slot << ";\n    { unsigned long long u = 0ull, v = 0ull;\n";
+          for (int k = 0; k < K; ++k) {
+            const int in_slot = kt.tab[cs.rd_off + r * K + k];
+            const bool ex = st == 0 && g.n_exp > 0;
+            s << "      { const ulonglong2 w = sw[" << (ex ? "wr + " : "")
+              << cs.w_smem + k * (N << (ex ? g.n_exp : 0)) + n << "]; const unsigned long long x = pk(t"
+              << st << "_" << in_slot << "); f2(u, x, w.x); f2(v, x, w.y); }\n";
+          }
+          s << "      t" << st + 1 << "_" << out_slot << " = fin(u, v); }\n";
+          continue;
+        }
         s << "    float2 t" << st + 1 << "_" << out_slot << " = make_float2(0.f, 0.f);\n";
         for (int k = 0; k < K; ++k) {
           const int in_slot = kt.tab[cs.rd_off + r * K + k];
@@ -571,10 +608,10 @@ bool chain_jit_compile(const std::vector<ChainJitSpec> &chains, bool exact, int 
       if (log) *log = "cuModuleLoadData / cuModuleGetFunction failed";
       return false;
     }
-    // W lives in dynamic shared memory next to 16 KiB of row tables: opt in to 40 KiB
+    // W lives in dynamic shared memory next to 16 KiB of row tables: opt in to 80 KiB
     if (Driver::get().FuncSetAttribute)
       Driver::get().FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
-                                     8 * kChainMaxW);
+                                     16 * kChainMaxW);
     g_fns[{srcs[i], device}] = f;
     (*fns)[i] = f;
     if (local_bytes && Driver::get().FuncGetAttribute)
@@ -657,7 +694,7 @@ cudaError_t chain_jit_launch(void *fn, const ChainGeom &g, const ChainTables *T,
   long long gx = 148LL * 8 / (p.nbatch > 0 ? p.nbatch : 1);
   if (gx > want) gx = want;
   if (gx < 1) gx = 1;
-  const unsigned smem = unsigned(8 * std::max(g.w_total, 1));
+  const unsigned smem = unsigned(16 * std::max(g.w_total, 1));  // (FFMA2 form: 16 B per W)
   const CUresult r = Driver::get().LaunchKernel(static_cast<CUfunction>(fn), unsigned(gx),
                                                 unsigned(p.nbatch), 1, 256, 1, 1, smem,
                                                 reinterpret_cast<CUstream>(stream), params,
