@@ -60,7 +60,7 @@ WORKLOAD_TEXT = {
              "per-slice stem benchmark at the largest stem fitting 180 GB HBM "
              "(2^33 complex64) (BASELINE configs[4])"),
 }
-SLICES_PER_GPU = {"cfg1": 16, "cfg2": 64, "cfg3": 16, "cfg4": 8, "cfg5": 2}
+SLICES_PER_GPU = {"cfg1": 16, "cfg2": 64, "cfg3": 16, "cfg4": 16, "cfg5": 8}
 
 
 def plan_file(cfg: str) -> str:
