@@ -54,6 +54,8 @@ struct Cfg {
   static constexpr int COLS_PER_EPI = BN >= 256 ? 128 : BN;
   static constexpr int THREADS = 32 * (2 + CONV_WARPS + EPI_WARPS);
   static constexpr int EPI_WARP0 = 2 + CONV_WARPS;
+  static constexpr int GATHER_WARP0 = 2 + CONV_WARPS + EPI_WARPS;  // gather variant: 4 more
+  static constexpr int GATHER_LAG = STAGES - 2;  // cp.async stages in flight per gatherer
   static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers
   static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024 + 256;
   // kind::tf32: F32 accumulate (bit 4), A/B TF32 (bits 7, 10), both K-major, N >> 3, M >> 4
@@ -164,10 +166,19 @@ struct TcfArgs {
   int k_blocks;    // 2K / BK
   int two_n;
   int n_tiles;     // 2N / BN
+  // gather variant: A[m][k] = X[moff_hi[m / 128] + moff_lo[m % 128] + koff[k]] (complex
+  // elements; the operand permutation read straight from the stem layout)
+  const float2 *x;
+  int64_t x_bs;
+  const int64_t *moff_lo, *moff_hi, *koff;
 };
 
-template <int BN>
-__global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+
+template <int BN, bool GATHER>
+__global__ void __launch_bounds__(Cfg<BN>::THREADS + (GATHER ? 128 : 0), 1)
     k_gemm_tcf(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const TcfArgs args) {
   using C = Cfg<BN>;
@@ -194,7 +205,7 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], GATHER ? 1 + 128 : 1);  // TMA (+ the 128 A gatherers)
       mbar_init(&conv[s], C::CONV_WARPS);
       mbar_init(&empty[s], 1);
     }
@@ -223,8 +234,8 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
         const int s = kb % C::STAGES;
         mbar_wait(&empty[s], ((kb / C::STAGES) & 1) ^ 1);
         unsigned char *st = stage(s);
-        mbar_expect_tx(&full[s], A_BYTES + C::B_BYTES);
-        tma_load_3d(st, &map_a, &full[s], kb * BK, m_tile * BM, za);
+        mbar_expect_tx(&full[s], (GATHER ? 0 : A_BYTES) + C::B_BYTES);
+        if (!GATHER) tma_load_3d(st, &map_a, &full[s], kb * BK, m_tile * BM, za);
         tma_load_3d(st + 2 * A_BYTES, &map_b, &full[s], kb * BK, n_tile * BN, zb);
       }
     }
@@ -278,6 +289,32 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&conv[s]);
+    }
+  } else if (GATHER && warp >= C::GATHER_WARP0) {
+    // ---- A gatherers: row g of the tile, its 16 complex k of each stage, 8-byte
+    // cp.async straight into the K-major SWIZZLE_128B layout TMA would have written
+    // (16-byte chunk c of row r at chunk c ^ (r & 7)); lanes = consecutive rows ----
+    const int g = threadIdx.x - 32 * C::GATHER_WARP0;  // 0 .. 127
+    const float2 *xrow = args.x + int64_t(za) * args.x_bs + args.moff_hi[m_tile] + args.moff_lo[g];
+    const uint32_t row_base = uint32_t(g) * 128u;
+    const int sw = g & 7;
+    for (int kb = 0; kb < args.k_blocks + C::GATHER_LAG; ++kb) {
+      if (kb < args.k_blocks) {
+        const int s = kb % C::STAGES;
+        mbar_wait(&empty[s], ((kb / C::STAGES) & 1) ^ 1);
+        const uint32_t dst = smem_u32(stage(s)) + row_base;
+        const int64_t *ko = args.koff + int64_t(kb) * (BK / 2);
+#pragma unroll
+        for (int j = 0; j < BK / 2; ++j)
+          cp_async8(dst + uint32_t((((j >> 1) ^ sw) << 4) + ((j & 1) << 3)), xrow + __ldg(ko + j));
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      const int done = kb - C::GATHER_LAG;  // this thread's copies of stage `done` landed
+      if (done >= 0) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(C::GATHER_LAG) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&full[done % C::STAGES]);
+      }
     }
   } else {
     // ---- epilogue: drain each K chunk into fp32 registers (RN adds), then store ----
@@ -378,7 +415,7 @@ bool make_map(CUtensorMap *map, const float *base, int64_t inner, int64_t rows, 
          CUDA_SUCCESS;
 }
 
-template <int BN>
+template <int BN, bool GATHER>
 cudaError_t launch_bn(const CUtensorMap &ma, const CUtensorMap &mb, const TcfArgs &args,
                       dim3 grid, cudaStream_t stream) {
   using C = Cfg<BN>;
@@ -386,11 +423,11 @@ cudaError_t launch_bn(const CUtensorMap &ma, const CUtensorMap &mb, const TcfArg
   bool &set = set_on[current_device()];
   if (!set) {
     const cudaError_t attr = cudaFuncSetAttribute(
-        k_gemm_tcf<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+        k_gemm_tcf<BN, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
     if (attr != cudaSuccess) return attr;
     set = true;
   }
-  k_gemm_tcf<BN><<<grid, C::THREADS, C::SMEM, stream>>>(ma, mb, args);
+  k_gemm_tcf<BN, GATHER><<<grid, C::THREADS + (GATHER ? 128 : 0), C::SMEM, stream>>>(ma, mb, args);
   return cudaGetLastError();
 }
 
@@ -418,11 +455,13 @@ size_t gemm_tcf_workspace_bytes(const GemmShape &s, const BatchPtrs &p) {
 }
 
 cudaError_t launch_gemm_tcf(const GemmShape &s, const BatchPtrs &p, void *workspace,
-                            size_t workspace_bytes, cudaStream_t stream) {
+                            size_t workspace_bytes, cudaStream_t stream, const TcfGather *ga) {
   if (!gemm_tcf_supported(s)) return cudaErrorNotSupported;
   if (gemm_tcf_workspace_bytes(s, p) > workspace_bytes) return cudaErrorNotSupported;
-  // A is read in place: one [D|M|K] block per slice, or shared by every slice
-  if (p.a_bs != 0 && p.a_bs != s.D * s.M * s.K) return cudaErrorNotSupported;
+  // A is read in place: one [D|M|K] block per slice, or shared by every slice; or
+  // gathered from the stem layout through offset tables (ga, D == 1)
+  if (ga && s.D != 1) return cudaErrorNotSupported;
+  if (!ga && p.a_bs != 0 && p.a_bs != s.D * s.M * s.K) return cudaErrorNotSupported;
   const int64_t nbA = (p.a_bs ? p.nbatch : 1) * s.D;
   const int64_t nbB = (p.b_bs ? p.nbatch : 1) * s.D;
   float *braw = static_cast<float *>(workspace);
@@ -433,11 +472,14 @@ cudaError_t launch_gemm_tcf(const GemmShape &s, const BatchPtrs &p, void *worksp
                                                       s.K * s.N, int(s.D), int(s.K), int(s.N),
                                                       braw);
   }
-  const int bn = pick_bn(s);
+  // the gather variant runs 128 more threads: 64-column tiles keep its epilogue in registers
+  const int bn = ga ? 64 : pick_bn(s);
   CUtensorMap ma, mb;
-  if (!make_map(&ma, static_cast<const float *>(p.a), 2 * s.K, s.M, nbA, 2 * s.M * s.K, BM) ||
+  if ((!ga && !make_map(&ma, static_cast<const float *>(p.a), 2 * s.K, s.M, nbA, 2 * s.M * s.K,
+                        BM)) ||
       !make_map(&mb, braw, 2 * s.K, 2 * s.N, nbB, 4 * s.N * s.K, bn))
     return cudaErrorNotSupported;
+  if (ga) ma = mb;  // unused by the gather variant
   TcfArgs args;
   args.c = static_cast<float *>(p.out);
   args.c_bs = 2 * p.out_bs;
@@ -448,14 +490,20 @@ cudaError_t launch_gemm_tcf(const GemmShape &s, const BatchPtrs &p, void *worksp
   args.k_blocks = int(2 * s.K / BK);
   args.two_n = int(2 * s.N);
   args.n_tiles = int(2 * s.N / bn);
+  args.x = static_cast<const float2 *>(p.a);
+  args.x_bs = p.a_bs;
+  args.moff_lo = ga ? ga->moff_lo : nullptr;
+  args.moff_hi = ga ? ga->moff_hi : nullptr;
+  args.koff = ga ? ga->koff : nullptr;
   dim3 grid(unsigned((2 * s.N / bn) * (s.M / BM)), 1, unsigned(s.D * p.nbatch));
+  if (ga) return launch_bn<64, true>(ma, mb, args, grid, stream);  // bn = 64 (registers)
   switch (bn) {
     case 256:
-      return launch_bn<256>(ma, mb, args, grid, stream);
+      return launch_bn<256, false>(ma, mb, args, grid, stream);
     case 128:
-      return launch_bn<128>(ma, mb, args, grid, stream);
+      return launch_bn<128, false>(ma, mb, args, grid, stream);
     default:
-      return launch_bn<64>(ma, mb, args, grid, stream);
+      return launch_bn<64, false>(ma, mb, args, grid, stream);
   }
 }
 

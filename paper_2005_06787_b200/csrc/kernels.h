@@ -393,7 +393,13 @@ bool gemm_tc_supported(const GemmShape &s);
 // Workspace: the raw B'' plane(s).
 bool gemm_tcf_supported(const GemmShape &s);
 size_t gemm_tcf_workspace_bytes(const GemmShape &s, const BatchPtrs &p);
+// Operand A gathered from the stem layout (no permuted copy): A[m][k] = X[moff_hi[m/128] +
+// moff_lo[m%128] + koff[k]] in complex elements, device tables.
+struct TcfGather {
+  const int64_t *moff_lo, *moff_hi, *koff;
+};
 cudaError_t launch_gemm_tcf(const GemmShape &s, const BatchPtrs &p, void *workspace,
-                            size_t workspace_bytes, cudaStream_t stream);
+                            size_t workspace_bytes, cudaStream_t stream,
+                            const TcfGather *gather = nullptr);
 
 }  // namespace stn

@@ -245,6 +245,7 @@ struct StepPlan {
   stn::PermTileGeom pat{}, pbt{}, pct{};                         // high-occupancy tile permutes
   std::shared_ptr<DevBuf> pa_bases, pb_bases, pc_bases;
   std::shared_ptr<DevBuf> skinny_tab;  // gathered skinny GEMM: k offsets, M bit strides
+  std::shared_ptr<DevBuf> tcf_gather;  // fused-split GEMM gathering A: m / k offset tables
   int skinny_mbits = 0;
   stn::AbsorbGeom pag{}, pbg{}, pcg{};
   stn::GemmShape gs{};
@@ -1076,6 +1077,32 @@ void choose_kernel(stn_plan &P, StepPlan &sp, const std::vector<int> &ldims,
           sp.skinny_tab->upload(tab);
           sp.skinny_mbits = nmb;
         }
+      }
+      // fused-split tcgen05 GEMM with a permuted A: gather A from the stem layout inside
+      // the GEMM (offset tables) instead of materialising the permuted operand
+      const char *tg = stn::debug_opt("tcf_gather");  // STN_DEBUG tcf_gather=0: permute
+      if (sp.kern == Kern::GemmTc && sp.tcf && !sp.a_id && all2 && sp.gs.D == 1 &&
+          !(tg && std::atoi(tg) == 0) && int(adims.size()) == nmb + nkb &&
+          (int64_t(1) << nmb) == sp.gs.M && (int64_t(1) << nkb) == sp.gs.K && sp.gs.M >= 128) {
+        const int r = int(adims.size());
+        auto mbit = [&](int j) { return int64_t(1) << (r - 1 - sp.gl[size_t(r - 1 - nkb - j)]); };
+        auto moff = [&](int64_t m) {
+          int64_t off = 0;
+          for (int j = 0; j < nmb; ++j)
+            if ((m >> j) & 1) off += mbit(j);
+          return off;
+        };
+        std::vector<int64_t> tab;  // [128 moff_lo | M/128 moff_hi | K koff]
+        for (int64_t m = 0; m < 128; ++m) tab.push_back(moff(m));
+        for (int64_t t = 0; t < sp.gs.M / 128; ++t) tab.push_back(moff(t * 128));
+        for (int64_t k = 0; k < sp.gs.K; ++k) {
+          int64_t off = 0;
+          for (int j = 0; j < nkb; ++j)
+            if ((k >> j) & 1) off += int64_t(1) << (r - 1 - sp.gl[size_t(r - 1 - j)]);
+          tab.push_back(off);
+        }
+        sp.tcf_gather = std::make_shared<DevBuf>();
+        sp.tcf_gather->upload(tab);
       }
     }
   }
@@ -2013,7 +2040,8 @@ void build_program(stn_plan &P, Program &prog, int which /*0 build, 1 cache, 2 n
     if (sp.kern != Kern::GemmSimt && sp.kern != Kern::GemmTc) continue;
     // A needs no scratch when the skinny GEMM gathers it through its offset table or the
     // tile permute writes it straight into the tcgen05 workspace (a_fused in launch_op)
-    const bool a_in_place = sp.skinny_tab || (sp.kern == Kern::GemmTc && !sp.tcf && sp.pa_bases &&
+    const bool a_in_place = sp.skinny_tab || sp.tcf_gather ||
+                            (sp.kern == Kern::GemmTc && !sp.tcf && sp.pa_bases &&
                                               stn::gemm_tc_supported(sp.gs));
     if (!sp.a_id && !a_in_place)
       scr[k][0] = new_item(sp.gemm_swap ? sp.rsize : sp.lsize, int64_t(k), int64_t(k));
@@ -2716,8 +2744,8 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
         prof.done(STN_KERNEL_PERMUTE, (es + 2 * es) * asize * nb, 0);
         ga = nullptr;
         ga_bs = asize;
-      } else if (sp.skinny_tab) {
-        // gathered by the skinny GEMM itself
+      } else if (sp.skinny_tab || sp.tcf_gather) {
+        // gathered by the GEMM itself (skinny SIMT / fused-split tcgen05)
       } else if (!sp.a_id) {
         void *dst = elem_ptr(P, P.cur->arena.ptr, op.scr_a * nb);
         if (sp.pa_bases)
@@ -2755,7 +2783,15 @@ void launch_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, cudaSt
       if (sp.kern == Kern::GemmTc && sp.tcf) {
         const size_t ws = stn::gemm_tcf_workspace_bytes(sp.gs, p);
         P.cur->tc_workspace.reserve(std::max<size_t>(ws, 16));
-        cuda_check(stn::launch_gemm_tcf(sp.gs, p, P.cur->tc_workspace.ptr, ws, st),
+        stn::TcfGather tg{};
+        if (sp.tcf_gather) {
+          const int64_t *t = sp.tcf_gather->as<int64_t>();
+          tg = {t, t + 128, t + 128 + sp.gs.M / 128};
+          p.a = ra.ptr;  // the stem itself
+          p.a_bs = ra.bs;
+        }
+        cuda_check(stn::launch_gemm_tcf(sp.gs, p, P.cur->tc_workspace.ptr, ws, st,
+                                        sp.tcf_gather ? &tg : nullptr),
                    "tcgen05 fused-split gemm");
         prof.done(STN_KERNEL_GEMM_TC, gbytes, flops);
         done = true;
