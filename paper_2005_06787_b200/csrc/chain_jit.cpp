@@ -330,8 +330,31 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
       s << "  for (int i = threadIdx.x; i < " << kn << "; i += 256) sw[" << cs.w_smem
         << " + i] = a.w[" << st << "][b * a.w_bs[" << st << "] + widx[" << cs.w_off << " + i]];\n";
   }
-  s << "  __syncthreads();\n"
-    << "  const int lane = threadIdx.x & 31;\n"
+  // W operands of small stages (K x N <= 16, not an expansion stage) held in registers for
+  // the whole kernel instead of one shared-memory load per multiply-add: only on request
+  // (STN_DEBUG chain_wreg=V, at most V values) -- the registers they take cost more than
+  // the loads they save (measured on B200: cfg5 86.9 -> 106.3 ms per slice with 16)
+  const char *wo = debug_opt("chain_wreg");
+  const int wreg_max = wo ? std::atoi(wo) : 0;
+  std::vector<char> hoist(size_t(g.n_stages), 0);
+  {
+    int used = 0;
+    for (int st = 0; st < g.n_stages; ++st) {
+      const ChainStage &cs = g.st[st];
+      const int kn = 1 << (cs.lk + cs.ln);
+      if (ff2 || (st == 0 && g.n_exp > 0) || kn > 16 || used + kn > wreg_max) continue;
+      hoist[size_t(st)] = 1;
+      used += kn;
+    }
+  }
+  s << "  __syncthreads();\n";
+  for (int st = 0; st < g.n_stages; ++st) {
+    if (!hoist[size_t(st)]) continue;
+    const ChainStage &cs = g.st[st];
+    for (int i = 0; i < (1 << (cs.lk + cs.ln)); ++i)
+      s << "  const float2 w" << st << "_" << i << " = sw[" << cs.w_smem + i << "];\n";
+  }
+  s << "  const int lane = threadIdx.x & 31;\n"
     << "  const long long xl = a.tabs[2048 + lane]"
     << (xswap ? " + (((lane >> " + std::to_string(xj) + ") & 1) ? " +
                     std::to_string(xl_p[1 << xj] - kt.xl[1 << xj]) + "LL : 0LL)"
@@ -401,8 +424,12 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
           const int in_slot = kt.tab[cs.rd_off + r * K + k];
           const bool ex = st == 0 && g.n_exp > 0;  // W block [k][e][n]
           s << "    t" << st + 1 << "_" << out_slot << " = " << cm << "(t" << st + 1 << "_"
-            << out_slot << ", t" << st << "_" << in_slot << ", sw[" << (ex ? "wr + " : "")
-            << cs.w_smem + k * (N << (ex ? g.n_exp : 0)) + n << "]);\n";
+            << out_slot << ", t" << st << "_" << in_slot << ", ";
+          if (hoist[size_t(st)])
+            s << "w" << st << "_" << k * N + n << ");\n";
+          else
+            s << "sw[" << (ex ? "wr + " : "") << cs.w_smem + k * (N << (ex ? g.n_exp : 0)) + n
+              << "]);\n";
         }
       }
   }
