@@ -280,7 +280,7 @@ void emit_exchange(std::ostringstream &s, const std::string &prefix, int n_log, 
 }
 
 // Emits the kernel of one chain. `kt` is the host copy of its tables.
-std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) {
+std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact, int minb = 1) {
   std::ostringstream s;
   const int ni = 1 << g.li;
   const char *cm = exact ? "cmx" : "cmf";
@@ -308,7 +308,8 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact) 
     chain_apply_swap(kt.ol, kt.oout, g.lo, oj, os_, ol_p, oout_p);
     oout = oout_p;
   }
-  s << "extern \"C\" __global__ void __launch_bounds__(256) stn_chain_" << id
+  s << "extern \"C\" __global__ void __launch_bounds__(256"
+    << (minb > 1 ? ", " + std::to_string(minb) : std::string()) << ") stn_chain_" << id
     << "(const JitArgs a) {\n"
     << "  __shared__ long long sxr[1024], sor[1024];\n"
     << (ff2 ? "  extern __shared__ ulonglong2 sw[];  // W of every stage as (wr, wr, wi, -wi)\n"
@@ -560,24 +561,34 @@ bool chain_jit_compile_only(const std::vector<ChainJitSpec> &chains, bool exact,
 }
 
 bool chain_jit_compile(const std::vector<ChainJitSpec> &chains, bool exact, int device,
-                       std::vector<void *> *fns, std::string *log,
-                       std::vector<int> *local_bytes) {
-  fns->assign(chains.size(), nullptr);
-  if (local_bytes) local_bytes->assign(chains.size(), 0);
+                       std::vector<void *> *fns_out, std::string *log,
+                       std::vector<int> *local_out, std::vector<void *> *alt_out) {
+  const size_t nc = chains.size();
+  fns_out->assign(nc, nullptr);
+  if (local_out) local_out->assign(nc, 0);
+  if (alt_out) alt_out->assign(nc, nullptr);
   if (chains.empty()) return true;
   if (!chain_jit_available()) {
     if (log) *log = "NVRTC or the driver module API is not available";
     return false;
   }
-  // one program per chain: independent, so they compile on parallel host threads
-  std::vector<std::string> srcs(chains.size());
-  for (size_t i = 0; i < chains.size(); ++i)
-    srcs[i] = std::string(kPrelude) + emit(*chains[i].geom, *chains[i].tables, 0, exact);
-  std::vector<std::vector<char>> cubins(chains.size());
-  std::vector<char> have(chains.size(), 0);
+  // one program per chain: independent, so they compile on parallel host threads. With
+  // alt_out, a second variant of every chain capped at 128 registers (two CTAs per SM);
+  // launch_chain_op times both on their first run and keeps the faster
+  const size_t nv = alt_out ? 2 * nc : nc;
+  std::vector<std::string> srcs(nv);
+  for (size_t i = 0; i < nv; ++i)
+    srcs[i] = std::string(kPrelude) +
+              emit(*chains[i % nc].geom, *chains[i % nc].tables, 0, exact, i < nc ? 1 : 2);
+  std::vector<void *> fnv(nv, nullptr);
+  std::vector<int> localv(nv, 0);
+  std::vector<void *> *fns = &fnv;
+  std::vector<int> *local_bytes = &localv;
+  std::vector<std::vector<char>> cubins(nv);
+  std::vector<char> have(nv, 0);
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    for (size_t i = 0; i < chains.size(); ++i) {
+    for (size_t i = 0; i < nv; ++i) {
       auto it = g_fns.find({srcs[i], device});
       if (it != g_fns.end()) {
         (*fns)[i] = it->second;
@@ -591,13 +602,13 @@ bool chain_jit_compile(const std::vector<ChainJitSpec> &chains, bool exact, int 
       }
     }
   }
-  for (size_t i = 0; i < chains.size(); ++i)
+  for (size_t i = 0; i < nv; ++i)
     if (!have[i] && read_file(cache_path(srcs[i]), &cubins[i])) have[i] = 1;
   std::vector<size_t> todo;
-  for (size_t i = 0; i < chains.size(); ++i)
+  for (size_t i = 0; i < nv; ++i)
     if (!have[i]) todo.push_back(i);
-  std::vector<std::string> logs(chains.size());
-  std::vector<char> ok(chains.size(), 1);
+  std::vector<std::string> logs(nv);
+  std::vector<char> ok(nv, 1);
   if (!todo.empty()) {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     const size_t nt = std::min<size_t>(todo.size(), hw);
@@ -616,7 +627,7 @@ bool chain_jit_compile(const std::vector<ChainJitSpec> &chains, bool exact, int 
     for (auto &t : pool) t.join();
   }
   std::lock_guard<std::mutex> lk(g_mu);
-  for (size_t i = 0; i < chains.size(); ++i) {
+  for (size_t i = 0; i < nv; ++i) {
     if (have[i] == 2) {
       if (local_bytes && Driver::get().FuncGetAttribute)
         Driver::get().FuncGetAttribute(&(*local_bytes)[i], CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES,
@@ -647,9 +658,16 @@ bool chain_jit_compile(const std::vector<ChainJitSpec> &chains, bool exact, int 
       int regs = 0, local = 0;
       Driver::get().FuncGetAttribute(&regs, CU_FUNC_ATTRIBUTE_NUM_REGS, f);
       Driver::get().FuncGetAttribute(&local, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, f);
-      fprintf(stderr, "chain kernel %zu: li %d lo %d stages %d, %d registers, %d B local\n", i,
-              chains[i].geom->li, chains[i].geom->lo, chains[i].geom->n_stages, regs, local);
+      fprintf(stderr, "chain kernel %zu%s: li %d lo %d stages %d, %d registers, %d B local\n",
+              i % nc, i < nc ? "" : " (128-register variant)", chains[i % nc].geom->li,
+              chains[i % nc].geom->lo, chains[i % nc].geom->n_stages, regs, local);
     }
+  }
+  for (size_t i = 0; i < nc; ++i) {
+    (*fns_out)[i] = fnv[i];
+    if (local_out) (*local_out)[i] = localv[i];
+    // the capped variant only where it does not spill
+    if (alt_out && localv[nc + i] == 0) (*alt_out)[i] = fnv[nc + i];
   }
   return true;
 }

@@ -21,7 +21,8 @@ int chain_vec_max();
 // the compilation failed: the chains then run on kernels_chain.cu.
 bool chain_jit_compile(const std::vector<ChainJitSpec> &chains, bool exact, int device,
                        std::vector<void *> *fns, std::string *log,
-                       std::vector<int> *local_bytes = nullptr);
+                       std::vector<int> *local_bytes = nullptr,
+                       std::vector<void *> *alt_fns = nullptr);
 // NVRTC compilation alone (no device needed): the CPU check that generated code builds.
 bool chain_jit_compile_only(const std::vector<ChainJitSpec> &chains, bool exact,
                             std::string *log);

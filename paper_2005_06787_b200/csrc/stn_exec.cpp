@@ -378,6 +378,8 @@ struct stn_plan {
     stn::ChainGeom cgeom{};
     std::shared_ptr<stn::ChainTables> host_tables;  // for the NVRTC-specialised kernel
     void *jit_fn = nullptr;                          // its CUfunction (chain_jit.cpp)
+    void *jit_alt = nullptr;   // the same kernel capped at 128 registers (two CTAs per SM)
+    mutable int jit_pick = 0;  // 0: not yet timed, 1: jit_fn, 2: jit_alt (first-run choice)
   };
   std::vector<Sweep> sweeps;
   std::map<int, int> sweep_of_step;
@@ -1667,13 +1669,21 @@ void plan_chains(stn_plan &P) {
     // segmented again; if NVRTC fails, plan again for the table-driven kernel
     std::vector<stn::ChainJitSpec> specs;
     for (auto &sw : P.sweeps) specs.push_back({&sw.cgeom, sw.host_tables.get()});
-    std::vector<void *> fns;
+    std::vector<void *> fns, alt;
     std::vector<int> local;
-    if (!stn::chain_jit_compile(specs, P.mode == STN_MODE_EXACT, P.device, &fns, &log, &local))
+    // STN_DEBUG chain_alt=1: also compile every chain capped at 128 registers and keep the
+    // faster variant on its first run (cfg5: 249 3.09 -> 2.77, 1185 3.09 -> 2.68 ms, the
+    // big chains spill when capped; no measurable change per slice, twice the NVRTC work)
+    const char *ao = stn::debug_opt("chain_alt");
+    const bool want_alt = ao && std::atoi(ao) != 0;
+    if (!stn::chain_jit_compile(specs, P.mode == STN_MODE_EXACT, P.device, &fns, &log, &local,
+                                want_alt ? &alt : nullptr))
       break;
     bool banned = false;
     for (size_t i = 0; i < fns.size(); ++i) {
       P.sweeps[i].jit_fn = fns[i];
+      P.sweeps[i].jit_alt = want_alt ? alt[i] : nullptr;
+      P.sweeps[i].jit_pick = 0;
       if (local[i] > 64 && round < 3) {
         P.chain_banned.insert(P.sweeps[i].steps);
         banned = true;
@@ -2602,10 +2612,39 @@ void launch_chain_op(stn_plan &P, const Op &op, const stn_cache *cache, int nb, 
     bytes += 8.0 * (w.bs ? nb : 1) * op.wrefs[j].size;
   }
   for (int stp : sw.steps) flops += 8.0 * double(P.steps[stp].d.mults) * nb;
-  ProfScope prof(P, st, sw.steps.front());
   stn::BatchPtrs p{x.ptr, nullptr, const_cast<void *>(o.ptr), x.bs, 0, o.bs, nb};
+  if (sw.jit_fn && sw.jit_alt && sw.jit_pick == 0) {
+    // first run outside a capture: time both variants (they write the same output, bit for
+    // bit) and keep the faster one for every later launch and graph capture
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cuda_check(cudaStreamIsCapturing(st, &cs), "capture status");
+    if (cs == cudaStreamCaptureStatusNone) {
+      cudaEvent_t ev[3];
+      for (auto &e : ev) cuda_check(cudaEventCreate(&e), "event");
+      float ms[2] = {0, 0};
+      cuda_check(cudaEventRecord(ev[0], st), "event");
+      cuda_check(stn::chain_jit_launch(sw.jit_fn, g, sw.tables->as<stn::ChainTables>(), p, st),
+                 "fused stem chain kernel (specialised)");
+      cuda_check(cudaEventRecord(ev[1], st), "event");
+      cuda_check(stn::chain_jit_launch(sw.jit_alt, g, sw.tables->as<stn::ChainTables>(), p, st),
+                 "fused stem chain kernel (specialised, 128 registers)");
+      cuda_check(cudaEventRecord(ev[2], st), "event");
+      cuda_check(cudaEventSynchronize(ev[2]), "event sync");
+      cudaEventElapsedTime(&ms[0], ev[0], ev[1]);
+      cudaEventElapsedTime(&ms[1], ev[1], ev[2]);
+      for (auto &e : ev) cudaEventDestroy(e);
+      sw.jit_pick = ms[1] < 0.97f * ms[0] ? 2 : 1;
+      if (stn::debug_opt("sweep_debug"))
+        fprintf(stderr, "chain from step %d: %.3f ms, 128-register variant %.3f ms -> %s\n",
+                sw.steps.front(), ms[0], ms[1], sw.jit_pick == 2 ? "variant" : "primary");
+      P.kernel_launches++;
+      return;
+    }
+  }
+  ProfScope prof(P, st, sw.steps.front());
   if (sw.jit_fn)
-    cuda_check(stn::chain_jit_launch(sw.jit_fn, g, sw.tables->as<stn::ChainTables>(), p, st),
+    cuda_check(stn::chain_jit_launch(sw.jit_pick == 2 ? sw.jit_alt : sw.jit_fn, g,
+                                     sw.tables->as<stn::ChainTables>(), p, st),
                "fused stem chain kernel (specialised)");
   else if (g.ma > stn::kChainTableLog)
     fail(STN_ERR_CUDA, "fused stem chain planned for the specialised kernel has none");
