@@ -1772,13 +1772,13 @@ void plan_chains(stn_plan &P, bool jit) {
         const bool slow = sp.kern == Kern::AbsorbTma || sp.kern == Kern::AbsorbTc ||
                           sp.kern == Kern::Absorb || sp.kern == Kern::Lanes ||
                           sp.kern == Kern::AbsorbMma;
-        // ... and while its math stays under the HBM stream: K x N <= 8 (K + N) complex
+        // ... and while its math stays under the HBM stream: K x N <= 12 (K + N) complex
         // multiply-adds per column element moved (cfg2 494 / 536, K x N = 1024 against
-        // 80 / 64 elements: 3.6 -> 2.7 TB/s)
+        // 80 / 64 elements: 3.6 -> 2.7 TB/s; cfg5 1365, 512 against 48, is kept)
         const int64_t K = int64_t(1) << sp.kbits.size(), N = int64_t(1) << sp.nbits.size();
         const bool coalesced = e_in[size_t(a)][size_t(a)] > 0.99 &&
                                (e_out[size_t(a)][size_t(a)] > 0.99 || 4 * sp.osize <= xsize) &&
-                               K * N <= 8 * (K + N);
+                               K * N <= 12 * (K + N);
         g = (single_all || (slow && coalesced)) ? 0.5 * double(sp.lsize + sp.rsize + sp.osize)
                                                 : 0.0;
         return sp.osize >= (int64_t(1) << min_bits) ? g - 1.0 : -1.0;
