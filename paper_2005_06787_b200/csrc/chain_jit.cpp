@@ -739,7 +739,8 @@ cudaError_t chain_jit_launch(void *fn, const ChainGeom &g, const ChainTables *T,
   long long gx = 148LL * 8 / (p.nbatch > 0 ? p.nbatch : 1);
   if (gx > want) gx = want;
   if (gx < 1) gx = 1;
-  const unsigned smem = unsigned(16 * std::max(g.w_total, 1));  // (FFMA2 form: 16 B per W)
+  // W bytes: 8 per element, 16 in the (opt-in) FFMA2 form
+  const unsigned smem = unsigned((debug_opt("chain_ffma2") ? 16 : 8) * std::max(g.w_total, 1));
   const CUresult r = Driver::get().LaunchKernel(static_cast<CUfunction>(fn), unsigned(gx),
                                                 unsigned(p.nbatch), 1, 256, 1, 1, smem,
                                                 reinterpret_cast<CUstream>(stream), params,

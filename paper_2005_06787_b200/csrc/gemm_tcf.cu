@@ -27,6 +27,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <mutex>
@@ -346,10 +347,12 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS + (GATHER ? 128 : 0), 1)
     }
     float *crow = args.c + int64_t(slice) * args.c_bs + int64_t(d) * args.c_ds +
                   int64_t(row) * args.two_n + int64_t(n_tile) * BN + C::COLS_PER_EPI * half;
+    const int col0 = n_tile * BN + C::COLS_PER_EPI * half;  // 2N < 64: padded B'' columns
 #pragma unroll
     for (int q = 0; q < C::COLS_PER_EPI / 4; ++q)
-      reinterpret_cast<float4 *>(crow)[q] =
-          make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+      if (col0 + 4 * q < args.two_n)
+        reinterpret_cast<float4 *>(crow)[q] =
+            make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
   }
   tc_fence_before();
   __syncthreads();
@@ -357,6 +360,23 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS + (GATHER ? 128 : 0), 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(C::TMEM_COLS));
+  }
+}
+
+// Narrow B (N < 32): rows 2n, 2n+1 of a zeroed B'' with 2 * npad rows.
+__global__ void k_expand_b_raw_small(const float2 *__restrict__ b, int64_t b_bs, int64_t b_ds,
+                                     int D, int K, int N, int npad, float *__restrict__ out) {
+  const int z = blockIdx.y;
+  const int64_t slice = z / D, d = z % D;
+  const float2 *src = b + slice * b_bs + d * b_ds;
+  float *o = out + int64_t(z) * 4 * K * npad;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < int64_t(K) * N;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int k = int(i / N), n = int(i % N);
+    const float2 v = src[i];
+    const int64_t row0 = int64_t(2 * n) * (2 * K) + 2 * k, row1 = row0 + 2 * K;
+    *reinterpret_cast<float2 *>(o + row0) = make_float2(v.x, -v.y);
+    *reinterpret_cast<float2 *>(o + row1) = make_float2(v.y, v.x);
   }
 }
 
@@ -444,14 +464,19 @@ int pick_bn(const GemmShape &s) {
 
 }  // namespace
 
+// padded B'' columns for a narrow N (8, 16: the tile's extra rows are zeros)
+int64_t tcf_npad(const GemmShape &s) { return s.N < 32 ? 32 : s.N; }
+
 bool gemm_tcf_supported(const GemmShape &s) {
-  return s.M % BM == 0 && s.N % 32 == 0 && s.K % 32 == 0 && s.M >= BM &&
+  // narrow N (8, 16) only for tall A (>= 512 tiles): the skinny SIMT GEMM wins below
+  return s.M % BM == 0 && (s.N % 32 == 0 || ((s.N == 8 || s.N == 16) && s.M >= (1 << 16))) &&
+         s.K % 32 == 0 && s.M >= BM &&
          s.M <= (int64_t(1) << 31) && s.N <= (int64_t(1) << 30) && s.K <= (int64_t(1) << 30);
 }
 
 size_t gemm_tcf_workspace_bytes(const GemmShape &s, const BatchPtrs &p) {
   const size_t nbB = size_t(p.b_bs ? p.nbatch : 1) * size_t(s.D);
-  return nbB * size_t(4) * size_t(s.N) * size_t(s.K) * 4;
+  return nbB * size_t(4) * size_t(tcf_npad(s)) * size_t(s.K) * 4;
 }
 
 cudaError_t launch_gemm_tcf(const GemmShape &s, const BatchPtrs &p, void *workspace,
@@ -465,7 +490,16 @@ cudaError_t launch_gemm_tcf(const GemmShape &s, const BatchPtrs &p, void *worksp
   const int64_t nbA = (p.a_bs ? p.nbatch : 1) * s.D;
   const int64_t nbB = (p.b_bs ? p.nbatch : 1) * s.D;
   float *braw = static_cast<float *>(workspace);
-  {
+  const int64_t npad = tcf_npad(s);
+  if (npad != s.N) {
+    const size_t bytes = size_t(nbB) * 4 * size_t(npad) * size_t(s.K) * 4;
+    cudaError_t e = cudaMemsetAsync(braw, 0, bytes, stream);
+    if (e != cudaSuccess) return e;
+    k_expand_b_raw_small<<<dim3(unsigned(std::min<int64_t>((s.K * s.N + 255) / 256, 1024)),
+                               unsigned(nbB)),
+                           256, 0, stream>>>(static_cast<const float2 *>(p.b), p.b_bs, s.K * s.N,
+                                             int(s.D), int(s.K), int(s.N), int(npad), braw);
+  } else {
     if (s.N % 32 || s.K % 32) return cudaErrorNotSupported;
     dim3 grid(unsigned(s.N / 32), unsigned(s.K / 32), unsigned(nbB));
     k_expand_b_raw<<<grid, dim3(32, 8), 0, stream>>>(static_cast<const float2 *>(p.b), p.b_bs,
@@ -473,11 +507,11 @@ cudaError_t launch_gemm_tcf(const GemmShape &s, const BatchPtrs &p, void *worksp
                                                       braw);
   }
   // the gather variant runs 128 more threads: 64-column tiles keep its epilogue in registers
-  const int bn = ga ? 64 : pick_bn(s);
+  const int bn = ga || npad != s.N ? 64 : pick_bn(s);
   CUtensorMap ma, mb;
   if ((!ga && !make_map(&ma, static_cast<const float *>(p.a), 2 * s.K, s.M, nbA, 2 * s.M * s.K,
                         BM)) ||
-      !make_map(&mb, braw, 2 * s.K, 2 * s.N, nbB, 4 * s.N * s.K, bn))
+      !make_map(&mb, braw, 2 * s.K, 2 * npad, nbB, 4 * npad * s.K, bn))
     return cudaErrorNotSupported;
   if (ga) ma = mb;  // unused by the gather variant
   TcfArgs args;
@@ -489,13 +523,13 @@ cudaError_t launch_gemm_tcf(const GemmShape &s, const BatchPtrs &p, void *worksp
   args.b_batched = p.b_bs != 0;
   args.k_blocks = int(2 * s.K / BK);
   args.two_n = int(2 * s.N);
-  args.n_tiles = int(2 * s.N / bn);
+  args.n_tiles = int(2 * npad / bn);
   args.x = static_cast<const float2 *>(p.a);
   args.x_bs = p.a_bs;
   args.moff_lo = ga ? ga->moff_lo : nullptr;
   args.moff_hi = ga ? ga->moff_hi : nullptr;
   args.koff = ga ? ga->koff : nullptr;
-  dim3 grid(unsigned((2 * s.N / bn) * (s.M / BM)), 1, unsigned(s.D * p.nbatch));
+  dim3 grid(unsigned((2 * npad / bn) * (s.M / BM)), 1, unsigned(s.D * p.nbatch));
   if (ga) return launch_bn<64, true>(ma, mb, args, grid, stream);  // bn = 64 (registers)
   switch (bn) {
     case 256:

@@ -25,6 +25,8 @@ def _needs_gpu():
     (256, 128, 16384, 1, 1, 1),  # long K: chunked TMEM accumulation keeps fp32 accuracy
     (4096, 32, 8192, 1, 1, 1),   # cfg5's skinny steps (2N = 64: the 128 x 64 fused tile)
     (512, 96, 512, 2, 1, 1),     # 2N = 192: 128 x 64 tiles
+    (65536, 8, 512, 1, 1, 1),    # narrow N (cfg4's 2^20 x 8 x 512): zero-padded B'' tile
+    (65536, 16, 256, 2, 1, 0),
 ])
 def test_tc_gemm_matches_fp64(M, N, K, batches, ab, bb, kernel, monkeypatch):
     """Both tcgen05 GEMMs: the fused-split one (gemm_tcf.cu, raw fp32 TMA tiles, lo
