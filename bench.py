@@ -326,7 +326,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # rank 0's stdout carries exactly one JSON line: no NCCL version / info banner
-    os.environ["NCCL_DEBUG"] = os.environ.get("STN_NCCL_DEBUG", "WARN")
+    # (NCCL prints its version banner to stdout at any NCCL_DEBUG level: leave it unset
+    # unless STN_NCCL_DEBUG asks for one)
+    if "STN_NCCL_DEBUG" in os.environ:
+        os.environ["NCCL_DEBUG"] = os.environ["STN_NCCL_DEBUG"]
+    else:
+        os.environ.pop("NCCL_DEBUG", None)
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
