@@ -49,8 +49,12 @@ struct Cfg {
   // each in registers at 384 threads)
   static constexpr int CONV_WARPS = BN >= 256 ? 2 : 4;
   static constexpr int B_BYTES = BN * BK * 4;
-  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // raw + lo of each
-  static constexpr int STAGES = (192 * 1024) / STAGE_BYTES;      // 2 (256), 3 (128), 4 (64)
+  // a ring of raw stages [A | B] (TMA / gather targets) and a shorter ring of lo buffers
+  // [A lo | B lo] written by the converters: more raw bytes in flight per SM than
+  // raw + lo stages side by side (6 / 4 / 2 raw stages at BN = 64 / 128 / 256)
+  static constexpr int RAW_BYTES = A_BYTES + B_BYTES;
+  static constexpr int NSL = 2;
+  static constexpr int STAGES = (192 * 1024 - NSL * RAW_BYTES) / RAW_BYTES;
   static constexpr int EPI_WARPS = BN >= 256 ? 8 : 4;
   static constexpr int COLS_PER_EPI = BN >= 256 ? 128 : BN;
   static constexpr int THREADS = 32 * (2 + CONV_WARPS + EPI_WARPS);
@@ -58,7 +62,7 @@ struct Cfg {
   static constexpr int GATHER_WARP0 = 2 + CONV_WARPS + EPI_WARPS;  // gather variant: 4 more
   static constexpr int GATHER_LAG = STAGES - 2;  // cp.async stages in flight per gatherer
   static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers
-  static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024 + 256;
+  static constexpr size_t SMEM = size_t(STAGES + NSL) * RAW_BYTES + 1024 + 256;
   // kind::tf32: F32 accumulate (bit 4), A/B TF32 (bits 7, 10), both K-major, N >> 3, M >> 4
   static constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) |
                                     (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
@@ -186,10 +190,11 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS + (GATHER ? 128 : 0), 1)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t *conv = full + C::STAGES;       // lo tiles written
-  uint64_t *empty = conv + C::STAGES;      // stage consumed by the MMAs
-  uint64_t *tmem_full = empty + C::STAGES; // [2]
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (C::STAGES + C::NSL) * C::RAW_BYTES);
+  uint64_t *empty = full + C::STAGES;      // raw stage consumed by the MMAs
+  uint64_t *conv = empty + C::STAGES;      // [NSL] lo buffer written
+  uint64_t *lo_free = conv + C::NSL;       // [NSL] lo buffer consumed by the MMAs
+  uint64_t *tmem_full = lo_free + C::NSL;  // [2]
   uint64_t *tmem_empty = tmem_full + 2;    // [2]
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
 
@@ -207,8 +212,11 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS + (GATHER ? 128 : 0), 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], GATHER ? 1 + 128 : 1);  // TMA (+ the 128 A gatherers)
-      mbar_init(&conv[s], C::CONV_WARPS);
       mbar_init(&empty[s], 1);
+    }
+    for (int l = 0; l < C::NSL; ++l) {
+      mbar_init(&conv[l], C::CONV_WARPS);
+      mbar_init(&lo_free[l], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tmem_full[b], 1);
@@ -226,8 +234,9 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS + (GATHER ? 128 : 0), 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // stage s: [A raw | A lo | B raw | B lo]
-  auto stage = [&](int s) { return smem + s * C::STAGE_BYTES; };
+  // raw stage s: [A raw | B raw]; lo buffer l: [A lo | B lo] (same offsets)
+  auto stage = [&](int s) { return smem + s * C::RAW_BYTES; };
+  auto lobuf = [&](int l) { return smem + (C::STAGES + l) * C::RAW_BYTES; };
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer: raw tiles only ----
@@ -237,7 +246,7 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS + (GATHER ? 128 : 0), 1)
         unsigned char *st = stage(s);
         mbar_expect_tx(&full[s], (GATHER ? 0 : A_BYTES) + C::B_BYTES);
         if (!GATHER) tma_load_3d(st, &map_a, &full[s], kb * BK, m_tile * BM, za);
-        tma_load_3d(st + 2 * A_BYTES, &map_b, &full[s], kb * BK, n_tile * BN, zb);
+        tma_load_3d(st + A_BYTES, &map_b, &full[s], kb * BK, n_tile * BN, zb);
       }
     }
   } else if (warp == 1) {
@@ -251,12 +260,13 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS + (GATHER ? 128 : 0), 1)
           mbar_wait(&tmem_empty[buf], ((chunk >> 1) & 1) ^ 1);
           tc_fence_after();
         }
-        mbar_wait(&conv[s], (kb / C::STAGES) & 1);
+        const int l = kb % C::NSL;
+        mbar_wait(&conv[l], (kb / C::NSL) & 1);
         tc_fence_after();
-        const uint32_t st = smem_u32(stage(s));
-        const uint64_t ahi = smem_desc_sw128(st), alo = smem_desc_sw128(st + A_BYTES);
-        const uint64_t bhi = smem_desc_sw128(st + 2 * A_BYTES);
-        const uint64_t blo = smem_desc_sw128(st + 2 * A_BYTES + C::B_BYTES);
+        const uint32_t st = smem_u32(stage(s)), lt = smem_u32(lobuf(l));
+        const uint64_t ahi = smem_desc_sw128(st), alo = smem_desc_sw128(lt);
+        const uint64_t bhi = smem_desc_sw128(st + A_BYTES);
+        const uint64_t blo = smem_desc_sw128(lt + A_BYTES);
         const uint32_t tacc = tmem_base + uint32_t(buf * BN);
 #pragma unroll
         for (int k = 0; k < BK / UK; ++k) {
@@ -267,6 +277,7 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS + (GATHER ? 128 : 0), 1)
           umma_tf32(tacc, alo + koff, bhi + koff, C::IDESC, 1u);
         }
         umma_commit(&empty[s]);
+        umma_commit(&lo_free[l]);
         if (chunk_last) umma_commit(&tmem_full[buf]);
       }
     }
@@ -275,21 +286,20 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS + (GATHER ? 128 : 0), 1)
     const int ct = threadIdx.x - 64;  // 0 .. 32 * CONV_WARPS - 1
     constexpr int NV = (A_BYTES + C::B_BYTES) / 16;  // float4 per stage
     for (int kb = 0; kb < args.k_blocks; ++kb) {
-      const int s = kb % C::STAGES;
+      const int s = kb % C::STAGES, l = kb % C::NSL;
       mbar_wait(&full[s], (kb / C::STAGES) & 1);
-      unsigned char *st = stage(s);
+      mbar_wait(&lo_free[l], ((kb / C::NSL) & 1) ^ 1);
+      const unsigned char *st = stage(s);
+      unsigned char *lt = lobuf(l);
 #pragma unroll 4
       for (int i = ct; i < NV; i += 32 * C::CONV_WARPS) {
-        const int a_part = i < A_BYTES / 16;
-        const int off = a_part ? i * 16 : 2 * A_BYTES + (i * 16 - A_BYTES);
-        const int lo_off = a_part ? A_BYTES : C::B_BYTES;
-        const float4 x = *reinterpret_cast<const float4 *>(st + off);
-        *reinterpret_cast<float4 *>(st + off + lo_off) = tf32_lo(x);
+        const float4 x = *reinterpret_cast<const float4 *>(st + i * 16);
+        *reinterpret_cast<float4 *>(lt + i * 16) = tf32_lo(x);
       }
       // generic-proxy smem writes -> visible to the tensor core (async proxy)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&conv[s]);
+      if (lane == 0) mbar_arrive(&conv[l]);
     }
   } else if (GATHER && warp >= C::GATHER_WARP0) {
     // ---- A gatherers: row g of the tile, its 16 complex k of each stage, 8-byte
