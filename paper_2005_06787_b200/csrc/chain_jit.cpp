@@ -336,7 +336,8 @@ std::string emit(const ChainGeom &g, const ChainTables &kt, int id, bool exact, 
   // (STN_DEBUG chain_wreg=V, at most V values) -- the registers they take cost more than
   // the loads they save (measured on B200: cfg5 86.9 -> 106.3 ms per slice with 16)
   const char *wo = debug_opt("chain_wreg");
-  const int wreg_max = wo ? std::atoi(wo) : 0;
+  const char *we = debug_opt("chain_wreg_exp");  // experiments: expansion kernels only
+  const int wreg_max = wo ? std::atoi(wo) : (we && g.n_exp > 0) ? std::atoi(we) : 0;
   std::vector<char> hoist(size_t(g.n_stages), 0);
   {
     int used = 0;
