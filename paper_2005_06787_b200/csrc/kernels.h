@@ -33,6 +33,16 @@ namespace stn {
 //   graphs=0               no CUDA graphs: every batch launched kernel by kernel
 //   chain=0, chain_min_bits=B, chain_jit=0   fused stem chains off / only with
 //                          intermediates >= 2^B elements (default 24) / table kernel only
+//   chain_single=0|2       one-stage chains off / for every step that fits (measurements)
+//   chain_multi_log=L      tile limit of multi-stage chains (default 6 = 64 values)
+//   chain_exp=0, chain_exp_pen=0   no expansion rows / no penalty for large expanded operands
+//   chain_vec=0|1|2        widest tile access (1, 2, 4 complex); chain_swap=0: no exchanges
+//   chain_pf_log=L         software-pipeline rows of tiles up to 2^L values
+//   chain_ffma2=1, chain_wreg=V, chain_wreg_exp=V, chain_alt=1   stage-math experiments
+//   chain_why=S, chain_src  why segments from step S do not fit / NVRTC source in the log
+//   side=1                 small steps on a second stream of the lane
+//   gemm_mc=1|2|4, gemm_gm=G   wide GEMM cluster size / raster band height in m tiles
+//   tcf_gather=0           fused-split GEMM reads a permuted A from a permuted copy
 //   bitperm_legacy         legacy bit-permute kernel for the selftest
 //   sweep_only=..., no_bulk, tma_lag=N, tma_nsr=N, perm_tb=N   pipeline experiments
 //   tcf=0|1|2              fused-split GEMM never / for 2N <= 128 (default) / always
