@@ -1258,7 +1258,9 @@ bool build_chain(const stn_plan &P, const std::vector<int> &steps, stn_plan::Swe
   // L2, and a W column selected by its row). Specialised kernel only.
   std::vector<int> exp_lines, exp_w;
   const char *eo = stn::debug_opt("chain_exp");  // STN_DEBUG chain_exp=0: no expansion rows
-  if (jit && ns >= 2 && !(eo && std::atoi(eo) == 0)) {
+  const char *es1 = stn::debug_opt("chain_exp_single");  // experiments: one-stage expansion
+  const bool exp_single = es1 && std::atoi(es1) != 0;
+  if (jit && (ns >= 2 || exp_single) && !(eo && std::atoi(eo) == 0)) {
     StageLines &z = sl[0];
     std::vector<int> keep, keep_w;
     for (size_t j = 0; j < z.n.size(); ++j)
@@ -1776,9 +1778,12 @@ void plan_chains(stn_plan &P, bool jit) {
         // multiply-adds per column element moved (cfg2 494 / 536, K x N = 1024 against
         // 80 / 64 elements: 3.6 -> 2.7 TB/s; cfg5 1365, 512 against 48, is kept)
         const int64_t K = int64_t(1) << sp.kbits.size(), N = int64_t(1) << sp.nbits.size();
+        const char *es1 = stn::debug_opt("chain_exp_single");
+        const bool exp_single = es1 && std::atoi(es1) != 0 && sp.nbits.size() >= 3;
         const bool coalesced = e_in[size_t(a)][size_t(a)] > 0.99 &&
-                               (e_out[size_t(a)][size_t(a)] > 0.99 || 4 * sp.osize <= xsize) &&
-                               K * N <= 12 * (K + N);
+                               (e_out[size_t(a)][size_t(a)] > 0.99 || 4 * sp.osize <= xsize ||
+                                exp_single) &&
+                               (K * N <= 12 * (K + N) || exp_single);
         g = (single_all || (slow && coalesced)) ? 0.5 * double(sp.lsize + sp.rsize + sp.osize)
                                                 : 0.0;
         return sp.osize >= (int64_t(1) << min_bits) ? g - 1.0 : -1.0;
