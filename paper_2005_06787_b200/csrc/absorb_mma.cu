@@ -56,7 +56,8 @@ __device__ __forceinline__ float tf32_hi(float x) {
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
-// Bounded wait: a barrier that never completes traps (~2 s) instead of hanging the GPU.
+// Bounded wait: a barrier that never completes traps (~60 s of clock: far beyond any
+// legitimate wait, preemption included) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t done = 0;
@@ -71,7 +72,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
     if (done) return;
     if (iter == 0) start = clock64();
-    if ((iter & 1023) == 1023 && clock64() - start > (4ll << 30)) __trap();
+    if ((iter & 1023) == 1023 && clock64() - start > (120ll << 30)) __trap();
   }
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {

@@ -63,7 +63,8 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                : "memory");
 }
 
-// Bounded wait: a barrier that never completes traps (~2 s) instead of hanging the GPU.
+// Bounded wait: a barrier that never completes traps (~60 s of clock: far beyond any
+// legitimate wait, preemption included) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t done = 0;
@@ -78,7 +79,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
     if (done) return;
     if (iter == 0) start = clock64();
-    if ((iter & 1023) == 1023 && clock64() - start > (4ll << 30)) __trap();
+    if ((iter & 1023) == 1023 && clock64() - start > (120ll << 30)) __trap();
   }
 }
 

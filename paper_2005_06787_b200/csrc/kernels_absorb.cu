@@ -262,7 +262,7 @@ __device__ __forceinline__ void ab3_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
     if (done) return;
     if (iter == 0) start = clock64();
-    if ((iter & 1023) == 1023 && clock64() - start > (4ll << 30)) __trap();
+    if ((iter & 1023) == 1023 && clock64() - start > (120ll << 30)) __trap();
   }
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {

@@ -24,7 +24,8 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// Bounded wait: a barrier that never completes traps (~2 s) instead of hanging the GPU.
+// Bounded wait: a barrier that never completes traps (~60 s of clock: far beyond any
+// legitimate wait, preemption included) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t done = 0;
@@ -46,7 +47,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "r"(addr), "r"(parity)
         : "memory");
     if (done) return;
-    if ((iter & 1023) == 0 && clock64() - start > (4ll << 30)) __trap();
+    if ((iter & 1023) == 0 && clock64() - start > (120ll << 30)) __trap();
   }
 }
 
