@@ -502,6 +502,10 @@ def main():
                 "ms_per_step": statistics.median(e2e_ms) if e2e_ms else None,
                 "api": "stn_run_slices_host (C ABI, pinned host digits in, amplitudes out)",
                 "one_time_setup_s": setup_s,
+                "allocation": "the plan's lane arenas and workspaces are allocated by its first "
+                              "batches (warm-up) and reused; the timed region allocates "
+                              "nothing (the executor's block cache only serves plans that are "
+                              "destroyed and created again)",
                 "setup": "plan upload (vertex tensors H2D) + branch-cache build, once per "
                          "process like the reference worker's ensure_plan (queue.hpp:204-219)"},
         "gpu_launches": int(launches * args.steps),
