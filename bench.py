@@ -253,8 +253,14 @@ def run_reference_arm(args):
         calib = {"step_ms": ms, "source": f"of a full slice on this host in this run "
                                           f"({sum(ms) / 1e3:.1f} s)"}
         walls.append(time.perf_counter() - t0)
-        if args.steps + args.warmup <= 1:
+        # the calibration slice is the first warm-up step, or the first timed one
+        if args.warmup == 0:
             vals.append(1e3 / sum(ms))
+        cb = {"value": 1e3 / sum(ms), "unit": "slices/s", "cores": threads, "kind": "port",
+              "sample": (f"one full slice through the oracle port of the reference executor "
+                         f"(oracle/stn_oracle.c gemm_lean), {threads} threads splitting each "
+                         f"step, {sum(ms) / 1e3:.1f} s"),
+              "slice_seconds": sum(ms) / 1e3}
     for i in range(args.warmup + args.steps - (1 if cfg == "cfg5" else 0)):
         t0 = time.perf_counter()
         if cfg == "cfg5":
