@@ -309,15 +309,23 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS + (GATHER ? 128 : 0), 1)
     const float2 *xrow = args.x + int64_t(za) * args.x_bs + args.moff_hi[m_tile] + args.moff_lo[g];
     const uint32_t row_base = uint32_t(g) * 128u;
     const int sw = g & 7;
+    // k offsets are linear in the bits of k: koff(16 kb + j) = koff(16 kb) + koff(j), so a
+    // stage needs one table load (its base) and 16 register-held low offsets
+    int64_t klo[BK / 2];
+#pragma unroll
+    for (int j = 0; j < BK / 2; ++j) klo[j] = __ldg(args.koff + j);
+    int64_t khi = __ldg(args.koff);
     for (int kb = 0; kb < args.k_blocks + C::GATHER_LAG; ++kb) {
       if (kb < args.k_blocks) {
         const int s = kb % C::STAGES;
+        const int64_t kbase = khi;
+        if (kb + 1 < args.k_blocks) khi = __ldg(args.koff + int64_t(kb + 1) * (BK / 2));
         mbar_wait(&empty[s], ((kb / C::STAGES) & 1) ^ 1);
         const uint32_t dst = smem_u32(stage(s)) + row_base;
-        const int64_t *ko = args.koff + int64_t(kb) * (BK / 2);
+        const float2 *src = xrow + kbase;
 #pragma unroll
         for (int j = 0; j < BK / 2; ++j)
-          cp_async8(dst + uint32_t((((j >> 1) ^ sw) << 4) + ((j & 1) << 3)), xrow + __ldg(ko + j));
+          cp_async8(dst + uint32_t((((j >> 1) ^ sw) << 4) + ((j & 1) << 3)), src + klo[j]);
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
       const int done = kb - C::GATHER_LAG;  // this thread's copies of stage `done` landed
