@@ -278,14 +278,23 @@ def test_53_qubit_fast_vs_reference_double(name):
         asg, vals, _, _, _ = read_ref(name, "single")
     except FileNotFoundError:
         pytest.skip("no reference values recorded")
+    try:
+        dasg = set(int(x) for x in read_ref(name, "double")[0])
+    except FileNotFoundError:
+        pytest.skip("no reference double values recorded")
     plan = load(name, "single", "fast")
     cache = build_branch_cache(plan)
+    checked = 0
     for a, want in zip(asg, vals):
+        if int(a) not in dasg:  # slices recorded in single precision only
+            continue
         truth, tol = truth_and_tolerance(name, int(a), want)
         err = rel_err(run_subtask(plan, int(a), cache).value, truth)
         print(f"{name} slice {int(a)}: fast err {err:.2e}, reference single err "
               f"{rel_err(want, truth):.2e}, tol {tol:.2e}")
         assert err <= tol, (name, int(a), err, tol)
+        checked += 1
+    assert checked > 0
 
 
 @pytest.mark.parametrize("name", ["cfg1_grid4x5_m14", "cfg2_grid5x6_m16"])
