@@ -65,6 +65,8 @@ slice0 cfg3_syc53_m12 double
 slice0 cfg4_syc53_m14 single
 slice0 cfg4_syc53_m14 double
 # cfg5: the reference cannot hold its 2^33 stems (Engine::gemm keeps 4 of them, 256 GiB)
-# and refuses every assignment (subtasks() overflows, scheme.hpp:33-37); its slices 0
-# and 1 come from the oracle port on a GPU box host: scripts/cfg5_parity.py ->
-# port_single.bin (tests/test_gpu_parity.py::test_cfg5_2pow33_stems_against_the_oracle_port)
+# and refuses every assignment (subtasks() overflows, scheme.hpp:33-37); its slices 0, 1
+# and 11400714819323198485 (digits across 64 of its 85 sliced edges) come from the oracle
+# port on a GPU box host: CFG5_SLICES=... scripts/cfg5_parity.py, then
+# scripts/port_golden.py -> port_single.bin
+# (tests/test_gpu_parity.py::test_cfg5_2pow33_stems_against_the_oracle_port)
