@@ -389,7 +389,7 @@ def _read_port(name):
     from golden_io import GOLDEN
     b = open(os.path.join(GOLDEN, name, "port_single.bin"), "rb").read()
     n, oe = struct.unpack_from("<QQ", b, 0)
-    asg = np.frombuffer(b, np.uint64, n, 16).astype(np.int64)
+    asg = [int(x) for x in np.frombuffer(b, np.uint64, n, 16)]  # up to 2^64 - 1
     vals = np.frombuffer(b, np.complex128, n * oe, 16 + 8 * n).reshape(n, oe)
     return asg, vals
 
