@@ -60,7 +60,8 @@ circuit cfg3_syc53_m12   sycamore53 12 6 29 none 0
 circuit cfg4_syc53_m14   sycamore53 14 6 29 none 0
 circuit cfg5_syc53_m20   sycamore53 20 6 33 none 0
 # 53-qubit slices: slice 0 through the reference executor itself
-slice0 cfg3_syc53_m12 single
+# cfg3 single: slices 0 and 16383 (the last: every sliced digit at its maximum)
+"$TOOL" golden "$HERE/cfg3_syc53_m12" --precision single --slices 0,16383 --scheme 0 --uncached 0 --threads 2 > /dev/null
 slice0 cfg3_syc53_m12 double
 slice0 cfg4_syc53_m14 single
 slice0 cfg4_syc53_m14 double
