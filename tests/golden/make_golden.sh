@@ -63,7 +63,8 @@ circuit cfg5_syc53_m20   sycamore53 20 6 33 none 0
 # cfg3 single: slices 0 and 16383 (the last: every sliced digit at its maximum)
 "$TOOL" golden "$HERE/cfg3_syc53_m12" --precision single --slices 0,16383 --scheme 0 --uncached 0 --threads 2 > /dev/null
 slice0 cfg3_syc53_m12 double
-slice0 cfg4_syc53_m14 single
+# cfg4 single: slices 0 and 524287 (the last)
+"$TOOL" golden "$HERE/cfg4_syc53_m14" --precision single --slices 0,524287 --scheme 0 --uncached 0 --threads 2 > /dev/null
 slice0 cfg4_syc53_m14 double
 # cfg5: the reference cannot hold its 2^33 stems (Engine::gemm keeps 4 of them, 256 GiB)
 # and refuses every assignment (subtasks() overflows, scheme.hpp:33-37); its slices 0, 1
